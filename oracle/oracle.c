@@ -1,0 +1,190 @@
+/*
+ * oracle.c — TEST INFRASTRUCTURE ONLY.  Plain, slow, obviously-correct CPU
+ * reference for the recursive-Cholesky hot path of arXiv:1602.06763
+ * ("Recursive Algorithms for Dense Linear Algebra: The ReLAPACK Collection").
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_1602_06763_b200/) never links, loads or calls it, and this file
+ * shares no code, header, table or helper with the CUDA path.
+ *
+ * Citation convention: P:a-b = /root/reference/PAPER.md lines a-b,
+ * S:a-b = /root/reference/SPEC.md lines a-b.
+ *
+ * What the method computes: the recursive xpotrf (P:275-307,
+ * P:366-370 "dpotrf2 ... used in LAPACK's blocked dpotrf as a replacement for
+ * the unblocked dpotf2") reaches exactly, up to rounding order, the unique
+ * lower-triangular L with positive diagonal such that A = L*L^T.  The oracle
+ * is therefore NOT recursive: it is that definition written out as the
+ * textbook left-looking ("jki") triple loop of the unblocked dpotf2
+ * (post-condition and NotPositiveDefinite error).
+ *
+ * Arithmetic rules (reading R7): IEEE double, one subtraction per
+ * term in ascending k, true division by the pivot, correctly rounded sqrt;
+ * built with -O3 -ffp-contract=off and no fast-math, so no FMA contraction.
+ * The per-element operation order does not depend on the OpenMP thread count
+ * (threads split the row index i only), so results are bitwise deterministic.
+ *
+ * The BLAS-3 steps of the recursion (TRSM, SYRK, GEMM; "two BLAS-3
+ * invocations surrounded by two recursive applications") are also given here
+ * by their plain definitions so the CUDA update kernels can be
+ * checked in isolation.
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+
+/* Element (i, j) of the factor being computed.  uplo = 'L': column-major
+ * lower triangle, a(i,j) = A[i + j*lda].  uplo = 'U': A = U^T U with U = L^T,
+ * so L(i,j) = U(j,i) = A[j + i*lda] (reading R5). */
+#define LIDX(i, j) (lower ? ((size_t)(i) + (size_t)(j) * (size_t)lda) \
+                          : ((size_t)(j) + (size_t)(i) * (size_t)lda))
+
+/*
+ * oracle_dpotrf — unblocked Cholesky, left-looking column form.
+ *   for j = 0..n-1:
+ *     for k = 0..j-1: for i = j..n-1: a(i,j) = a(i,j) - a(i,k)*a(j,k)
+ *     d = a(j,j); if !(d > 0) return j+1            (info, 1-based)
+ *     a(j,j) = sqrt(d); for i = j+1..n-1: a(i,j) = a(i,j) / a(j,j)
+ * Returns LAPACK info: 0 success, -1 bad uplo, -2 n<0, -4 lda<max(1,n),
+ * k>0 leading minor of order k not positive definite (factorization stops;
+ * columns < k-1 are final).  Only the uplo triangle is read or written.
+ */
+int oracle_dpotrf(char uplo, int n, double* A, int lda) {
+  int lower;
+  if (uplo == 'L' || uplo == 'l') lower = 1;
+  else if (uplo == 'U' || uplo == 'u') lower = 0;
+  else return -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  for (int j = 0; j < n; ++j) {
+    /* a(j:n-1, j) -= sum_{k<j} a(j:n-1, k) * a(j, k), ascending k per element.
+     * Threads own disjoint row ranges; each element sees the same k order. */
+#pragma omp parallel for schedule(static) if (n - j > 512)
+    for (int i = j; i < n; ++i) {
+      double s = A[LIDX(i, j)];
+      for (int k = 0; k < j; ++k) {
+        double p = A[LIDX(i, k)] * A[LIDX(j, k)];
+        s = s - p;
+      }
+      A[LIDX(i, j)] = s;
+    }
+    double d = A[LIDX(j, j)];
+    if (!(d > 0.0)) return j + 1; /* catches d <= 0, -0.0 and NaN */
+    d = sqrt(d);
+    A[LIDX(j, j)] = d;
+    for (int i = j + 1; i < n; ++i) A[LIDX(i, j)] = A[LIDX(i, j)] / d;
+  }
+  return 0;
+}
+
+/*
+ * oracle_dpotrf_cols — the same loop stopped after the first `ncols` columns
+ * (a bounded sample of one factorization, used only by bench.py's
+ * cpu_baseline).  Returns info as oracle_dpotrf, restricted to those columns.
+ */
+int oracle_dpotrf_cols(char uplo, int n, double* A, int lda, int ncols) {
+  int lower = (uplo == 'L' || uplo == 'l');
+  if (!lower && !(uplo == 'U' || uplo == 'u')) return -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  if (ncols > n) ncols = n;
+  for (int j = 0; j < ncols; ++j) {
+#pragma omp parallel for schedule(static) if (n - j > 512)
+    for (int i = j; i < n; ++i) {
+      double s = A[LIDX(i, j)];
+      for (int k = 0; k < j; ++k) {
+        double p = A[LIDX(i, k)] * A[LIDX(j, k)];
+        s = s - p;
+      }
+      A[LIDX(i, j)] = s;
+    }
+    double d = A[LIDX(j, j)];
+    if (!(d > 0.0)) return j + 1;
+    d = sqrt(d);
+    A[LIDX(j, j)] = d;
+    for (int i = j + 1; i < n; ++i) A[LIDX(i, j)] = A[LIDX(i, j)] / d;
+  }
+  return 0;
+}
+
+/*
+ * oracle_dpotrf_batched — oracle_dpotrf applied to each matrix of a batch
+ * (CFG[4]); matrices are independent, so threads split the batch.
+ * A_all holds matrix b at offset[b] with leading dimension lda[b].
+ */
+void oracle_dpotrf_batched(char uplo, int batch, const int* n, double* A_all,
+                           const int64_t* offset, const int* lda, int* info) {
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int b = 0; b < batch; ++b)
+    info[b] = oracle_dpotrf(uplo, n[b], A_all + offset[b], lda[b]);
+}
+
+/*
+ * oracle_dtrsm_rlt — TRSM Right/Lower/Trans/NonUnit, the solve
+ * step of the recursion: B (m x k, col-major, ldb) := B * L^{-T}, i.e. solve
+ * X * L^T = B for X with L (k x k lower, ldl).  Row r of X:
+ *   x(r,j) = (b(r,j) - sum_{p<j} x(r,p) * L(j,p)) / L(j,j), ascending p.
+ */
+void oracle_dtrsm_rlt(int m, int k, const double* L, int ldl, double* B, int ldb) {
+#pragma omp parallel for schedule(static) if (m > 256)
+  for (int r = 0; r < m; ++r) {
+    for (int j = 0; j < k; ++j) {
+      double s = B[(size_t)r + (size_t)j * ldb];
+      for (int p = 0; p < j; ++p) {
+        double q = B[(size_t)r + (size_t)p * ldb] * L[(size_t)j + (size_t)p * ldl];
+        s = s - q;
+      }
+      B[(size_t)r + (size_t)j * ldb] = s / L[(size_t)j + (size_t)j * ldl];
+    }
+  }
+}
+
+/*
+ * oracle_dsyrk_ln — SYRK Lower/NoTrans with alpha = -1, beta = 1,
+ * the trailing update of the recursion: C (n x n, ldc) lower triangle only
+ *   c(i,j) = c(i,j) - sum_{p<k} a(i,p) * a(j,p),  i >= j, ascending p.
+ * The strict upper triangle of C is never read or written.
+ */
+void oracle_dsyrk_ln(int n, int k, const double* A, int lda, double* C, int ldc) {
+#pragma omp parallel for schedule(dynamic, 16) if (n > 128)
+  for (int j = 0; j < n; ++j) {
+    for (int i = j; i < n; ++i) {
+      double s = C[(size_t)i + (size_t)j * ldc];
+      for (int p = 0; p < k; ++p) {
+        double q = A[(size_t)i + (size_t)p * lda] * A[(size_t)j + (size_t)p * lda];
+        s = s - q;
+      }
+      C[(size_t)i + (size_t)j * ldc] = s;
+    }
+  }
+}
+
+/*
+ * oracle_dgemm_nt — GEMM NoTrans/Trans with alpha = -1, beta = 1,
+ * the update inside the recursive TRSM: C (m x n) -= A (m x k) * B (n x k)^T.
+ */
+void oracle_dgemm_nt(int m, int n, int k, const double* A, int lda, const double* B,
+                     int ldb, double* C, int ldc) {
+#pragma omp parallel for schedule(static) if (n > 64)
+  for (int j = 0; j < n; ++j) {
+    for (int i = 0; i < m; ++i) {
+      double s = C[(size_t)i + (size_t)j * ldc];
+      for (int p = 0; p < k; ++p) {
+        double q = A[(size_t)i + (size_t)p * lda] * B[(size_t)j + (size_t)p * ldb];
+        s = s - q;
+      }
+      C[(size_t)i + (size_t)j * ldc] = s;
+    }
+  }
+}
+
+/* Number of OpenMP threads the oracle will use (for bench reporting). */
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
