@@ -1,0 +1,181 @@
+/*
+ * relapack.h — C ABI of the B200-native recursive FP64 Cholesky (xpotrf) of
+ * Peise & Bientinesi, "Recursive Algorithms for Dense Linear Algebra: The
+ * ReLAPACK Collection", arXiv:1602.06763.
+ *
+ * Citation convention: P:a-b = PAPER.md lines a-b, S:a-b =
+ * SPEC.md lines a-b of the reference text.
+ *
+ * The operation.  For a symmetric positive definite A (only the `uplo`
+ * triangle is read) compute, in place, the lower factor L with A = L L^T
+ * (uplo 'L') or the upper factor U with A = U^T U (uplo 'U', U = L^T).  The
+ * method is the recursive algorithm of P:275-307 (blocked -> recursive with
+ * b = n/2, quadrant split, "two BLAS-3 invocations surrounded by two
+ * recursive applications", crossover size c) applied to Cholesky as in
+ * LAPACK's dpotrf2 and SPEC rec_potrf:
+ *     potrf(A11); A21 := A21 L11^{-T} (recursive TRSM);
+ *     A22 := A22 - A21 A21^T (SYRK, lower triangle only); potrf(A22).
+ * The call mirrors LAPACK xPOTRF(UPLO, N, A, LDA, INFO) as north_star asks.
+ *
+ * Storage.  Column-major FP64, element (i, j) at A[i + j*lda].
+ * Only the `uplo` triangle (diagonal included) is read or written; the
+ * opposite strict triangle and rows n..lda-1 are bitwise untouched.
+ *
+ * Errors (LAPACK info convention; no printing, no abort):
+ *   info = 0    success
+ *   info = -1   uplo not one of 'L','l','U','u'
+ *   info = -2   n < 0
+ *   info = -3   A is NULL while n > 0 (extension)
+ *   info = -4   lda < max(1, n)
+ *   info = k>0  the leading minor of order k is not positive definite: the
+ *               k-th pivot d satisfied !(d > 0) (d <= 0 or NaN).  The
+ *               factorization stops there (dpotrf2 semantics):
+ *               the leading (k-1) x (k-1) block holds the factor of the
+ *               leading minor of order k-1; every later update is skipped and
+ *               the rest of the triangle is unspecified.
+ *   info <= -1000  CUDA runtime failure; relapack_last_error() describes it.
+ *
+ * Threading / streams.  Entry points are reentrant; the per-device plan
+ * cache (captured CUDA graphs) is mutex-guarded.  Work is ordered on the
+ * stream set by relapack_set_stream (default: the legacy default stream) or
+ * passed explicitly to the _async / _batched variants.
+ *
+ * Ownership.  The caller owns every matrix buffer; the library never frees
+ * caller memory.  The library owns per-device workspace (info scalars,
+ * staging buffer for host matrices, captured graphs, TMA descriptors),
+ * released by relapack_finalize().
+ */
+#ifndef RELAPACK_B200_H_
+#define RELAPACK_B200_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RELAPACK_API __attribute__((visibility("default")))
+#else
+#define RELAPACK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* A CUDA stream handle (cudaStream_t) passed as an opaque pointer so that this
+ * header does not require the CUDA headers.  NULL = legacy default stream. */
+typedef void* relapack_stream_t;
+
+/*
+ * relapack_dpotrf — synchronous LAPACK-style entry point (north_star; P:226-229
+ * "conforming to the established interfaces").
+ *   uplo  in   'L' or 'U' (case-insensitive)
+ *   n     in   order of A, n >= 0
+ *   A     in/out  DEVICE or HOST pointer to the lda x n column-major matrix.
+ *               Device memory (cudaMalloc / PyTorch storage) is factored in
+ *               place.  Host memory (pageable or pinned) is staged through a
+ *               library-owned device buffer: the uplo triangle is copied in,
+ *               factored on the GPU, and only the uplo triangle is copied back.
+ *   lda   in   leading dimension, lda >= max(1, n)
+ *   info  out  host int, see "Errors" above
+ * Returns after the factorization completed (stream synchronised).
+ */
+RELAPACK_API void relapack_dpotrf(const char* uplo, const int* n, double* A, const int* lda, int* info);
+
+/*
+ * relapack_dpotrf_async — device-only, stream-ordered variant.
+ *   A       DEVICE pointer (lda x n, column-major)
+ *   d_info  DEVICE int written with the info value when the work completes
+ *   stream  CUDA stream the work is ordered on
+ * Returns the argument-check code immediately (0, -1, -2, -3, -4 as above, or
+ * <= -1000 for a CUDA error during enqueue); the numerical info (k > 0) is
+ * only known through d_info after the stream has progressed.
+ */
+RELAPACK_API int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int* d_info, relapack_stream_t stream);
+
+/*
+ * relapack_dpotrf_batched — independent small factorizations (CFG[4]), one
+ * kernel launch.  Matrix b is d_A[b] (DEVICE pointer, d_lda[b] x d_n[b]).
+ *   d_n, d_A, d_lda, d_info  DEVICE arrays of length `batch`
+ * Per matrix: info as relapack_dpotrf; n outside [0, RELAPACK_BATCH_NMAX] sets
+ * that matrix's info to -2, lda < max(1, n) sets -4; such matrices are skipped.
+ * Returns 0, -1 (bad uplo), -2 (batch < 0) or <= -1000 (CUDA error).
+ */
+#define RELAPACK_BATCH_NMAX 64
+RELAPACK_API int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const* d_A, const int* d_lda,
+                            int* d_info, relapack_stream_t stream);
+
+/* ---- multi-GPU: one process per GPU, NCCL over NVLink ---- */
+typedef struct relapack_comm relapack_comm_t;
+
+/* Writes a 128-byte NCCL unique id (rank 0 creates it; broadcast it with any
+ * transport, e.g. torch.distributed).  Returns 0 or <= -1000. */
+RELAPACK_API int relapack_comm_unique_id(char uid[128]);
+
+/* Creates a communicator over `nranks` processes; `device` is this rank's GPU.
+ * Returns 0 or <= -1000 (NCCL or CUDA failure; see relapack_last_error). */
+RELAPACK_API int relapack_comm_init(relapack_comm_t** comm, const char uid[128], int nranks, int rank, int device);
+RELAPACK_API void relapack_comm_destroy(relapack_comm_t* comm);
+
+/*
+ * relapack_dpotrf_dist — SPMD distributed factorization of one matrix.
+ * Every rank passes a full-size DEVICE buffer A (lda x n, identical input on
+ * every rank).  The top recursion levels' trailing updates (TRSM rows and
+ * SYRK row-blocks of the L-view; for uplo 'U' these are memory block-columns)
+ * are sharded block-cyclically over the ranks with block `nb`; the freshly
+ * solved panel blocks are all-gathered with NCCL.  Below `dist_min` the
+ * recursion runs redundantly on every rank.  On return every rank holds the
+ * full factor and the same info.
+ *   nb        row-block size of the block-cyclic distribution (>= 64, mult. of 64)
+ *   dist_min  subproblem order below which the recursion is replicated
+ */
+RELAPACK_API void relapack_dpotrf_dist(const char* uplo, const int* n, double* A, const int* lda, int nb, int dist_min,
+                          relapack_comm_t* comm, int* info);
+
+/* ---- configuration, introspection, teardown ---- */
+RELAPACK_API void relapack_set_stream(relapack_stream_t stream);
+RELAPACK_API const char* relapack_last_error(void);
+RELAPACK_API void relapack_finalize(void);
+
+/* Tuning knobs (also read from env RELAPACK_CROSSOVER / RELAPACK_SPLIT_TILE /
+ * RELAPACK_GRAPH).  crossover c: base case when n <= c (16 <= c <= 64);
+ * split tile T: n1 = T*floor(n/(2T)) (T in {8,16,32,64,128}); graphs 0/1.
+ * Return 0, or -1 on an out-of-range value. */
+RELAPACK_API int relapack_set_crossover(int c);
+RELAPACK_API int relapack_set_split_tile(int t);
+RELAPACK_API int relapack_set_graphs(int enabled);
+RELAPACK_API int relapack_get_crossover(void);
+
+/*
+ * Host-only plan introspection (no GPU needed):
+ *   relapack_split_point(n, align) -> n1 of the split rule
+ *     n1 = align*floor(n/(2*align)) if that is >= align, else floor(n/2).
+ *   relapack_plan_ledger(n, c, T, levels, flops_by_level, count)
+ *     leading-term FLOP ledger of the recursion tree the driver would build:
+ *     flops_by_level[l] (l = 0..levels-1) = TRSM (m*k^2) + SYRK (n2^2*k) flops
+ *     issued at recursion level l+1, flops_by_level[levels] = base-case flops
+ *     (sum c_b^3/3); *count = number of kernel launches in the plan.
+ *     Returns the recursion depth, or -1 on bad arguments.
+ */
+RELAPACK_API int relapack_split_point(int n, int align);
+RELAPACK_API int relapack_plan_ledger(int n, int c, int T, int levels, double* flops_by_level, int* count);
+
+/*
+ * Per-kernel-class profiling (bench.py's roofline line).  While enabled, the
+ * executor launches the plan without a CUDA graph and brackets every kernel
+ * with CUDA events on the launch stream.  relapack_profile_read(kind, ...)
+ * synchronises those events and returns, for kind 0 = base potf2, 1 = base
+ * TRSM, 2 = GEMM update, 3 = SYRK update: the summed kernel time (ms), the
+ * summed leading-term algorithmic flops and the number of launches recorded
+ * since the last relapack_profile_reset().  Return 0, or -1 on a bad kind.
+ */
+RELAPACK_API int relapack_profile_enable(int on);
+RELAPACK_API int relapack_profile_read(int kind, double* ms_total, double* flops_total, int* launches);
+RELAPACK_API void relapack_profile_reset(void);
+
+/* Library version string (build id). */
+RELAPACK_API const char* relapack_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RELAPACK_B200_H_ */

@@ -1,0 +1,241 @@
+"""paper_1602_06763_b200 — B200-native recursive FP64 Cholesky (xpotrf) of
+arXiv:1602.06763 (ReLAPACK), behind the C ABI in include/relapack.h.
+
+This module is argument marshalling only: every step of the factorization
+runs in the sm_100a kernels of librelapack_b200.so.  There is no CPU
+fallback: if the library is missing or a CUDA device is absent the calls
+raise.
+
+    import torch, paper_1602_06763_b200 as rl
+    A = ...                            # (n, n) float64 CUDA tensor, column-major view (strides (1, lda))
+    info = rl.dpotrf(A, "L")           # A's lower triangle := L, A = L L^T
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+__all__ = [
+    "lib",
+    "library_path",
+    "dpotrf",
+    "dpotrf_raw",
+    "dpotrf_async",
+    "dpotrf_batched",
+    "split_point",
+    "profile_enable",
+    "profile_reset",
+    "profile_read",
+    "plan_ledger",
+    "set_crossover",
+    "set_split_tile",
+    "set_graphs",
+    "get_crossover",
+    "last_error",
+    "finalize",
+    "colmajor",
+    "declared_symbols",
+    "RelapackError",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "librelapack_b200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "relapack.h")
+_lib = None
+
+
+class RelapackError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load the in-tree CUDA library (built by __graft_entry__.build()); fail loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(library_path):
+            raise RelapackError(
+                f"{library_path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = ctypes.CDLL(library_path)
+        c_int, c_char, c_void_p, c_double = ctypes.c_int, ctypes.c_char, ctypes.c_void_p, ctypes.c_double
+        ip = ctypes.POINTER(c_int)
+        L.relapack_dpotrf.argtypes = [ctypes.c_char_p, ip, c_void_p, ip, ip]
+        L.relapack_dpotrf.restype = None
+        L.relapack_dpotrf_async.argtypes = [c_char, c_int, c_void_p, c_int, c_void_p, c_void_p]
+        L.relapack_dpotrf_async.restype = c_int
+        L.relapack_dpotrf_batched.argtypes = [c_char, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.relapack_dpotrf_batched.restype = c_int
+        L.relapack_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.relapack_comm_unique_id.restype = c_int
+        L.relapack_comm_init.argtypes = [ctypes.POINTER(c_void_p), ctypes.c_char_p, c_int, c_int, c_int]
+        L.relapack_comm_init.restype = c_int
+        L.relapack_comm_destroy.argtypes = [c_void_p]
+        L.relapack_comm_destroy.restype = None
+        L.relapack_dpotrf_dist.argtypes = [ctypes.c_char_p, ip, c_void_p, ip, c_int, c_int, c_void_p, ip]
+        L.relapack_dpotrf_dist.restype = None
+        L.relapack_set_stream.argtypes = [c_void_p]
+        L.relapack_set_stream.restype = None
+        L.relapack_last_error.restype = ctypes.c_char_p
+        L.relapack_finalize.restype = None
+        for f in ("relapack_set_crossover", "relapack_set_split_tile", "relapack_set_graphs"):
+            getattr(L, f).argtypes = [c_int]
+            getattr(L, f).restype = c_int
+        L.relapack_get_crossover.restype = c_int
+        L.relapack_split_point.argtypes = [c_int, c_int]
+        L.relapack_split_point.restype = c_int
+        L.relapack_plan_ledger.argtypes = [c_int, c_int, c_int, c_int, ctypes.POINTER(c_double), ip]
+        L.relapack_plan_ledger.restype = c_int
+        L.relapack_version.restype = ctypes.c_char_p
+        L.relapack_profile_enable.argtypes = [c_int]
+        L.relapack_profile_enable.restype = c_int
+        L.relapack_profile_read.argtypes = [c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_double), ip]
+        L.relapack_profile_read.restype = c_int
+        L.relapack_profile_reset.restype = None
+        _lib = L
+    return _lib
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/relapack.h (the C ABI)."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(relapack_[a-z_0-9]+)\s*\(", src)))
+
+
+def last_error() -> str:
+    return (lib().relapack_last_error() or b"").decode()
+
+
+def finalize() -> None:
+    lib().relapack_finalize()
+
+
+def set_crossover(c: int) -> None:
+    if lib().relapack_set_crossover(int(c)) != 0:
+        raise ValueError(f"crossover {c} out of range [16, 128]")
+
+
+def set_split_tile(t: int) -> None:
+    if lib().relapack_set_split_tile(int(t)) != 0:
+        raise ValueError(f"split tile {t} not in (8, 16, 32, 64, 128)")
+
+
+def set_graphs(enabled: bool) -> None:
+    lib().relapack_set_graphs(1 if enabled else 0)
+
+
+def get_crossover() -> int:
+    return lib().relapack_get_crossover()
+
+
+PROFILE_KINDS = {"potf2": 0, "trsm": 1, "gemm": 2, "syrk": 3}
+
+
+def profile_enable(on: bool) -> None:
+    lib().relapack_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    lib().relapack_profile_reset()
+
+
+def profile_read(kind: str):
+    """(ms_total, flops_total, launches) recorded for one kernel class since the last reset."""
+    ms, fl, cnt = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_int(0)
+    if lib().relapack_profile_read(PROFILE_KINDS[kind], ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(cnt)) != 0:
+        raise ValueError(kind)
+    return ms.value, fl.value, cnt.value
+
+
+def split_point(n: int, align: int) -> int:
+    return lib().relapack_split_point(int(n), int(align))
+
+
+def plan_ledger(n: int, c: int, T: int, levels: int):
+    """(depth, flops_by_level[levels], base_flops, launches) of the plan the driver builds (host only)."""
+    buf = (ctypes.c_double * (levels + 1))()
+    cnt = ctypes.c_int(0)
+    depth = lib().relapack_plan_ledger(int(n), int(c), int(T), int(levels), buf, ctypes.byref(cnt))
+    if depth < 0:
+        raise ValueError("bad plan arguments")
+    vals = list(buf)
+    return depth, vals[:levels], vals[levels], cnt.value
+
+
+def colmajor(X):
+    """A column-major (strides (1, n)) float64 copy of a 2-D torch tensor."""
+    return X.t().contiguous().t()
+
+
+def _matrix_args(A):
+    """(pointer, n, lda) of a 2-D float64 torch tensor with unit row stride."""
+    import torch
+
+    if not isinstance(A, torch.Tensor) or A.dtype != torch.float64 or A.dim() != 2:
+        raise TypeError("A must be a 2-D float64 torch tensor")
+    n = A.shape[1]
+    if A.shape[0] != n:
+        raise ValueError("A must be square")
+    if n > 1 and A.stride(0) != 1:
+        raise ValueError("A must be column-major (stride(0) == 1); use colmajor(A)")
+    lda = max(1, A.stride(1) if n > 1 else max(1, A.shape[0]))
+    return A.data_ptr(), n, lda
+
+
+def dpotrf(A, uplo: str = "L", stream=None) -> int:
+    """Factor A in place (LAPACK dpotrf semantics, include/relapack.h); returns info.
+
+    A: (n, n) float64 torch tensor, column-major (strides (1, lda)), on a CUDA
+    device (factored in place on the GPU) or on the CPU (pinned or pageable:
+    the uplo triangle is staged through the GPU and copied back).
+    """
+    import torch
+
+    ptr, n, lda = _matrix_args(A)
+    if A.is_cuda:
+        st = stream if stream is not None else torch.cuda.current_stream(A.device)
+        lib().relapack_set_stream(ctypes.c_void_p(st.cuda_stream))
+    else:
+        st = stream if stream is not None else (torch.cuda.current_stream() if torch.cuda.is_available() else None)
+        lib().relapack_set_stream(ctypes.c_void_p(st.cuda_stream if st is not None else 0))
+    info = ctypes.c_int(0)
+    lib().relapack_dpotrf(uplo.encode(), ctypes.byref(ctypes.c_int(n)), ctypes.c_void_p(ptr),
+                          ctypes.byref(ctypes.c_int(lda)), ctypes.byref(info))
+    if info.value <= -1000:
+        raise RelapackError(f"relapack_dpotrf failed: {last_error()}")
+    return info.value
+
+
+def dpotrf_raw(uplo: str, n: int, ptr: int, lda: int) -> int:
+    """Direct C-ABI call with raw arguments (argument-checking tests)."""
+    info = ctypes.c_int(0)
+    lib().relapack_dpotrf(uplo.encode(), ctypes.byref(ctypes.c_int(n)), ctypes.c_void_p(ptr),
+                          ctypes.byref(ctypes.c_int(lda)), ctypes.byref(info))
+    return info.value
+
+
+def dpotrf_async(A, d_info, uplo: str = "L", stream=None) -> int:
+    """Stream-ordered factorization; d_info: int32 CUDA tensor (1 element). Returns the argument code."""
+    import torch
+
+    ptr, n, lda = _matrix_args(A)
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    r = lib().relapack_dpotrf_async(uplo.encode(), n, ctypes.c_void_p(ptr), lda, ctypes.c_void_p(d_info.data_ptr()),
+                                    ctypes.c_void_p(st.cuda_stream))
+    if r <= -1000:
+        raise RelapackError(f"relapack_dpotrf_async failed: {last_error()}")
+    return r
+
+
+def dpotrf_batched(ns, ptrs, ldas, infos, uplo: str = "L", stream=None) -> int:
+    """Batched small factorizations; ns/ldas/infos int32 and ptrs int64 CUDA tensors of length batch."""
+    import torch
+
+    st = stream if stream is not None else torch.cuda.current_stream(ns.device)
+    r = lib().relapack_dpotrf_batched(uplo.encode(), int(ns.numel()), ctypes.c_void_p(ns.data_ptr()),
+                                      ctypes.c_void_p(ptrs.data_ptr()), ctypes.c_void_p(ldas.data_ptr()),
+                                      ctypes.c_void_p(infos.data_ptr()), ctypes.c_void_p(st.cuda_stream))
+    if r <= -1000:
+        raise RelapackError(f"relapack_dpotrf_batched failed: {last_error()}")
+    return r

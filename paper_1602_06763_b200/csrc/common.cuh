@@ -1,0 +1,91 @@
+// common.cuh — sm_100a building blocks shared by the relapack kernels:
+// L-view addressing, mbarrier / TMA (cp.async.bulk.tensor) wrappers and the
+// FP64 tensor-core MMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4).
+//
+// FP64 on sm_100a (measured, tools/microbench/fp64_peak.cu, profiles/): there is
+// no tcgen05 kind::f64; DMMA.8x8x4 reaches 37.0 TFLOP/s vs 34.2 for DFMA
+// register chains at 1965 MHz, so every dense update runs on DMMA.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace relapack {
+
+// Layout of the L-view: the algorithm always works on
+// the lower factor L.  uplo 'L': L(i,j) = A[i + j*ld] (kLayoutN, rows
+// contiguous).  uplo 'U': A = U^T U, L = U^T, so L(i,j) = A[j + i*ld]
+// (kLayoutT, columns contiguous).
+enum : int { kLayoutN = 0, kLayoutT = 1 };
+
+__host__ __device__ __forceinline__ int64_t lv_off(int layout, int64_t i, int64_t j, int64_t ld) {
+  return layout == kLayoutN ? i + j * ld : j + i * ld;
+}
+
+// ----------------------------------------------------------------------------
+// mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// TMA: 2-D tiled bulk tensor load global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// FP64 tensor core: D(8x8) += A(8x4) * B(4x8).  Lane l: a = A[l/4][l%4],
+// b = B[l%4][l/4], d = {D[l/4][2(l%4)], D[l/4][2(l%4)+1]}.
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int ld_info(const int* d_info) {
+  return *reinterpret_cast<const volatile int*>(d_info);
+}
+
+}  // namespace relapack

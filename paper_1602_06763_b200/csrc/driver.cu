@@ -1,0 +1,557 @@
+// driver.cu — C-ABI entry points (include/relapack.h) and the host recursion
+// driver: validates LAPACK arguments, maps uplo 'U' onto the L-view (layout
+// T), turns the plan (plan.h) into kernel launches, captures them once per
+// (device, A, n, lda, uplo, info pointer, knobs) into a CUDA graph and replays
+// it.  Every step of the factorization runs in the kernels of update.cu,
+// potf2.cu and trsm.cu; there is no CPU fallback.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/relapack.h"
+#include "common.cuh"
+#include "driver_internal.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace relapack {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+static std::mutex g_err_mu;
+static std::string g_last_error_global;
+
+void set_error(const std::string& s) {
+  g_last_error = s;
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_last_error_global = s;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return -1000 - (int)e;
+}
+
+// ------------------------------------------------------------------ knobs
+static std::atomic<int> g_crossover{-1}, g_split_tile{-1}, g_graphs{-1};
+static std::atomic<uintptr_t> g_stream{0};
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return atoi(v);
+}
+
+PlanParams current_params() {
+  PlanParams p;
+  int c = g_crossover.load();
+  if (c < 0) c = env_int("RELAPACK_CROSSOVER", 64);
+  int t = g_split_tile.load();
+  if (t < 0) t = env_int("RELAPACK_SPLIT_TILE", 64);
+  if (c < 16 || c > kPotf2Max) c = 64;
+  if (t != 8 && t != 16 && t != 32 && t != 64 && t != 128) t = 64;
+  p.crossover = c;
+  p.split_tile = t;
+  p.trsm_base = kTrsmMax;
+  return p;
+}
+
+static bool graphs_enabled() {
+  int g = g_graphs.load();
+  if (g < 0) g = env_int("RELAPACK_GRAPH", 1);
+  return g != 0;
+}
+
+// ------------------------------------------------------------------ per-device state
+struct Plan {
+  std::vector<PlanOp> ops;
+  std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
+  cudaGraphExec_t exec = nullptr;
+  ~Plan() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, int, int, int>;
+
+struct DeviceState {
+  std::mutex mu;          // guards the plan cache
+  std::mutex sync_mu;     // serialises the synchronous entry point (shared info / staging)
+  bool configured = false;
+  cudaStream_t capture = nullptr;
+  int* d_info = nullptr;  // library-owned info scalar for the synchronous API
+  int* h_info = nullptr;  // pinned
+  double* stage = nullptr;  // staging buffer for host matrices
+  size_t stage_elems = 0;
+  std::list<std::pair<PlanKey, std::unique_ptr<Plan>>> lru;
+  std::map<PlanKey, std::list<std::pair<PlanKey, std::unique_ptr<Plan>>>::iterator> index;
+};
+
+static std::mutex g_dev_mu;
+static DeviceState* g_dev[kMaxDevices] = {};
+
+DeviceState* device_state(int dev) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_dev[dev]) g_dev[dev] = new DeviceState();
+  return g_dev[dev];
+}
+
+static cudaError_t ensure_device(DeviceState* ds) {
+  if (ds->configured) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&ds->capture, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&ds->d_info, sizeof(int))) != cudaSuccess) return e;
+  if ((e = cudaHostAlloc(&ds->h_info, sizeof(int), cudaHostAllocDefault)) != cudaSuccess) return e;
+  if ((e = configure_kernels()) != cudaSuccess) return e;
+  ds->configured = true;
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ executor
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
+cudaError_t launch_set_int(int* p, int v, cudaStream_t st) {
+  k_set_int<<<1, 1, 0, st>>>(p, v);
+  return cudaGetLastError();
+}
+
+static void fill_update(UpdateOp& u, const PlanOp& op, double* A, int64_t ld, int layout, const int* d_info) {
+  UpdateArgs& a = u.args;
+  memset(&a, 0, sizeof(a));
+  a.C = A + lv_off(layout, op.c_i, op.c_j, ld);
+  a.ldc = ld;
+  a.layout = layout;
+  a.d_info = d_info;
+  a.K = op.k;
+  if (op.kind == OP_SYRK) {
+    a.M = a.N = op.n;
+    a.tri = 1;
+  } else {
+    a.M = op.m;
+    a.N = op.n;
+    a.tri = 0;
+  }
+  u.tile = update_tile_for(a.M, a.N, a.tri);
+  a.tiles_m = (a.M + u.tile - 1) / u.tile;
+  a.A = A + lv_off(layout, op.a_i, op.a_j, ld);
+  a.lda = ld;
+  a.B = A + lv_off(layout, op.b_i, op.b_j, ld);
+  a.ldb = ld;
+  u.use_tma = make_operand_map(&u.tmA, a.A, ld, layout, a.M, a.K, u.tile) &&
+              make_operand_map(&u.tmB, a.B, ld, layout, a.N, a.K, u.tile);
+}
+
+// ------------------------------------------------------------------ profiling
+struct ProfRecord {
+  cudaEvent_t start, stop;
+  int kind;
+  double flops;
+};
+static std::mutex g_prof_mu;
+static std::atomic<int> g_prof_on{0};
+static std::vector<ProfRecord> g_prof;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, int* d_info, cudaStream_t st,
+                           bool profile) {
+  cudaError_t e = launch_set_int(d_info, 0, st);
+  if (e != cudaSuccess) return e;
+  std::unique_lock<std::mutex> plk(g_prof_mu, std::defer_lock);
+  if (profile) plk.lock();
+  for (size_t i = 0; i < pl.ops.size(); ++i) {
+    const PlanOp& op = pl.ops[i];
+    ProfRecord rec{};
+    if (profile) {
+      rec.start = prof_event();
+      rec.stop = prof_event();
+      rec.kind = (int)op.kind;
+      rec.flops = op.flops;
+      cudaEventRecord(rec.start, st);
+    }
+    switch (op.kind) {
+      case OP_POTF2:
+        e = launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
+        break;
+      case OP_TRSM:
+        e = launch_trsm_base(A + lv_off(layout, op.a_i, op.a_j, ld), ld, A + lv_off(layout, op.c_i, op.c_j, ld), ld,
+                             layout, op.m, op.k, d_info, st);
+        break;
+      case OP_GEMM:
+      case OP_SYRK:
+        e = launch_update(pl.upd[i], st);
+        break;
+    }
+    if (e != cudaSuccess) return e;
+    if (profile) {
+      cudaEventRecord(rec.stop, st);
+      g_prof.push_back(rec);
+    }
+  }
+  return cudaSuccess;
+}
+
+// Enqueue the factorization of the device matrix A (already validated).
+int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st) {
+  DeviceState* ds = device_state(dev);
+  cudaError_t e;
+  PlanParams pp = current_params();
+  const bool profile = g_prof_on.load() != 0;
+  const bool use_graph = graphs_enabled() && !profile;
+  std::lock_guard<std::mutex> lk(ds->mu);
+  if ((e = ensure_device(ds)) != cudaSuccess) return cuda_fail(e, "device setup");
+  PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
+              pp.split_tile, use_graph ? 1 : 0};
+  Plan* plan = nullptr;
+  auto it = ds->index.find(key);
+  if (it != ds->index.end()) {
+    ds->lru.splice(ds->lru.begin(), ds->lru, it->second);
+    plan = it->second->second.get();
+  } else {
+    auto p = std::make_unique<Plan>();
+    build_potrf_plan(n, pp, p->ops);
+    p->upd.resize(p->ops.size());
+    for (size_t i = 0; i < p->ops.size(); ++i)
+      if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
+    if (use_graph) {
+      cudaGraph_t g = nullptr;
+      if ((e = cudaStreamBeginCapture(ds->capture, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        return cuda_fail(e, "begin capture");
+      cudaError_t er = run_ops(*p, A, ld, layout, d_info, ds->capture, false);
+      e = cudaStreamEndCapture(ds->capture, &g);
+      if (er != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return cuda_fail(er, "launch during capture");
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "end capture");
+      e = cudaGraphInstantiate(&p->exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+    }
+    ds->lru.emplace_front(key, std::move(p));
+    ds->index[key] = ds->lru.begin();
+    plan = ds->lru.front().second.get();
+    while (ds->lru.size() > 32) {
+      ds->index.erase(ds->lru.back().first);
+      ds->lru.pop_back();
+    }
+  }
+  if (use_graph)
+    e = cudaGraphLaunch(plan->exec, st);
+  else
+    e = run_ops(*plan, A, ld, layout, d_info, st, profile);
+  if (e != cudaSuccess) return cuda_fail(e, "launch");
+  return 0;
+}
+
+static int check_args(char uplo, int n, const void* A, int lda, int* layout) {
+  if (uplo == 'L' || uplo == 'l')
+    *layout = kLayoutN;
+  else if (uplo == 'U' || uplo == 'u')
+    *layout = kLayoutT;
+  else
+    return -1;
+  if (n < 0) return -2;
+  if (n > 0 && A == nullptr) return -3;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  return 0;
+}
+
+static bool is_device_pointer(const void* p, int* dev) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    *dev = at.device;
+    return true;
+  }
+  return false;
+}
+
+// Copy the uplo triangle between a host matrix (ld_h) and a device matrix
+// (ld_d) in column panels: only the triangle (plus the diagonal blocks of the
+// panels) crosses PCIe.
+static cudaError_t copy_triangle(double* dst, int64_t ld_dst, const double* src, int64_t ld_src, int n, int layout,
+                                 cudaMemcpyKind kind, cudaStream_t st) {
+  const int w = 256;
+  for (int j0 = 0; j0 < n; j0 += w) {
+    const int jw = (n - j0 < w) ? n - j0 : w;
+    int64_t r0, rows;
+    if (layout == kLayoutN) {  // lower: memory column j holds rows j..n-1
+      r0 = j0;
+      rows = n - j0;
+    } else {  // upper: memory column j holds rows 0..j
+      r0 = 0;
+      rows = j0 + jw;
+    }
+    cudaError_t e = cudaMemcpy2DAsync(dst + r0 + (int64_t)j0 * ld_dst, ld_dst * sizeof(double),
+                                      src + r0 + (int64_t)j0 * ld_src, ld_src * sizeof(double),
+                                      rows * sizeof(double), jw, kind, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace relapack
+
+using namespace relapack;
+
+// =================================================================== C ABI
+extern "C" {
+
+void relapack_dpotrf(const char* uplo, const int* n_, double* A, const int* lda_, int* info) {
+  if (!uplo || !n_ || !lda_ || !info) {
+    if (info) *info = -1;
+    return;
+  }
+  const int n = *n_, lda = *lda_;
+  int layout = 0;
+  int ai = check_args(*uplo, n, A, lda, &layout);
+  if (ai != 0) {
+    *info = ai;
+    return;
+  }
+  if (n == 0) {
+    *info = 0;
+    return;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(g_stream.load());
+  int dev = 0;
+  const bool on_device = is_device_pointer(A, &dev);
+  cudaError_t e;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (on_device && dev != cur) {
+    if ((e = cudaSetDevice(dev)) != cudaSuccess) {
+      *info = cuda_fail(e, "set device");
+      return;
+    }
+  }
+  if (!on_device) dev = cur;
+  DeviceState* ds = device_state(dev);
+  std::lock_guard<std::mutex> sync_lk(ds->sync_mu);
+  {
+    std::lock_guard<std::mutex> lk(ds->mu);
+    if ((e = ensure_device(ds)) != cudaSuccess) {
+      *info = cuda_fail(e, "device setup");
+      return;
+    }
+  }
+  double* dA = A;
+  int64_t ld = lda;
+  if (!on_device) {
+    // stage through a library-owned device buffer (ld rounded up for TMA alignment)
+    const int64_t ldd = ((int64_t)n + 31) / 32 * 32;
+    const size_t need = (size_t)ldd * n;
+    if (ds->stage_elems < need) {
+      if (ds->stage) cudaFree(ds->stage);
+      ds->stage = nullptr;
+      ds->stage_elems = 0;
+      if ((e = cudaMalloc(&ds->stage, need * sizeof(double))) != cudaSuccess) {
+        *info = cuda_fail(e, "staging buffer");
+        return;
+      }
+      ds->stage_elems = need;
+    }
+    dA = ds->stage;
+    ld = ldd;
+    if ((e = copy_triangle(dA, ld, A, lda, n, layout, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+      *info = cuda_fail(e, "H2D");
+      return;
+    }
+  }
+  int r = enqueue_potrf(dev, dA, n, ld, layout, ds->d_info, st);
+  if (r != 0) {
+    *info = r;
+    return;
+  }
+  if (!on_device) {
+    if ((e = copy_triangle(A, lda, dA, ld, n, layout, cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
+      *info = cuda_fail(e, "D2H");
+      return;
+    }
+  }
+  if ((e = cudaMemcpyAsync(ds->h_info, ds->d_info, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    *info = cuda_fail(e, "sync");
+    return;
+  }
+  *info = *ds->h_info;
+  if (on_device && dev != cur) cudaSetDevice(cur);
+}
+
+int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int* d_info, relapack_stream_t stream) {
+  int layout = 0;
+  int ai = check_args(uplo, n, A, lda, &layout);
+  if (ai != 0) return ai;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  if (n > 0 && !is_device_pointer(A, &dev)) {
+    set_error("relapack_dpotrf_async: A is not a device pointer");
+    return -3;
+  }
+  if (d_info == nullptr) return -5;
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(d_info, 0, sizeof(int), st);
+    return e == cudaSuccess ? 0 : cuda_fail(e, "memset info");
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (dev != cur) cudaSetDevice(dev);
+  int r = enqueue_potrf(dev, A, n, lda, layout, d_info, st);
+  if (dev != cur) cudaSetDevice(cur);
+  return r;
+}
+
+int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const* d_A, const int* d_lda, int* d_info,
+                            relapack_stream_t stream) {
+  int layout;
+  if (uplo == 'L' || uplo == 'l')
+    layout = kLayoutN;
+  else if (uplo == 'U' || uplo == 'u')
+    layout = kLayoutT;
+  else
+    return -1;
+  if (batch < 0) return -2;
+  if (batch == 0) return 0;
+  cudaError_t e = launch_potf2_batched(layout, batch, d_n, d_A, d_lda, d_info, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "batched launch");
+}
+
+void relapack_set_stream(relapack_stream_t stream) { g_stream.store(reinterpret_cast<uintptr_t>(stream)); }
+
+const char* relapack_last_error(void) {
+  if (!g_last_error.empty()) return g_last_error.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  static thread_local std::string copy;
+  copy = g_last_error_global;
+  return copy.c_str();
+}
+
+void relapack_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < kMaxDevices; ++d) {
+    DeviceState* ds = g_dev[d];
+    if (!ds) continue;
+    cudaSetDevice(d);
+    {
+      std::lock_guard<std::mutex> l2(ds->mu);
+      ds->index.clear();
+      ds->lru.clear();
+      if (ds->stage) cudaFree(ds->stage);
+      if (ds->d_info) cudaFree(ds->d_info);
+      if (ds->h_info) cudaFreeHost(ds->h_info);
+      if (ds->capture) cudaStreamDestroy(ds->capture);
+    }
+    delete ds;
+    g_dev[d] = nullptr;
+  }
+  cudaSetDevice(cur);
+}
+
+int relapack_set_crossover(int c) {
+  if (c < 16 || c > kPotf2Max) return -1;  // base case held in one SM's shared memory
+  g_crossover.store(c);
+  return 0;
+}
+
+int relapack_set_split_tile(int t) {
+  if (t != 8 && t != 16 && t != 32 && t != 64 && t != 128) return -1;
+  g_split_tile.store(t);
+  return 0;
+}
+
+int relapack_set_graphs(int enabled) {
+  g_graphs.store(enabled ? 1 : 0);
+  return 0;
+}
+
+int relapack_get_crossover(void) { return current_params().crossover; }
+
+int relapack_split_point(int n, int align) { return split_point(n, align); }
+
+int relapack_plan_ledger(int n, int c, int T, int levels, double* flops_by_level, int* count) {
+  if (n < 0 || c < 1 || T < 1 || levels < 0 || (levels > 0 && !flops_by_level)) return -1;
+  PlanParams p;
+  p.crossover = c;
+  p.split_tile = T;
+  p.trsm_base = kTrsmMax;
+  std::vector<PlanOp> ops;
+  build_potrf_plan(n, p, ops);
+  if (flops_by_level)
+    for (int l = 0; l <= levels; ++l) flops_by_level[l] = 0.0;
+  for (const PlanOp& op : ops) {
+    if (!flops_by_level) break;
+    if (op.kind == OP_POTF2)
+      flops_by_level[levels] += op.flops;
+    else if (op.level >= 1 && op.level <= levels)
+      flops_by_level[op.level - 1] += op.flops;
+  }
+  if (count) *count = (int)ops.size();
+  return plan_depth(n, p);
+}
+
+int relapack_profile_enable(int on) {
+  g_prof_on.store(on ? 1 : 0);
+  return 0;
+}
+
+int relapack_profile_read(int kind, double* ms_total, double* flops_total, int* launches) {
+  if (kind < 0 || kind > 3) return -1;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double ms = 0.0, fl = 0.0;
+  int cnt = 0;
+  for (const ProfRecord& r : g_prof) {
+    if (r.kind != kind) continue;
+    cudaEventSynchronize(r.stop);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.start, r.stop);
+    ms += t;
+    fl += r.flops;
+    ++cnt;
+  }
+  if (ms_total) *ms_total = ms;
+  if (flops_total) *flops_total = fl;
+  if (launches) *launches = cnt;
+  return 0;
+}
+
+void relapack_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (ProfRecord& r : g_prof) {
+    cudaEventSynchronize(r.stop);
+    g_prof_pool.push_back(r.start);
+    g_prof_pool.push_back(r.stop);
+  }
+  g_prof.clear();
+}
+
+const char* relapack_version(void) { return "relapack-b200 0.1 (sm_100a, DMMA FP64)"; }
+
+}  // extern "C"

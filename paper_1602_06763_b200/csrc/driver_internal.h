@@ -1,0 +1,15 @@
+// driver_internal.h — shared between driver.cu and dist.cu (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "plan.h"
+
+namespace relapack {
+void set_error(const std::string& s);
+int cuda_fail(cudaError_t e, const char* what);
+PlanParams current_params();
+// Enqueue the whole recursive factorization of the device L-view matrix A on st.
+int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st);
+}  // namespace relapack

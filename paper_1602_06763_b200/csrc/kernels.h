@@ -1,0 +1,68 @@
+// kernels.h — launch interface between the host recursion driver (driver.cu)
+// and the sm_100a kernels.  Internal to the library (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace relapack {
+
+constexpr int kMaxDevices = 64;
+constexpr int RELAPACK_BATCH_NMAX_ = 64;  // == RELAPACK_BATCH_NMAX in include/relapack.h
+
+// ---- K3/K4 update (update.cu) ----
+struct UpdateArgs {
+  double* C;          // L-view block (M x N) to update
+  int64_t ldc;
+  int M, N, K;
+  int layout;         // kLayoutN / kLayoutT
+  int tri;            // 1: SYRK, lower-triangular tiles only (M == N, A == B)
+  int tiles_m;
+  const int* d_info;  // device info flag: kernels return immediately if != 0
+  const double* A;    // fallback (non-TMA) operand pointers, L-view blocks
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+};
+
+struct UpdateOp {
+  UpdateArgs args;
+  CUtensorMap tmA, tmB;
+  bool use_tma;
+  int tile;  // CTA tile (128 or 64), see update_tile_for
+};
+
+cudaError_t launch_update(const UpdateOp& op, cudaStream_t st);
+bool make_operand_map(CUtensorMap* map, const double* base, int64_t ld, int layout, int rows, int K, int box_rows);
+int update_tile_for(int M, int N, int tri);
+
+// ---- K1 base-case potf2 (potf2.cu) ----
+// Factor the n x n L-view block at A (n <= kPotf2Max) in shared memory; on a
+// non-positive pivot at local column j write d_info = info_base + j + 1.
+constexpr int kPotf2Max = 64;
+cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, int info_base, cudaStream_t st);
+
+// ---- K5 base TRSM (trsm.cu): B(m x t) := B * L^{-T}, L t x t lower (t <= kTrsmMax)
+constexpr int kTrsmMax = 64;
+cudaError_t launch_trsm_base(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
+                             const int* d_info, cudaStream_t st);
+
+// ---- K2 batched potf2 (batched.cu)
+cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* const* d_A, const int* d_lda,
+                                 int* d_info, cudaStream_t st);
+
+// ---- one-time per-device kernel attributes (max dynamic smem); call before graph capture
+cudaError_t configure_update();
+cudaError_t configure_potf2();
+cudaError_t configure_trsm();
+inline cudaError_t configure_kernels() {
+  cudaError_t e = configure_update();
+  if (e == cudaSuccess) e = configure_potf2();
+  if (e == cudaSuccess) e = configure_trsm();
+  return e;
+}
+
+// ---- misc device helpers (driver.cu)
+cudaError_t launch_set_int(int* p, int v, cudaStream_t st);
+
+}  // namespace relapack

@@ -1,0 +1,340 @@
+// update.cu — K3/K4: the BLAS-3 trailing updates of the recursion on the FP64
+// tensor cores of sm_100a.
+//
+//   C(M x N) -= A(M x K) * B(N x K)^T            (GEMM inside the recursive TRSM:
+//                                                 B2 -= X1 Lb^T)
+//   C(N x N) -= A A^T, lower triangle only        (SYRK A22 -= L21 L21^T, §8a a4;
+//                                                 S:192-200)
+//
+// All operands are L-view blocks (common.cuh): layout N (uplo 'L', rows
+// contiguous) or T (uplo 'U', the k index contiguous).  Design:
+//  * CTA tile TBM x TBM (128, or 64 for problems too small to fill 148 SMs),
+//    K-step 16, 4-stage shared-memory ring filled by TMA (cp.async.bulk.tensor,
+//    128B swizzle) issued by thread 0, mbarrier full/empty handshake.
+//  * FP64 tensor cores: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4); each warp owns
+//    a 64x32 (TBM 128, 8 warps) or 32x32 (TBM 64, 4 warps) register tile.
+//  * the k -> MMA-k mapping differs per layout so both fragment reads are
+//    shared-memory bank-conflict free (2 wavefronts per 256 B fragment).
+//  * SYRK enumerates only lower-triangular tiles; diagonal tiles mask i < j,
+//    so the other triangle is never read or written.
+//  * epilogue staged through shared memory: coalesced C -= tile along the
+//    contiguous global dimension with 16 loads in flight per thread.
+//  * non-TMA fallback (odd ld or a base not 16-B aligned): the CTA fills the
+//    same swizzled layout with plain loads, one stage at a time.
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace relapack {
+
+namespace {
+
+constexpr int BK = 16, STAGES = 4;
+
+template <int TBM>
+struct Cfg {
+  static constexpr int NUM_WARPS = TBM == 128 ? 8 : 4;  // 8 warps keep 2 per SMSP (255-reg budget)
+  static constexpr int THREADS = NUM_WARPS * 32;
+  static constexpr int WTM = TBM == 128 ? 64 : 32;      // warp tile rows
+  static constexpr int WTN = 32;                        // warp tile cols
+  static constexpr int MT = WTM / 8, NT = WTN / 8;      // DMMA tiles per warp
+  static constexpr int WGM = TBM / WTM;                 // warps along M (2)
+  static constexpr int TILE_BYTES = TBM * BK * 8;
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+  static constexpr int CPAD = TBM + 1;                  // epilogue staging stride (odd)
+  static constexpr int PIPE_BYTES =
+      STAGES * STAGE_BYTES > TBM * CPAD * 8 ? STAGES * STAGE_BYTES : TBM * CPAD * 8;
+  static constexpr int SMEM_BYTES = PIPE_BYTES + 1024 /*align*/ + 2 * STAGES * 8 /*barriers*/;
+};
+
+// Byte offset of operand element (row r, k) inside a TBM x 16 stage tile.
+// Layout N: TBM/16 TMA boxes of [16 k][16 rows] (128 B rows, 128B swizzle:
+// 16-B chunk index XOR (k mod 8)).  Layout T: one box of [TBM rows][16 k].
+template <int LAYOUT>
+__device__ __forceinline__ uint32_t tile_off(int r, int k) {
+  if (LAYOUT == kLayoutN)
+    return (uint32_t)((r >> 4) * 2048 + k * 128 + ((((r & 15) >> 1) ^ (k & 7)) << 4) + ((r & 1) << 3));
+  else
+    return (uint32_t)(r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3));
+}
+
+// MMA k-slot (t = lane%4) of k-step s -> tile k.  Chosen per layout so that
+// the 32 lanes of a fragment read hit every bank exactly twice.
+template <int LAYOUT>
+__device__ __forceinline__ int kmap(int s, int t) {
+  return LAYOUT == kLayoutN ? 4 * t + s : 4 * s + t;
+}
+
+__device__ __forceinline__ void tri_index(int x, int& ti, int& tj) {
+  int r = (int)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
+  while ((r + 1) * (r + 2) / 2 <= x) ++r;
+  while (r * (r + 1) / 2 > x) --r;
+  ti = r;
+  tj = x - r * (r + 1) / 2;
+}
+
+// Fallback loader: the whole CTA fills one stage with plain loads (zero outside).
+template <int LAYOUT, int TBM>
+__device__ __forceinline__ void fill_tile_ldg(uint8_t* tile, const double* X, int64_t ldx, int rows, int r0, int K,
+                                              int k0) {
+  for (int e = threadIdx.x; e < TBM * BK; e += Cfg<TBM>::THREADS) {
+    int r, k;
+    if (LAYOUT == kLayoutN) {
+      r = e % TBM;
+      k = e / TBM;
+    } else {
+      k = e % BK;
+      r = e / BK;
+    }
+    double v = 0.0;
+    if (r0 + r < rows && k0 + k < K) v = X[lv_off(LAYOUT, r0 + r, k0 + k, ldx)];
+    *reinterpret_cast<double*>(tile + tile_off<LAYOUT>(r, k)) = v;
+  }
+}
+
+template <int LAYOUT, int TBM>
+__device__ __forceinline__ void issue_stage(uint8_t* smem, uint64_t* full, const CUtensorMap* tmA,
+                                            const CUtensorMap* tmB, int kt, int m0, int n0) {
+  using C = Cfg<TBM>;
+  const int s = kt % STAGES;
+  uint8_t* sa = smem + s * C::STAGE_BYTES;
+  uint8_t* sb = sa + C::TILE_BYTES;
+  mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+  if (LAYOUT == kLayoutN) {
+#pragma unroll
+    for (int b = 0; b < TBM / 16; ++b) {
+      tma_load_2d(sa + b * 2048, tmA, m0 + 16 * b, kt * BK, &full[s]);
+      tma_load_2d(sb + b * 2048, tmB, n0 + 16 * b, kt * BK, &full[s]);
+    }
+  } else {
+    tma_load_2d(sa, tmA, kt * BK, m0, &full[s]);
+    tma_load_2d(sb, tmB, kt * BK, n0, &full[s]);
+  }
+}
+
+// One BK-deep step of the warp tile: 4 MMA k-steps x (MT x NT) DMMA.8x8x4.
+template <int LAYOUT, int TBM>
+__device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::NT][2], const uint8_t* sa,
+                                          const uint8_t* sb, int wm, int wn, int g, int t) {
+  using C = Cfg<TBM>;
+#pragma unroll
+  for (int ks = 0; ks < BK / 4; ++ks) {
+    const int k = kmap<LAYOUT>(ks, t);
+    double a[C::MT], b[C::NT];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+      a[mt] = *reinterpret_cast<const double*>(sa + tile_off<LAYOUT>(wm * C::WTM + mt * 8 + g, k));
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+      b[nt] = *reinterpret_cast<const double*>(sb + tile_off<LAYOUT>(wn * C::WTN + nt * 8 + g, k));
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) dmma_884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+  }
+}
+
+template <int LAYOUT, bool USE_TMA, int TBM>
+__global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
+    k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args) {
+  using C = Cfg<TBM>;
+  if (ld_info(args.d_info) != 0) return;  // dpotrf2 semantics: stop after a failed pivot
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  int tm, tn;
+  if (args.tri) {
+    tri_index(blockIdx.x, tm, tn);
+  } else {
+    tm = blockIdx.x % args.tiles_m;
+    tn = blockIdx.x / args.tiles_m;
+  }
+  const int m0 = tm * TBM, n0 = tn * TBM;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp % C::WGM, wn = warp / C::WGM;
+  const int g = lane >> 2, t = lane & 3;
+  const int KT = (args.K + BK - 1) / BK;
+
+  double acc[C::MT][C::NT][2];
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  if (USE_TMA) {
+    // Producer = thread 0 (inside warp 0): keeps STAGES-1 TMA stages in flight;
+    // a stage is refilled once every warp released it (empty barrier).
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], C::NUM_WARPS);
+      }
+      fence_barrier_init();
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, kt, m0, n0);
+    for (int kt = 0; kt < KT; ++kt) {
+      if (threadIdx.x == 0 && kt + STAGES - 1 < KT) {
+        if (kt >= 1) mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
+        issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, kt + STAGES - 1, m0, n0);
+      }
+      const int s = kt % STAGES;
+      mbar_wait(&full[s], (kt / STAGES) & 1);
+      const uint8_t* sa = smem + s * C::STAGE_BYTES;
+      mma_stage<LAYOUT, TBM>(acc, sa, sa + C::TILE_BYTES, wm, wn, g, t);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  } else {
+    for (int kt = 0; kt < KT; ++kt) {
+      __syncthreads();
+      fill_tile_ldg<LAYOUT, TBM>(smem, args.A, args.lda, args.M, m0, args.K, kt * BK);
+      fill_tile_ldg<LAYOUT, TBM>(smem + C::TILE_BYTES, args.B, args.ldb, args.N, n0, args.K, kt * BK);
+      __syncthreads();
+      mma_stage<LAYOUT, TBM>(acc, smem, smem + C::TILE_BYTES, wm, wn, g, t);
+    }
+  }
+
+  // Epilogue: stage the accumulator tile in shared memory (the pipeline
+  // buffers are free now), then C -= tile with coalesced accesses along the
+  // contiguous global dimension, 16 independent loads in flight per thread.
+  // SYRK tiles write only i >= j.
+  __syncthreads();
+  double* sC = reinterpret_cast<double*>(smem);
+#pragma unroll
+  for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int il = wm * C::WTM + mt * 8 + g, jl = wn * C::WTN + nt * 8 + 2 * t + c;
+        // fast index = the globally contiguous one (i for layout N, j for layout T)
+        sC[LAYOUT == kLayoutN ? jl * C::CPAD + il : il * C::CPAD + jl] = acc[mt][nt][c];
+      }
+  __syncthreads();
+  constexpr int SLOW_STEP = C::THREADS / TBM;  // 2
+  const int f = threadIdx.x % TBM;             // fast index
+  const int s0 = threadIdx.x / TBM;
+  const int fi = (LAYOUT == kLayoutN ? m0 : n0) + f;
+  const int flim = LAYOUT == kLayoutN ? args.M : args.N;
+  const int slim = LAYOUT == kLayoutN ? args.N : args.M;
+  const int sbase = LAYOUT == kLayoutN ? n0 : m0;
+  if (fi < flim) {
+    double* Cf = args.C + fi;  // + slow * ldc
+#pragma unroll 1
+    for (int q0 = 0; q0 < TBM / SLOW_STEP; q0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int sg = sbase + s0 + SLOW_STEP * (q0 + q);
+        const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
+        v[q] = (sg < slim && (!args.tri || i >= j)) ? Cf[(int64_t)sg * args.ldc] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int sl = s0 + SLOW_STEP * (q0 + q);
+        const int sg = sbase + sl;
+        const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
+        if (sg < slim && (!args.tri || i >= j)) Cf[(int64_t)sg * args.ldc] = v[q] - sC[sl * C::CPAD + f];
+      }
+    }
+  }
+}
+
+template <int LAYOUT, bool USE_TMA, int TBM>
+cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const UpdateArgs& a, int grid, cudaStream_t st) {
+  k_update<LAYOUT, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
+template <int TBM>
+cudaError_t launch_tbm(const UpdateOp& op, cudaStream_t st) {
+  const UpdateArgs& a = op.args;
+  const int tiles_m = (a.M + TBM - 1) / TBM, tiles_n = (a.N + TBM - 1) / TBM;
+  const int grid = a.tri ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  if (a.layout == kLayoutN)
+    return op.use_tma ? launch_one<kLayoutN, true, TBM>(op.tmA, op.tmB, a, grid, st)
+                      : launch_one<kLayoutN, false, TBM>(op.tmA, op.tmB, a, grid, st);
+  return op.use_tma ? launch_one<kLayoutT, true, TBM>(op.tmA, op.tmB, a, grid, st)
+                    : launch_one<kLayoutT, false, TBM>(op.tmA, op.tmB, a, grid, st);
+}
+
+template <int TBM>
+cudaError_t configure_tbm() {
+  cudaError_t e;
+  const int sm = Cfg<TBM>::SMEM_BYTES;
+  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if ((e = cudaFuncSetAttribute(k_update<kLayoutN, true, TBM>, attr, sm)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_update<kLayoutN, false, TBM>, attr, sm)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_update<kLayoutT, true, TBM>, attr, sm)) != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_update<kLayoutT, false, TBM>, attr, sm);
+}
+
+}  // namespace
+
+// Tile size for an update: 128 x 128 CTA tiles when they fill the 148 SMs,
+// else 64 x 64 (4x the CTAs; latency of the small updates near the leaves).
+int update_tile_for(int M, int N, int tri) {
+  const long tm = (M + 127) / 128, tn = (N + 127) / 128;
+  const long t128 = tri ? tm * (tm + 1) / 2 : tm * tn;
+  return t128 >= 148 ? 128 : 64;
+}
+
+cudaError_t configure_update() {
+  cudaError_t e = configure_tbm<128>();
+  if (e != cudaSuccess) return e;
+  return configure_tbm<64>();
+}
+
+cudaError_t launch_update(const UpdateOp& op, cudaStream_t st) {
+  const UpdateArgs& a = op.args;
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaSuccess;
+  return op.tile == 128 ? launch_tbm<128>(op, st) : launch_tbm<64>(op, st);
+}
+
+// Host: TMA descriptor for an operand block of the L-view (rows x K) with
+// box rows `box_rows` (= the CTA tile).  Layout N: dims {rows, K}, box {16, 16};
+// layout T: dims {K, rows}, box {16, box_rows}.
+bool make_operand_map(CUtensorMap* map, const double* base, int64_t ld, int layout, int rows, int K, int box_rows) {
+  typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return false;
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld & 1) != 0 || rows <= 0 || K <= 0) return false;
+  cuuint64_t dims[2];
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2];
+  cuuint32_t estr[2] = {1, 1};
+  if (layout == kLayoutN) {
+    dims[0] = (cuuint64_t)rows;
+    dims[1] = (cuuint64_t)K;
+    box[0] = 16;
+    box[1] = BK;
+  } else {
+    dims[0] = (cuuint64_t)K;
+    dims[1] = (cuuint64_t)rows;
+    box[0] = BK;
+    box[1] = (cuuint32_t)box_rows;
+  }
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace relapack

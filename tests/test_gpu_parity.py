@@ -1,0 +1,273 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle on the
+same seeded inputs.  Tolerances (north_star, readings R8/R9):
+floored elementwise relative error <= 1e-10, backward error <= 10, identical
+info; bitwise for the exact-integer pins and for the untouched triangle.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1602_06763_b200 as rl
+from inputs import gen
+from tests.metrics import backward_error, floored_rel_err, lower_of, sym_from
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def to_dev(A: np.ndarray) -> torch.Tensor:
+    """Column-major device copy of a Fortran-ordered numpy matrix (same bits, same lda)."""
+    lda, n = A.shape
+    buf = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()  # (n, lda) row-major == column-major (lda, n)
+    return buf.t()[:lda, :n] if lda == n else buf.t()[:n, :]
+
+
+def dev_full(dA: torch.Tensor, lda: int) -> np.ndarray:
+    """The whole lda x n column-major buffer behind a device view, as Fortran numpy."""
+    n = dA.shape[1]
+    base = torch.as_strided(dA, (lda, n), (1, lda))
+    return np.asfortranarray(base.cpu().numpy())
+
+
+def run_both(A, uplo, n=None):
+    """(gpu_result_full, gpu_info, oracle_result_full, oracle_info)."""
+    lda = A.shape[0]
+    n = A.shape[1] if n is None else n
+    dA = to_dev(A)
+    info = rl.dpotrf(dA, uplo)
+    torch.cuda.synchronize()
+    G = dev_full(dA, lda)
+    R = np.array(A, order="F", copy=True)
+    rinfo = oracle.dpotrf(R, uplo, n=n)
+    return G, info, R, rinfo
+
+
+def check_spd(A, uplo, tol=TOL):
+    n = A.shape[1]
+    G, info, R, rinfo = run_both(A, uplo)
+    assert info == rinfo == 0
+    Lg, Lo = lower_of(G[:n], uplo), lower_of(R[:n], uplo)
+    err = floored_rel_err(Lg, Lo, A[:n])
+    assert err <= tol, f"n={n} uplo={uplo} floored rel err {err:.3e}"
+    assert backward_error(sym_from(A[:n], uplo), Lg) <= 10.0
+    # the opposite strict triangle and the lda padding are bitwise untouched
+    other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+    assert np.array_equal(G[:n][other].view(np.uint64), A[:n][other].view(np.uint64))
+    if A.shape[0] > n:
+        assert np.array_equal(G[n:].view(np.uint64), A[n:].view(np.uint64))
+    return err
+
+
+# ---------------------------------------------------------------- base case (n <= c)
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 31, 33, 64])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_base_case_random(n, uplo):
+    check_spd(gen.spd(n, n), uplo)
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_P1_integer_n8_bitwise(uplo):
+    for seed in range(1, 51):
+        A, L = gen.integer_L(8, seed)
+        G, info, _, _ = run_both(A, uplo)
+        assert info == 0
+        assert np.array_equal(lower_of(G, uplo), L)
+
+
+# ---------------------------------------------------------------- recursion
+@pytest.mark.parametrize("n", [65, 100, 127, 128, 129, 200, 256, 300, 513, 1000, 1031])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_recursive_random(n, uplo):
+    check_spd(gen.spd(n, 7 + n), uplo)
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_recursive_normal_dist(n):
+    check_spd(gen.spd(n, 3, "normal"), "U")
+
+
+@pytest.mark.parametrize("n", [256, 1000])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_P1_integer_recursive_bitwise(n, uplo):
+    A, L = gen.integer_L(n, 11)
+    G, info, _, _ = run_both(A, uplo)
+    assert info == 0
+    assert np.array_equal(lower_of(G, uplo), L)
+
+
+@pytest.mark.parametrize("n", [777, 2048])
+def test_P2_min_matrix_exact(n):
+    A = gen.min_matrix(n)
+    dA = to_dev(A)
+    assert rl.dpotrf(dA, "L") == 0
+    assert torch.equal(torch.tril(dA), torch.tril(torch.ones(n, n, dtype=torch.float64, device="cuda")))
+
+
+@pytest.mark.parametrize("n,lda", [(300, 304), (257, 300), (300, 301), (129, 131)])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_lda_padding_and_odd_lda(n, lda, uplo):
+    """Odd lda takes the non-TMA fallback loader; padding rows stay untouched."""
+    A = gen.spd(n, 5, lda=lda)
+    check_spd(A, uplo)
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_nan_sentinels_other_triangle(uplo):
+    n = 333
+    A = gen.spd(n, 2)
+    other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+    A = np.array(A, order="F")
+    A[other] = np.nan
+    G, info, R, rinfo = run_both(A, uplo)
+    assert info == rinfo == 0
+    assert np.all(np.isnan(G[other]))
+    assert not np.any(np.isnan(G[~other]))
+
+
+# ---------------------------------------------------------------- info
+@pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("k", [0, 1, 63, 64, 65, 100, 255, 256, 499])
+def test_P7_indefinite_info(uplo, k):
+    n = 500
+    A = gen.indefinite(gen.spd(n, 4), k)
+    G, info, R, rinfo = run_both(A, uplo)
+    assert rinfo == k + 1
+    assert info == rinfo
+    # the leading (k x k) block holds the factor of the leading minor of order k
+    # (dpotrf2 semantics; the recursion skips the updates after the failure, so
+    # rows below the failing diagonal block are left unspecified)
+    if k > 0:
+        Lg, Lo = lower_of(G, uplo)[:k, :k], lower_of(R, uplo)[:k, :k]
+        floor = 1e-4 * np.sqrt(np.abs(np.diag(A)))[:k, None]
+        assert np.max(np.abs(Lg - Lo) / np.maximum(np.abs(Lo), floor)) <= TOL
+
+
+def test_nan_pivot_info():
+    n = 200
+    A = np.array(gen.spd(n, 1), order="F")
+    A[150, 150] = np.nan
+    _, info, _, rinfo = run_both(A, "L")
+    assert info == rinfo == 151
+
+
+def test_repeat_calls_use_cached_graph():
+    n = 700
+    A = gen.spd(n, 9)
+    dA = to_dev(A)
+    for _ in range(3):
+        dA.copy_(to_dev(A))
+        assert rl.dpotrf(dA, "L") == 0
+    R = np.array(A, order="F")
+    oracle.dpotrf(R, "L")
+    assert floored_rel_err(np.tril(dA.cpu().numpy()), np.tril(R), A) <= TOL
+
+
+def test_graphs_off_same_bits():
+    n = 600
+    A = gen.spd(n, 10)
+    d1, d2 = to_dev(A), to_dev(A)
+    rl.set_graphs(True)
+    assert rl.dpotrf(d1, "L") == 0
+    rl.set_graphs(False)
+    try:
+        assert rl.dpotrf(d2, "L") == 0
+    finally:
+        rl.set_graphs(True)
+    assert torch.equal(d1, d2)  # same kernels, same order: deterministic
+
+
+@pytest.mark.parametrize("c", [16, 24, 32, 48])
+def test_crossover_values(c):
+    rl.set_crossover(c)
+    try:
+        check_spd(gen.spd(517, c), "L")
+    finally:
+        rl.set_crossover(64)
+
+
+# ---------------------------------------------------------------- other entry points
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_host_matrix_path(uplo):
+    """relapack_dpotrf with a HOST pointer stages the triangle through the GPU."""
+    n = 450
+    A = gen.spd(n, 12, lda=452)
+    R = np.array(A, order="F", copy=True)
+    rinfo = oracle.dpotrf(R, uplo, n=n)
+    H_full = torch.from_numpy(np.array(A.T, order="C", copy=True)).t()  # own CPU buffer (452 x n), column-major
+    H = H_full[:n, :]  # (n, n) view with lda 452
+    info = rl.dpotrf(H, uplo)
+    assert info == rinfo == 0
+    G = np.asfortranarray(H_full.numpy())
+    assert floored_rel_err(lower_of(G[:n], uplo), lower_of(R[:n], uplo), A[:n]) <= TOL
+    other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+    assert np.array_equal(G[:n][other], A[:n][other])
+    assert np.all(np.isnan(G[n:]))
+
+
+def test_async_entry_point():
+    n = 640
+    A = gen.spd(n, 13)
+    dA = to_dev(A)
+    d_info = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        assert rl.dpotrf_async(dA, d_info, "L", stream=s) == 0
+    s.synchronize()
+    assert int(d_info.item()) == 0
+    R = np.array(A, order="F")
+    oracle.dpotrf(R, "L")
+    assert floored_rel_err(np.tril(dA.cpu().numpy()), np.tril(R), A) <= TOL
+    B = gen.indefinite(A, 321)
+    dB = to_dev(B)
+    assert rl.dpotrf_async(dB, d_info, "L") == 0
+    torch.cuda.synchronize()
+    assert int(d_info.item()) == 322
+
+
+def test_argument_errors_on_device():
+    d = torch.zeros(16, dtype=torch.float64, device="cuda")
+    assert rl.dpotrf_raw("Q", 2, d.data_ptr(), 2) == -1
+    assert rl.dpotrf_raw("L", 4, d.data_ptr(), 2) == -4
+
+
+# ---------------------------------------------------------------- batched (CFG[4] shape)
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_batched_parity(uplo):
+    b = gen.batched_spd(3000, 5)
+    buf = torch.from_numpy(b["buf"]).cuda()
+    ptrs = (buf.data_ptr() + 8 * torch.from_numpy(b["offsets"])).cuda()
+    ns = torch.from_numpy(b["ns"]).cuda()
+    ldas = torch.from_numpy(b["ldas"]).cuda()
+    infos = torch.full((len(b["ns"]),), -99, dtype=torch.int32, device="cuda")
+    assert rl.dpotrf_batched(ns, ptrs, ldas, infos, uplo) == 0
+    torch.cuda.synchronize()
+    ref = b["buf"].copy()
+    rinfo = oracle.dpotrf_batched(uplo, b["ns"], ref, b["offsets"], b["ldas"])
+    ginfo = infos.cpu().numpy()
+    assert np.array_equal(ginfo, rinfo)
+    assert np.array_equal(ginfo, b["expected_info"])
+    G = buf.cpu().numpy()
+    worst = 0.0
+    for i in np.nonzero(rinfo == 0)[0]:
+        nb, off = int(b["ns"][i]), int(b["offsets"][i])
+        A = b["buf"][off: off + nb * nb].reshape(nb, nb).T
+        g = G[off: off + nb * nb].reshape(nb, nb).T
+        r = ref[off: off + nb * nb].reshape(nb, nb).T
+        worst = max(worst, floored_rel_err(lower_of(g, uplo), lower_of(r, uplo), A))
+        other = np.triu(np.ones((nb, nb), bool), 1) if uplo == "L" else np.tril(np.ones((nb, nb), bool), -1)
+        assert np.array_equal(g[other], A[other])
+    assert worst <= TOL
+
+
+def test_batched_bad_sizes():
+    n_ok = 16
+    buf = torch.from_numpy(np.asfortranarray(gen.spd(n_ok, 1)).T.copy().reshape(-1)).cuda()
+    ns = torch.tensor([n_ok, 65, -1, 16, 0], dtype=torch.int32, device="cuda")
+    ldas = torch.tensor([16, 65, 1, 8, 1], dtype=torch.int32, device="cuda")
+    ptrs = torch.tensor([buf.data_ptr()] * 5, dtype=torch.int64, device="cuda")
+    infos = torch.zeros(5, dtype=torch.int32, device="cuda")
+    assert rl.dpotrf_batched(ns, ptrs, ldas, infos, "L") == 0
+    torch.cuda.synchronize()
+    assert infos.cpu().tolist() == [0, -2, -2, -4, 0]

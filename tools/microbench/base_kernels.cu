@@ -1,0 +1,37 @@
+// Times the base-case kernels (K1 potf2, K5 trsm) in isolation, warm, with
+// CUDA events around 200 back-to-back launches.  Includes the library sources.
+#include <cstdio>
+#include <vector>
+#include "../../paper_1602_06763_b200/csrc/potf2.cu"
+#include "../../paper_1602_06763_b200/csrc/trsm.cu"
+using namespace relapack;
+int main() {
+  const int n = 4096;
+  std::vector<double> h((size_t)n * n);
+  for (int j = 0; j < n; ++j) for (int i = 0; i < n; ++i) h[(size_t)i + (size_t)j * n] = (i == j) ? n : 1.0 / (1 + i + j);
+  double* d; cudaMalloc(&d, h.size() * 8);
+  int* info; cudaMalloc(&info, 4); cudaMemset(info, 0, 4);
+  configure_potf2(); configure_trsm();
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  auto time = [&](const char* name, auto fn) {
+    for (int w = 0; w < 3; ++w) { cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice); fn(); }
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int i = 0; i < 200; ++i) fn();
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    cudaMemset(info, 0, 4);
+    printf("%-40s %8.2f us/launch  (%s)\n", name, ms * 1000 / 200, cudaGetErrorString(cudaGetLastError()));
+  };
+  for (int nb : {1, 8, 16, 32, 64}) {
+    char nm[64]; snprintf(nm, 64, "potf2 n=%d layout N", nb);
+    time(nm, [&] { launch_potf2(d, n, kLayoutN, nb, info, 0, 0); });
+  }
+  time("potf2 n=64 layout T", [&] { launch_potf2(d, n, kLayoutT, 64, info, 0, 0); });
+  for (int m : {64, 512, 2048, 8192}) for (int t : {16, 64}) {
+    char nm[64]; snprintf(nm, 64, "trsm m=%d t=%d layout N", m, t);
+    time(nm, [&] { launch_trsm_base(d, n, d + 64, n, kLayoutN, m, t, info, 0); });
+  }
+  time("trsm m=2048 t=64 layout T", [&] { launch_trsm_base(d, n, d + 64 * n, n, kLayoutT, 2048, 64, info, 0); });
+  return 0;
+}
