@@ -136,7 +136,7 @@ RELAPACK_API const char* relapack_last_error(void);
 RELAPACK_API void relapack_finalize(void);
 
 /* Tuning knobs (also read from env RELAPACK_CROSSOVER / RELAPACK_SPLIT_TILE /
- * RELAPACK_GRAPH).  crossover c: base case when n <= c (16 <= c <= 64);
+ * RELAPACK_GRAPH).  crossover c: base case when n <= c (16 <= c <= 128);
  * split tile T: n1 = T*floor(n/(2T)) (T in {8,16,32,64,128}); graphs 0/1.
  * Return 0, or -1 on an out-of-range value. */
 RELAPACK_API int relapack_set_crossover(int c);
@@ -170,6 +170,9 @@ RELAPACK_API int relapack_plan_ledger(int n, int c, int T, int levels, double* f
 RELAPACK_API int relapack_profile_enable(int on);
 RELAPACK_API int relapack_profile_read(int kind, double* ms_total, double* flops_total, int* launches);
 RELAPACK_API void relapack_profile_reset(void);
+/* Per-launch records since the last reset, 7 doubles each: kind, m, n, k,
+ * recursion level, algorithmic flops, milliseconds.  Returns the count. */
+RELAPACK_API int relapack_profile_records(int max, double* out);
 
 /* Library version string (build id). */
 RELAPACK_API const char* relapack_version(void);

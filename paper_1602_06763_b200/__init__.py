@@ -27,6 +27,7 @@ __all__ = [
     "profile_enable",
     "profile_reset",
     "profile_read",
+    "profile_records",
     "plan_ledger",
     "set_crossover",
     "set_split_tile",
@@ -92,6 +93,8 @@ def lib():
         L.relapack_profile_read.argtypes = [c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_double), ip]
         L.relapack_profile_read.restype = c_int
         L.relapack_profile_reset.restype = None
+        L.relapack_profile_records.argtypes = [c_int, ctypes.POINTER(c_double)]
+        L.relapack_profile_records.restype = c_int
         _lib = L
     return _lib
 
@@ -146,6 +149,19 @@ def profile_read(kind: str):
     if lib().relapack_profile_read(PROFILE_KINDS[kind], ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(cnt)) != 0:
         raise ValueError(kind)
     return ms.value, fl.value, cnt.value
+
+
+def profile_records(max_records: int = 100000):
+    """Per-launch (kind, m, n, k, level, flops, ms) records since the last reset."""
+    buf = (ctypes.c_double * (7 * max_records))()
+    cnt = lib().relapack_profile_records(max_records, buf)
+    kinds = {v: k for k, v in PROFILE_KINDS.items()}
+    out = []
+    for i in range(cnt):
+        r = buf[7 * i: 7 * i + 7]
+        out.append(dict(kind=kinds[int(r[0])], m=int(r[1]), n=int(r[2]), k=int(r[3]), level=int(r[4]),
+                        flops=r[5], ms=r[6]))
+    return out
 
 
 def split_point(n: int, align: int) -> int:

@@ -157,6 +157,7 @@ struct ProfRecord {
   cudaEvent_t start, stop;
   int kind;
   double flops;
+  int m, n, k, level;
 };
 static std::mutex g_prof_mu;
 static std::atomic<int> g_prof_on{0};
@@ -188,6 +189,10 @@ static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, in
       rec.stop = prof_event();
       rec.kind = (int)op.kind;
       rec.flops = op.flops;
+      rec.m = op.m;
+      rec.n = op.n;
+      rec.k = op.k;
+      rec.level = op.level;
       cudaEventRecord(rec.start, st);
     }
     switch (op.kind) {
@@ -540,6 +545,21 @@ int relapack_profile_read(int kind, double* ms_total, double* flops_total, int* 
   if (flops_total) *flops_total = fl;
   if (launches) *launches = cnt;
   return 0;
+}
+
+int relapack_profile_records(int max, double* out) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int cnt = 0;
+  for (const ProfRecord& r : g_prof) {
+    if (cnt >= max) break;
+    cudaEventSynchronize(r.stop);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.start, r.stop);
+    double* o = out + 7 * cnt;
+    o[0] = r.kind; o[1] = r.m; o[2] = r.n; o[3] = r.k; o[4] = r.level; o[5] = r.flops; o[6] = t;
+    ++cnt;
+  }
+  return cnt;
 }
 
 void relapack_profile_reset(void) {

@@ -39,7 +39,7 @@ int update_tile_for(int M, int N, int tri);
 // ---- K1 base-case potf2 (potf2.cu) ----
 // Factor the n x n L-view block at A (n <= kPotf2Max) in shared memory; on a
 // non-positive pivot at local column j write d_info = info_base + j + 1.
-constexpr int kPotf2Max = 64;
+constexpr int kPotf2Max = 128;
 cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, int info_base, cudaStream_t st);
 
 // ---- K5 base TRSM (trsm.cu): B(m x t) := B * L^{-T}, L t x t lower (t <= kTrsmMax)

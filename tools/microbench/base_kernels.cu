@@ -2,6 +2,7 @@
 // CUDA events around 200 back-to-back launches.  Includes the library sources.
 #include <cstdio>
 #include <vector>
+#define RELAPACK_PROBE 1
 #include "../../paper_1602_06763_b200/csrc/potf2.cu"
 #include "../../paper_1602_06763_b200/csrc/trsm.cu"
 using namespace relapack;
@@ -23,9 +24,19 @@ int main() {
     cudaMemset(info, 0, 4);
     printf("%-40s %8.2f us/launch  (%s)\n", name, ms * 1000 / 200, cudaGetErrorString(cudaGetLastError()));
   };
-  for (int nb : {1, 8, 16, 32, 64}) {
+  for (int nb : {1, 8, 16, 32, 64, 96, 128}) {
     char nm[64]; snprintf(nm, 64, "potf2 n=%d layout N", nb);
     time(nm, [&] { launch_potf2(d, n, kLayoutN, nb, info, 0, 0); });
+  }
+  {
+    long long pr[64];
+    cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
+    launch_potf2(d, n, kLayoutN, 128, info, 0, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
+    printf("potf2 n=128 phases (cycles from start): stage-in %lld |", pr[1] - pr[0]);
+    for (int p = 0; p < 16; ++p) printf(" P%d %lld |", p, pr[2 + p] - pr[0]);
+    printf(" end %lld\n", pr[63] - pr[0]);
   }
   time("potf2 n=64 layout T", [&] { launch_potf2(d, n, kLayoutT, 64, info, 0, 0); });
   for (int m : {64, 512, 2048, 8192}) for (int t : {16, 64}) {
