@@ -130,6 +130,24 @@ RELAPACK_API void relapack_comm_destroy(relapack_comm_t* comm);
 RELAPACK_API void relapack_dpotrf_dist(const char* uplo, const int* n, double* A, const int* lda, int nb, int dist_min,
                           relapack_comm_t* comm, int* info);
 
+/*
+ * Test hooks of the multi-GPU mode (no NCCL needed):
+ *   relapack_dpotrf_dist_loopback  runs the distributed schedule for `nranks`
+ *     virtual ranks on the current GPU; A_ranks[s] is rank s's full DEVICE
+ *     copy of A.  Collectives are emulated by device copies between the ranks'
+ *     buffers and the ranks run one after another between collectives, so no
+ *     kernel waits on another rank.  infos[s] (host) = rank s's info.
+ *     Returns 0 or an argument / CUDA error code.
+ *   relapack_dist_schedule  host-only: rank `rank`'s step list, 16 int64 per
+ *     step (kind, level, c_i, c_j, a_i, a_j, b_i, b_j, m, n, k, info_base,
+ *     c_buf, a_buf, b_buf, 0); kinds 0 potf2, 1 trsm, 2 gemm, 3 syrk,
+ *     10 pack, 11 allgather, 12 unpack.  Returns the step count or -1.
+ */
+RELAPACK_API int relapack_dpotrf_dist_loopback(const char* uplo, int n, double* const* A_ranks, int lda, int nb,
+                                               int dist_min, int nranks, int* infos);
+RELAPACK_API int relapack_dist_schedule(int n, int c, int T, int nb, int dist_min, int rank, int nranks, int64_t* out,
+                                        int max_ops);
+
 /* ---- configuration, introspection, teardown ---- */
 RELAPACK_API void relapack_set_stream(relapack_stream_t stream);
 RELAPACK_API const char* relapack_last_error(void);

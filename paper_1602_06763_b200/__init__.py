@@ -95,6 +95,11 @@ def lib():
         L.relapack_profile_reset.restype = None
         L.relapack_profile_records.argtypes = [c_int, ctypes.POINTER(c_double)]
         L.relapack_profile_records.restype = c_int
+        L.relapack_dpotrf_dist_loopback.argtypes = [ctypes.c_char_p, c_int, c_void_p, c_int, c_int, c_int, c_int, ip]
+        L.relapack_dpotrf_dist_loopback.restype = c_int
+        L.relapack_dist_schedule.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                             ctypes.POINTER(ctypes.c_int64), c_int]
+        L.relapack_dist_schedule.restype = c_int
         _lib = L
     return _lib
 
@@ -162,6 +167,94 @@ def profile_records(max_records: int = 100000):
         out.append(dict(kind=kinds[int(r[0])], m=int(r[1]), n=int(r[2]), k=int(r[3]), level=int(r[4]),
                         flops=r[5], ms=r[6]))
     return out
+
+
+DIST_KINDS = {0: "potf2", 1: "trsm", 2: "gemm", 3: "syrk", 10: "pack", 11: "allgather", 12: "unpack"}
+DIST_FIELDS = ("kind", "level", "c_i", "c_j", "a_i", "a_j", "b_i", "b_j", "m", "n", "k", "info_base",
+               "c_buf", "a_buf", "b_buf")
+
+
+def dist_schedule(n: int, rank: int, nranks: int, nb: int = 512, dist_min: int = 4096, c: int | None = None,
+                  T: int = 64):
+    """Host-only: rank `rank`'s multi-GPU step list (list of dicts, see include/relapack.h)."""
+    c = get_crossover() if c is None else c
+    cnt = lib().relapack_dist_schedule(n, c, T, nb, dist_min, rank, nranks, None, 0)
+    if cnt < 0:
+        raise ValueError("bad schedule arguments")
+    buf = (ctypes.c_int64 * (16 * max(cnt, 1)))()
+    lib().relapack_dist_schedule(n, c, T, nb, dist_min, rank, nranks, buf, cnt)
+    out = []
+    for i in range(cnt):
+        row = buf[16 * i: 16 * i + 15]
+        d = dict(zip(DIST_FIELDS, (int(v) for v in row)))
+        d["kind"] = DIST_KINDS[d["kind"]]
+        out.append(d)
+    return out
+
+
+def _locate_nccl() -> None:
+    """Point RELAPACK_NCCL_LIB at the NCCL the process uses (torch's bundled one) if not set."""
+    if os.environ.get("RELAPACK_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl  # the wheel torch links against
+
+        for d in nvidia.nccl.__path__:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["RELAPACK_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
+
+
+class Comm:
+    """NCCL communicator for relapack_dpotrf_dist (one process per GPU)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        _locate_nccl()
+        self.ptr = ctypes.c_void_p()
+        r = lib().relapack_comm_init(ctypes.byref(self.ptr), uid, nranks, rank, device)
+        if r != 0:
+            raise RelapackError(f"relapack_comm_init failed ({r}): {last_error()}")
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        _locate_nccl()
+        buf = ctypes.create_string_buffer(128)
+        r = lib().relapack_comm_unique_id(buf)
+        if r != 0:
+            raise RelapackError(f"relapack_comm_unique_id failed ({r}): {last_error()}")
+        return buf.raw
+
+    def close(self):
+        if self.ptr:
+            lib().relapack_comm_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+
+def dpotrf_dist(A, comm: "Comm", uplo: str = "L", nb: int = 512, dist_min: int = 4096) -> int:
+    """Distributed factorization of the device matrix A (identical on every rank); returns info."""
+    ptr, n, lda = _matrix_args(A)
+    info = ctypes.c_int(0)
+    lib().relapack_dpotrf_dist(uplo.encode(), ctypes.byref(ctypes.c_int(n)), ctypes.c_void_p(ptr),
+                               ctypes.byref(ctypes.c_int(lda)), nb, dist_min, comm.ptr, ctypes.byref(info))
+    if info.value <= -1000:
+        raise RelapackError(f"relapack_dpotrf_dist failed: {last_error()}")
+    return info.value
+
+
+def dpotrf_dist_loopback(As, uplo: str = "L", nb: int = 512, dist_min: int = 4096):
+    """Test hook: run the distributed schedule for len(As) virtual ranks on one GPU; returns the infos."""
+    ptrs = [_matrix_args(A) for A in As]
+    n, lda = ptrs[0][1], ptrs[0][2]
+    arr = (ctypes.c_void_p * len(As))(*[p[0] for p in ptrs])
+    infos = (ctypes.c_int * len(As))()
+    r = lib().relapack_dpotrf_dist_loopback(uplo.encode(), n, arr, lda, nb, dist_min, len(As), infos)
+    if r != 0:
+        raise RelapackError(f"relapack_dpotrf_dist_loopback failed ({r}): {last_error()}")
+    return list(infos)
 
 
 def split_point(n: int, align: int) -> int:

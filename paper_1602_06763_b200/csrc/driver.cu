@@ -53,6 +53,12 @@ static int env_int(const char* name, int dflt) {
   return atoi(v);
 }
 
+static std::atomic<int> g_stream_set{0};
+
+cudaStream_t current_stream_or(cudaStream_t fallback) {
+  return g_stream_set.load() ? reinterpret_cast<cudaStream_t>(g_stream.load()) : fallback;
+}
+
 PlanParams current_params() {
   PlanParams p;
   int c = g_crossover.load();
@@ -447,7 +453,10 @@ int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const*
   return e == cudaSuccess ? 0 : cuda_fail(e, "batched launch");
 }
 
-void relapack_set_stream(relapack_stream_t stream) { g_stream.store(reinterpret_cast<uintptr_t>(stream)); }
+void relapack_set_stream(relapack_stream_t stream) {
+  g_stream.store(reinterpret_cast<uintptr_t>(stream));
+  g_stream_set.store(1);
+}
 
 const char* relapack_last_error(void) {
   if (!g_last_error.empty()) return g_last_error.c_str();

@@ -12,4 +12,6 @@ int cuda_fail(cudaError_t e, const char* what);
 PlanParams current_params();
 // Enqueue the whole recursive factorization of the device L-view matrix A on st.
 int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st);
+// The stream set with relapack_set_stream, or `fallback` if none was set.
+cudaStream_t current_stream_or(cudaStream_t fallback);
 }  // namespace relapack

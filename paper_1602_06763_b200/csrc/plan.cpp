@@ -24,9 +24,11 @@ int split_point(int n, int align) {
 
 namespace {
 
-void build_trsm(int L_off, int B_i, int B_j, int m, int k, int level, const PlanParams& p,
+void build_trsm(int L_off, int b_buf, int B_i, int B_j, int m, int k, int level, const PlanParams& p,
                 std::vector<PlanOp>& ops) {
-  // L block origin is (L_off, L_off) on the diagonal; B block origin (B_i, B_j), m x k.
+  // L block origin is (L_off, L_off) on the diagonal of BUF_A; B block origin
+  // (B_i, B_j) of buffer b_buf, m x k.
+  if (m <= 0 || k <= 0) return;
   if (k <= p.trsm_base) {
     PlanOp op{};
     op.kind = OP_TRSM;
@@ -35,11 +37,12 @@ void build_trsm(int L_off, int B_i, int B_j, int m, int k, int level, const Plan
     op.a_i = L_off; op.a_j = L_off;
     op.m = m; op.k = k;
     op.flops = (double)m * k * k;
+    op.c_buf = b_buf;
     ops.push_back(op);
     return;
   }
   const int pp = split_point(k, p.split_tile), q = k - pp;
-  build_trsm(L_off, B_i, B_j, m, pp, level, p, ops);
+  build_trsm(L_off, b_buf, B_i, B_j, m, pp, level, p, ops);
   PlanOp g{};
   g.kind = OP_GEMM;
   g.level = level;
@@ -48,8 +51,9 @@ void build_trsm(int L_off, int B_i, int B_j, int m, int k, int level, const Plan
   g.b_i = L_off + pp; g.b_j = L_off;   // Lb (q x p)
   g.m = m; g.n = q; g.k = pp;
   g.flops = 2.0 * m * q * pp;
+  g.c_buf = b_buf; g.a_buf = b_buf; g.b_buf = BUF_A;
   ops.push_back(g);
-  build_trsm(L_off + pp, B_i, B_j + pp, m, q, level, p, ops);
+  build_trsm(L_off + pp, b_buf, B_i, B_j + pp, m, q, level, p, ops);
 }
 
 void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, std::vector<PlanOp>& ops) {
@@ -67,7 +71,7 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
   }
   const int n1 = split_point(n, p.split_tile), n2 = n - n1;
   build_potrf(off, n1, level + 1, info_base, p, ops);
-  build_trsm(off, off + n1, off, n2, n1, level + 1, p, ops);
+  build_trsm(off, BUF_A, off + n1, off, n2, n1, level + 1, p, ops);
   PlanOp s{};
   s.kind = OP_SYRK;
   s.level = level + 1;
@@ -85,6 +89,147 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
 void build_potrf_plan(int n, const PlanParams& p, std::vector<PlanOp>& ops) {
   ops.clear();
   build_potrf(0, n, 0, 0, p, ops);
+}
+
+void append_potrf(int off, int n, int level, int info_base, const PlanParams& p, std::vector<PlanOp>& ops) {
+  build_potrf(off, n, level, info_base, p, ops);
+}
+
+void append_trsm(int l_off, int b_buf, int b_i, int b_j, int m, int k, int level, const PlanParams& p,
+                 std::vector<PlanOp>& ops) {
+  build_trsm(l_off, b_buf, b_i, b_j, m, k, level, p, ops);
+}
+
+// ---------------------------------------------------------------- multi-GPU
+int dist_owned_rows(int lo, int hi, int rank, const DistParams& d) {
+  int cnt = 0;
+  for (int b = lo / d.nb; b * d.nb < hi; ++b) {
+    if (dist_owner_block(b, d) != rank) continue;
+    const int r0 = b * d.nb > lo ? b * d.nb : lo;
+    const int r1 = (b + 1) * d.nb < hi ? (b + 1) * d.nb : hi;
+    if (r1 > r0) cnt += r1 - r0;
+  }
+  return cnt;
+}
+
+namespace {
+
+struct DistCtx {
+  const PlanParams& p;
+  const DistParams& d;
+  std::vector<PlanOp>& ops;
+  int64_t send_elems = 0;
+  int max_rows = 0, max_cols = 0;
+};
+
+int max_owned(int lo, int hi, const DistParams& d) {
+  int m = 0;
+  for (int r = 0; r < d.nranks; ++r) {
+    const int c = dist_owned_rows(lo, hi, r, d);
+    m = c > m ? c : m;
+  }
+  return m;
+}
+
+// Exchange rows [lo, hi) x cols [c0, c0 + ncols): every rank packs its owned
+// rows, all-gathers, and scatters all ranks' rows back (replicating them).
+void exchange_rows(DistCtx& x, int lo, int hi, int c0, int ncols, int level) {
+  const int rows_max = max_owned(lo, hi, x.d);
+  if (rows_max <= 0 || ncols <= 0) return;
+  PlanOp pk{};
+  pk.kind = OP_PACK;
+  pk.level = level;
+  pk.c_i = lo; pk.c_j = c0; pk.m = hi - lo; pk.k = ncols; pk.n = rows_max;
+  x.ops.push_back(pk);
+  PlanOp ag{};
+  ag.kind = OP_ALLGATHER;
+  ag.level = level;
+  ag.m = rows_max; ag.k = ncols;
+  x.ops.push_back(ag);
+  PlanOp up = pk;
+  up.kind = OP_UNPACK;
+  x.ops.push_back(up);
+  const int64_t e = (int64_t)rows_max * ncols;
+  if (e > x.send_elems) x.send_elems = e;
+  if (rows_max > x.max_rows) x.max_rows = rows_max;
+  if (ncols > x.max_cols) x.max_cols = ncols;
+}
+
+void dist_potrf(DistCtx& x, int off, int n, int level, int info_base) {
+  if (n <= 0) return;
+  if (n < x.d.dist_min || x.d.nranks == 1) {
+    // replicated leaf: gather the block's rows (their owners hold the updated
+    // values) and factor it redundantly on every rank (same info everywhere)
+    if (x.d.nranks > 1) exchange_rows(x, off, off + n, off, n, level);
+    build_potrf(off, n, level, info_base, x.p, x.ops);
+    return;
+  }
+  const int n1 = split_point(n, x.p.split_tile), n2 = n - n1;
+  dist_potrf(x, off, n1, level + 1, info_base);  // L11 replicated on return
+  // TRSM on this rank's rows of A21, packed contiguously in the send buffer
+  const int lo = off + n1, hi = off + n;
+  const int own = dist_owned_rows(lo, hi, x.d.rank, x.d);
+  const int rows_max = max_owned(lo, hi, x.d);
+  PlanOp pk{};
+  pk.kind = OP_PACK;
+  pk.level = level + 1;
+  pk.c_i = lo; pk.c_j = off; pk.m = n2; pk.k = n1; pk.n = rows_max;
+  x.ops.push_back(pk);
+  build_trsm(off, BUF_SEND, 0, 0, own, n1, level + 1, x.p, x.ops);
+  PlanOp ag{};
+  ag.kind = OP_ALLGATHER;
+  ag.level = level + 1;
+  ag.m = rows_max; ag.k = n1;
+  x.ops.push_back(ag);
+  PlanOp up = pk;
+  up.kind = OP_UNPACK;
+  x.ops.push_back(up);  // L21 replicated
+  const int64_t e = (int64_t)rows_max * n1;
+  if (e > x.send_elems) x.send_elems = e;
+  if (rows_max > x.max_rows) x.max_rows = rows_max;
+  if (n1 > x.max_cols) x.max_cols = n1;
+  // SYRK on this rank's row blocks of A22: for an owned row block [r0, r1)
+  // (relative to A22), C(r0:r1, 0:r0) -= L21(r0:r1) L21(0:r0)^T (GEMM) and the
+  // diagonal block C(r0:r1, r0:r1) -= L21(r0:r1) L21(r0:r1)^T (SYRK).
+  for (int b = lo / x.d.nb; b * x.d.nb < hi; ++b) {
+    if (dist_owner_block(b, x.d) != x.d.rank) continue;
+    const int g0 = b * x.d.nb > lo ? b * x.d.nb : lo;
+    const int g1 = (b + 1) * x.d.nb < hi ? (b + 1) * x.d.nb : hi;
+    if (g1 <= g0) continue;
+    if (g0 > lo) {
+      PlanOp g{};
+      g.kind = OP_GEMM;
+      g.level = level + 1;
+      g.c_i = g0; g.c_j = lo;      // C rows [g0, g1), cols [lo, g0)
+      g.a_i = g0; g.a_j = off;     // L21 rows [g0, g1)
+      g.b_i = lo; g.b_j = off;     // L21 rows [lo, g0)
+      g.m = g1 - g0; g.n = g0 - lo; g.k = n1;
+      g.flops = 2.0 * g.m * g.n * g.k;
+      x.ops.push_back(g);
+    }
+    PlanOp sy{};
+    sy.kind = OP_SYRK;
+    sy.level = level + 1;
+    sy.c_i = g0; sy.c_j = g0;
+    sy.a_i = g0; sy.a_j = off;
+    sy.b_i = g0; sy.b_j = off;
+    sy.n = sy.m = g1 - g0; sy.k = n1;
+    sy.flops = (double)sy.n * sy.n * n1;
+    x.ops.push_back(sy);
+  }
+  dist_potrf(x, off + n1, n2, level + 1, info_base + n1);  // L22 replicated on return
+}
+
+}  // namespace
+
+void build_dist_plan(int n, const PlanParams& p, const DistParams& d, std::vector<PlanOp>& ops, int64_t* send_elems,
+                     int* max_rows, int* max_cols) {
+  ops.clear();
+  DistCtx x{p, d, ops};
+  dist_potrf(x, 0, n, 0, 0);
+  if (send_elems) *send_elems = x.send_elems;
+  if (max_rows) *max_rows = x.max_rows;
+  if (max_cols) *max_cols = x.max_cols;
 }
 
 int plan_depth(int n, const PlanParams& p) {

@@ -20,18 +20,31 @@
 
 namespace relapack {
 
-enum OpKind : int { OP_POTF2 = 0, OP_TRSM = 1, OP_GEMM = 2, OP_SYRK = 3 };
+enum OpKind : int {
+  OP_POTF2 = 0, OP_TRSM = 1, OP_GEMM = 2, OP_SYRK = 3,
+  // multi-GPU steps (dist schedule only)
+  OP_PACK = 10,       // gather this rank's owned rows of a block into the send buffer
+  OP_ALLGATHER = 11,  // ncclAllGather(send, recv, m * k doubles per rank)
+  OP_UNPACK = 12      // scatter every rank's packed rows back into the matrix
+};
+
+// Buffers an op can address (L-view, same layout as the matrix).
+enum BufId : int { BUF_A = 0, BUF_SEND = 1, BUF_RECV = 2 };
 
 struct PlanOp {
   OpKind kind;
   int level;       // recursion level of the potrf node issuing it (top split = 1; base = its node's level)
-  // L-view coordinates (row, col) of the blocks, relative to the matrix origin
+  // L-view coordinates (row, col) of the blocks, relative to the buffer origin
   int c_i, c_j;    // output block (POTF2: the diagonal block; TRSM: B; GEMM/SYRK: C)
   int a_i, a_j;    // operand A (TRSM: L block; GEMM/SYRK: A)
   int b_i, b_j;    // operand B (GEMM: B; SYRK: same as A)
   int m, n, k;     // POTF2: n; TRSM: m rows, k = t; GEMM: M=m, N=n, K=k; SYRK: N=n, K=k
   int info_base;   // POTF2 only
   double flops;    // leading-term algorithmic flops of this op
+  int c_buf = BUF_A, a_buf = BUF_A, b_buf = BUF_A;
+  // PACK/UNPACK: rows [c_i, c_i + m) x cols [c_j, c_j + k) of the matrix,
+  // block-cyclic ownership with row block nb over nranks (rows counted from 0)
+  // ALLGATHER: m = rows per rank (padded), k = columns
 };
 
 struct PlanParams {
@@ -42,6 +55,34 @@ struct PlanParams {
 
 int split_point(int n, int align);
 void build_potrf_plan(int n, const PlanParams& p, std::vector<PlanOp>& ops);
+// Append the plan of potrf on the diagonal block at `off` (order n) of BUF_A.
+void append_potrf(int off, int n, int level, int info_base, const PlanParams& p, std::vector<PlanOp>& ops);
+// Append the recursive TRSM  B := B L^{-T}: L = k x k diagonal block of BUF_A
+// at (l_off, l_off); B = m x k block of buffer b_buf at (b_i, b_j).
+void append_trsm(int l_off, int b_buf, int b_i, int b_j, int m, int k, int level, const PlanParams& p,
+                 std::vector<PlanOp>& ops);
 int plan_depth(int n, const PlanParams& p);
+
+// ---- multi-GPU schedule ----
+// Row-block-cyclic ownership of L-view rows, "snake" order so every rank gets
+// an equal share of the lower triangle: block b = i / nb, round q = b / P,
+// position p = b % P; owner = p on even rounds, P - 1 - p on odd rounds.
+struct DistParams {
+  int nranks = 1, rank = 0;
+  int nb = 512;         // row block of the cyclic distribution
+  int dist_min = 4096;  // nodes smaller than this are factored redundantly on every rank
+};
+inline int dist_owner_block(int b, const DistParams& d) {
+  const int q = b / d.nranks, p = b % d.nranks;
+  return (q & 1) ? d.nranks - 1 - p : p;
+}
+inline int dist_owner(int row, const DistParams& d) { return dist_owner_block(row / d.nb, d); }
+// Rows of [lo, hi) owned by `rank` (count).
+int dist_owned_rows(int lo, int hi, int rank, const DistParams& d);
+// Build this rank's step list for the distributed factorization of order n.
+// Returns the largest packed row count times the largest column count that
+// any PACK/ALLGATHER uses (the send-buffer size in doubles) via *send_elems.
+void build_dist_plan(int n, const PlanParams& p, const DistParams& d, std::vector<PlanOp>& ops, int64_t* send_elems,
+                     int* max_rows, int* max_cols);
 
 }  // namespace relapack

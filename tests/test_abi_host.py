@@ -115,7 +115,7 @@ def test_knobs():
     with pytest.raises(ValueError):
         rl.set_split_tile(48)
     with pytest.raises(ValueError):
-        rl.set_crossover(96)  # the base case lives in one SM's shared memory: c <= 64
+        rl.set_crossover(160)  # the base case lives in one SM's shared memory: c <= 128
     rl.set_crossover(48)
     assert rl.get_crossover() == 48
     rl.set_crossover(64)
