@@ -154,6 +154,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--nb", type=int, default=512, help="multi-GPU row block")
+    ap.add_argument("--dist-min", type=int, default=8192, help="multi-GPU replicated-leaf threshold")
+    ap.add_argument("--batch-count", type=int, default=131072)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -294,7 +297,7 @@ def e2e_host(rl, P, n, uplo, steps, st, dev):
     import torch
 
     H0 = P.cpu().pin_memory()  # pinned host input (column-major view of symmetric data)
-    H = torch.empty_like(H0.t()).t().pin_memory() if False else torch.empty((n, n), dtype=torch.float64).pin_memory().t()
+    H = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
     times = []
     for i in range(steps + 1):
         H.copy_(H0)
@@ -320,15 +323,174 @@ def e2e_host(rl, P, n, uplo, steps, st, dev):
 
 
 def run_batch(args, rank, world, dev):
-    raise SystemExit("batch bench: see --config batch (added with the batched kernel measurements)")
+    """CFG[4]: 131072 independent SPD matrices, n ~ U{16,32,48,64}, 1 % indefinite;
+    the batch is split across ranks (fixed total work: strong scaling)."""
+    import numpy as np
+    import torch
+
+    import paper_1602_06763_b200 as rl
+    from inputs import gen
+
+    count = args.batch_count
+    b = gen.batched_spd(count, args.seed)
+    lo, hi = rank * count // world, (rank + 1) * count // world
+    ns = b["ns"][lo:hi]
+    offs = b["offsets"][lo:hi] - (b["offsets"][lo] if hi > lo else 0)
+    base = int(b["offsets"][lo]) if hi > lo else 0
+    end = int(b["offsets"][hi - 1] + int(b["ns"][hi - 1]) ** 2) if hi > lo else 0
+    host = b["buf"][base:end]
+    P = torch.from_numpy(host).to(dev)
+    W = torch.empty_like(P)
+    ptrs = (W.data_ptr() + 8 * torch.from_numpy(offs.astype(np.int64))).to(dev)
+    d_ns = torch.from_numpy(ns.astype(np.int32)).to(dev)
+    d_ld = d_ns.clone()
+    d_info = torch.zeros(len(ns), dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    flops = float((ns.astype(np.float64) ** 3).sum() / 3.0)
+    tri_bytes = float((8.0 * ns.astype(np.float64) * (ns + 1)).sum())  # lower triangle read + written
+
+    def step():
+        W.copy_(P)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        rl.dpotrf_batched(d_ns, ptrs, d_ld, d_info, "L", stream=st)
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        times = [step() for _ in range(args.steps)]
+    exp = b["expected_info"][lo:hi]
+    assert np.array_equal(d_info.cpu().numpy(), exp), "per-matrix info mismatch"
+    ms = sum(times) / len(times)
+    ms_max = _max_over_ranks(ms, world, dev)
+    tot_flops = float((b["ns"].astype(np.float64) ** 3).sum() / 3.0)
+    tot_bytes = float((8.0 * b["ns"].astype(np.float64) * (b["ns"] + 1)).sum())
+    if rank != 0:
+        return 0
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = tri_bytes / (ms / 1e3) / 1e9
+    out = {
+        "metric": "dpotrf FP64 GFLOP/s (n^3/3) and % of FP64 peak",
+        "value": round(tot_flops / (ms_max / 1e3) / 1e9, 2), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Philox, A_b = B_b B_b^T + n_b I, 1% with A_kk <- -A_kk)",
+        "config": {"workload": f"batched dpotrf, {count} matrices n~U{{16,32,48,64}} (BASELINE.json configs[4])",
+                   "count": count, "l2": "2 GB batch > 126 MB L2; restored from a pristine copy between steps"},
+        "roofline": {"kernel": "k_potf2_batched", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                     "note": "algorithmic bytes = lower triangles read + written once (8 n(n+1) per matrix)"},
+        "gb_per_s": round(tot_bytes / (ms_max / 1e3) / 1e9, 1),
+        "gpu_launches": args.steps, "step_times_ms": [round(t, 4) for t in times], "clocks": clk.summary(),
+        "info_parity": "per-matrix info == closed form (k+1 for the 1% negated diagonals)",
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def _max_over_ranks(v, world, dev):
+    if world == 1:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_dist(args, rank, world, dev, n, uplo, dist):
-    raise SystemExit("multi-GPU bench not available yet")
+    """One factorization sharded over the ranks: snake block-cyclic
+    row blocks of the L-view, NCCL all-gather of the solved panel rows."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1602_06763_b200 as rl
+
+    if rank == 0:
+        P = gen_matrix(n, uplo, dist, args.seed, dev)
+    else:
+        P = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+    base = torch.as_strided(P, (n * n,), (1,))
+    tdist.broadcast(base, src=0)  # identical input bits on every rank
+    W = torch.empty_like(P.t()).t()
+    uid = [rl.Comm.unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(uid, src=0)
+    comm = rl.Comm(uid[0], world, rank, torch.cuda.current_device())
+    nb, dmin = args.nb, args.dist_min
+    st = torch.cuda.current_stream(dev)
+
+    def step():
+        W.copy_(P)
+        torch.cuda.synchronize(dev)
+        tdist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        info = rl.dpotrf_dist(W, comm, uplo, nb=nb, dist_min=dmin, stream=st)
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        assert info == 0, info
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        times = [step() for _ in range(args.steps)]
+    ms = _max_over_ranks(sum(times) / len(times), world, dev)
+    sched = rl.dist_schedule(n, rank, world, nb=nb, dist_min=dmin)
+    launches = sum(1 for o in sched if o["kind"] != "allgather")
+    comm.close()
+    if rank != 0:
+        return 0
+    gflops = n ** 3 / 3.0 / (ms / 1e3) / 1e9
+    out = {
+        "metric": "dpotrf FP64 GFLOP/s (n^3/3) and % of FP64 peak",
+        "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Philox B, A = B B^T + n I)",
+        "config": {"workload": f"single dpotrf n={n} uplo={uplo} sharded over {world} GPUs",
+                   "n": n, "uplo": uplo, "nb": nb, "dist_min": dmin, "parallelism": f"rowblock-cyclic x{world}",
+                   "l2": "input > L2; restored from a pristine copy between steps (untimed)"},
+        "pct_fp64_peak_per_gpu": round(100 * gflops / 1e3 / FP64_PEAK_TFLOPS_DATASHEET / world, 2),
+        "gpu_launches": launches * args.steps, "step_times_ms": [round(t, 4) for t in times],
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def _host_panel(n, J, seed, dist, uplo):
+    """Host copy of the part of A the oracle's first J columns read: L-view
+    columns 0..J-1 (A = B B^T + n I with the same row-panel Philox draws as
+    inputs.gen.spd_torch)."""
+    import numpy as np
+
+    from inputs import gen
+
+    panel = 4096
+    B = np.empty((n, n))
+    for p, r0 in enumerate(range(0, n, panel)):
+        r1 = min(n, r0 + panel)
+        B[r0:r1] = gen.draw_B(r1 - r0, seed, dist, m=n, stream=1 + p)
+    C = B @ B[:J].T  # n x J: columns 0..J-1 of B B^T
+    C[np.arange(J), np.arange(J)] += float(n)
+    A = np.zeros((n, n), order="F")
+    if uplo == "L":
+        A[:, :J] = C
+    else:
+        A[:J, :] = C.T
+    return A
 
 
 def run_reference(args, rank, n, uplo, dist, cfg_idx, world):
-    """The oracle (as it stands) on the host cores, bounded sample of the same workload."""
+    """--impl reference: the oracle (as it stands) on the box's host cores, each
+    step a bounded sample of the same workload (rank 0 only)."""
     if rank != 0:
         return 0
     import numpy as np
@@ -337,20 +499,60 @@ def run_reference(args, rank, n, uplo, dist, cfg_idx, world):
     from inputs import gen
 
     oracle.build()
-    A = gen.spd(n, args.seed, dist) if n <= 4096 else None
-    if A is None:
-        # same recipe on the host; the product B B^T of the full matrix is skipped by
-        # sampling rows: the oracle's first J columns only read the first J rows/cols
-        # of A (left-looking), so a J x n panel of A is generated exactly.
-        pass
-    times = []
-    J = None
-    res = None
-    for i in range(args.warmup + args.steps):
-        if A is not None:
-            res = cpu_oracle_sample(A, n, uplo, target_s=6.0)
-    out = {"impl": "reference", "metric": "dpotrf FP64 GFLOP/s (n^3/3) and % of FP64 peak",
-           "value": res["value"] if res else None, "unit": "GFLOP/s"}
+    if args.config == "batch":
+        b = gen.batched_spd(args.batch_count, args.seed)
+        S = 8192
+        ns, offs = b["ns"][:S], b["offsets"][:S]
+        end = int(offs[-1] + int(ns[-1]) ** 2)
+        sample_flops = float((ns.astype(np.float64) ** 3).sum() / 3.0)
+        times = []
+        for i in range(args.warmup + args.steps):
+            buf = b["buf"][:end].copy()
+            t0 = time.perf_counter()
+            oracle.dpotrf_batched("L", ns, buf, offs, ns)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+        sample = f"first {S} of {args.batch_count} matrices of the CFG[4] batch"
+        workload = f"batched dpotrf, {args.batch_count} matrices n~U{{16,32,48,64}} (BASELINE.json configs[4])"
+    else:
+        J = min(n, 256)
+        A = _host_panel(n, max(J, min(n, 2048)), args.seed, dist, uplo)
+        Jmax = max(J, min(n, 2048))
+        # size the sample: ~3 s per step
+        while True:
+            X = np.array(A, order="F")
+            t0 = time.perf_counter()
+            oracle.dpotrf_cols(X, uplo, J)
+            dt = time.perf_counter() - t0
+            if dt > 0.75 or J >= Jmax:
+                break
+            J = min(Jmax, J * 2)
+        sample_flops = sum(2.0 * j * (n - j) for j in range(J))
+        times = []
+        for i in range(args.warmup + args.steps):
+            X = np.array(A, order="F")
+            t0 = time.perf_counter()
+            info = oracle.dpotrf_cols(X, uplo, J)
+            dt = time.perf_counter() - t0
+            assert info == 0
+            if i >= args.warmup:
+                times.append(dt)
+        sample = (f"first {J} of {n} columns of the n={n} uplo={uplo} factorization "
+                  f"(left-looking triple loop, {sample_flops:.3e} flops per step)")
+        workload = f"single dpotrf n={n} uplo={uplo} B~{dist} (BASELINE.json configs[{cfg_idx}])"
+    sec = sum(times) / len(times)
+    val = sample_flops / sec / 1e9
+    out = {
+        "impl": "reference", "metric": "dpotrf FP64 GFLOP/s (n^3/3) and % of FP64 peak",
+        "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sec, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded Philox)",
+        "config": {"workload": workload, "n": n, "uplo": uplo},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
     print(json.dumps(out))
     return 0
 

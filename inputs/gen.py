@@ -86,11 +86,19 @@ def spd_torch(n: int, seed: int, dist: str = "uniform", lda: int | None = None, 
     import torch
 
     lda = n if lda is None else lda
-    B = torch.from_numpy(draw_B(n, seed, dist)).to(device)
+    panel = 4096  # B is drawn in row panels, panel p from Philox stream 1 + p (any panel is independent)
+    B = torch.empty((n, n), dtype=torch.float64, device=device)
+    for p, r0 in enumerate(range(0, n, panel)):
+        r1 = min(n, r0 + panel)
+        B[r0:r1] = torch.from_numpy(draw_B(r1 - r0, seed, dist, m=n, stream=1 + p)).to(device)
     M = B @ B.T
     del B
-    M = torch.tril(M)
-    M = M + torch.tril(M, -1).T
+    # exact symmetry: mirror the lower triangle onto the upper one, tile by tile (in place)
+    for i0 in range(0, n, panel):
+        for j0 in range(i0 + panel, n, panel):
+            M[i0:i0 + panel, j0:j0 + panel] = M[j0:j0 + panel, i0:i0 + panel].T
+        blk = M[i0:i0 + panel, i0:i0 + panel]
+        blk.copy_(torch.tril(blk) + torch.tril(blk, -1).T)
     M.diagonal().add_(float(n))
     # M is symmetric, so its row-major storage equals the column-major one.
     if lda == n:

@@ -41,6 +41,50 @@
                           : ((size_t)(j) + (size_t)(i) * (size_t)lda))
 
 /*
+ * update_column — a(j:n-1, j) -= sum_{k<j} a(j:n-1, k) * a(j, k), one
+ * subtraction per term in ascending k for every element (the "jki" loop of the
+ * left-looking algorithm).  Threads own disjoint row ranges; the
+ * loop nest is ordered so the innermost index walks contiguous memory (rows
+ * for 'L', k for 'U').  The per-element operation sequence is the same in
+ * both orders, so the result is bitwise independent of order and threads.
+ */
+static void update_column(int lower, int n, double* A, int lda, int j) {
+  if (lower) {
+#pragma omp parallel if (n - j > 512)
+    {
+      int nt = 1, t = 0;
+#ifdef _OPENMP
+      extern int omp_get_num_threads(void);
+      extern int omp_get_thread_num(void);
+      nt = omp_get_num_threads();
+      t = omp_get_thread_num();
+#endif
+      const int rows = n - j;
+      const int i0 = j + (int)((long long)rows * t / nt), i1 = j + (int)((long long)rows * (t + 1) / nt);
+      double* aj = A + (size_t)j * (size_t)lda;
+      for (int k = 0; k < j; ++k) {
+        const double* ak = A + (size_t)k * (size_t)lda;
+        const double ajk = ak[j];
+        for (int i = i0; i < i1; ++i) {
+          double p = ak[i] * ajk;
+          aj[i] = aj[i] - p;
+        }
+      }
+    }
+  } else {
+#pragma omp parallel for schedule(static) if (n - j > 512)
+    for (int i = j; i < n; ++i) {
+      double s = A[LIDX(i, j)];
+      for (int k = 0; k < j; ++k) {
+        double p = A[LIDX(i, k)] * A[LIDX(j, k)];
+        s = s - p;
+      }
+      A[LIDX(i, j)] = s;
+    }
+  }
+}
+
+/*
  * oracle_dpotrf — unblocked Cholesky, left-looking column form.
  *   for j = 0..n-1:
  *     for k = 0..j-1: for i = j..n-1: a(i,j) = a(i,j) - a(i,k)*a(j,k)
@@ -58,17 +102,7 @@ int oracle_dpotrf(char uplo, int n, double* A, int lda) {
   if (n < 0) return -2;
   if (lda < (n > 1 ? n : 1)) return -4;
   for (int j = 0; j < n; ++j) {
-    /* a(j:n-1, j) -= sum_{k<j} a(j:n-1, k) * a(j, k), ascending k per element.
-     * Threads own disjoint row ranges; each element sees the same k order. */
-#pragma omp parallel for schedule(static) if (n - j > 512)
-    for (int i = j; i < n; ++i) {
-      double s = A[LIDX(i, j)];
-      for (int k = 0; k < j; ++k) {
-        double p = A[LIDX(i, k)] * A[LIDX(j, k)];
-        s = s - p;
-      }
-      A[LIDX(i, j)] = s;
-    }
+    update_column(lower, n, A, lda, j);
     double d = A[LIDX(j, j)];
     if (!(d > 0.0)) return j + 1; /* catches d <= 0, -0.0 and NaN */
     d = sqrt(d);
@@ -90,15 +124,7 @@ int oracle_dpotrf_cols(char uplo, int n, double* A, int lda, int ncols) {
   if (lda < (n > 1 ? n : 1)) return -4;
   if (ncols > n) ncols = n;
   for (int j = 0; j < ncols; ++j) {
-#pragma omp parallel for schedule(static) if (n - j > 512)
-    for (int i = j; i < n; ++i) {
-      double s = A[LIDX(i, j)];
-      for (int k = 0; k < j; ++k) {
-        double p = A[LIDX(i, k)] * A[LIDX(j, k)];
-        s = s - p;
-      }
-      A[LIDX(i, j)] = s;
-    }
+    update_column(lower, n, A, lda, j);
     double d = A[LIDX(j, j)];
     if (!(d > 0.0)) return j + 1;
     d = sqrt(d);

@@ -234,9 +234,13 @@ class Comm:
             self.ptr = ctypes.c_void_p()
 
 
-def dpotrf_dist(A, comm: "Comm", uplo: str = "L", nb: int = 512, dist_min: int = 4096) -> int:
+def dpotrf_dist(A, comm: "Comm", uplo: str = "L", nb: int = 512, dist_min: int = 4096, stream=None) -> int:
     """Distributed factorization of the device matrix A (identical on every rank); returns info."""
+    import torch
+
     ptr, n, lda = _matrix_args(A)
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    lib().relapack_set_stream(ctypes.c_void_p(st.cuda_stream))
     info = ctypes.c_int(0)
     lib().relapack_dpotrf_dist(uplo.encode(), ctypes.byref(ctypes.c_int(n)), ctypes.c_void_p(ptr),
                                ctypes.byref(ctypes.c_int(lda)), nb, dist_min, comm.ptr, ctypes.byref(info))
