@@ -84,6 +84,29 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+// 1/sqrt(d) for a positive normal d: hardware approximation (MUFU.RSQ64H) +
+// two branch-free Newton steps (~1 ulp); short dependent chain for the
+// pivot step of the base-case factorizations.
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double e = fma(-h * y, y, 0.5);
+    y = fma(y, e, y);
+  }
+  return y;
+}
+
+// sqrt(d) from y ~ 1/sqrt(d): r = d*y corrected by one fma-exact residual step
+// (branch-free; exact for perfect squares, within an ulp otherwise).
+__device__ __forceinline__ double sqrt_from_rsqrt(double d, double y) {
+  const double r = d * y;
+  const double e = fma(-r, r, d);
+  return fma(e, 0.5 * y, r);
+}
+
 __device__ __forceinline__ int ld_info(const int* d_info) {
   return *reinterpret_cast<const volatile int*>(d_info);
 }

@@ -1,6 +1,5 @@
-// potf2.cu — K1 (base case of the recursion, order n <= 128) and K2 (batched
-// small factorizations, n <= 64): Cholesky of a block held entirely in one
-// SM's shared memory (north_star subsystem (2); P:301-307 crossover to the
+// potf2.cu — K1 (base case of the recursion, order n <= 128): Cholesky of a
+// block held entirely in one SM's shared memory (north_star subsystem (2); P:301-307 crossover to the
 // unblocked kernel; "the unblocked kernel is slightly faster ...
 // within the processor's L1 cache" -> on the GPU: within shared memory).
 //
@@ -34,28 +33,6 @@ __device__ long long g_probe[64];
 #else
 #define PROBE(k)
 #endif
-
-// 1/sqrt(d) for a positive normal d: hardware approximation + 2 Newton steps
-// (no special-case branches on the critical path; ~1 ulp).
-__device__ __forceinline__ double rsqrt_nr(double d) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  const double h = 0.5 * d;
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const double e = fma(-h * y, y, 0.5);
-    y = fma(y, e, y);
-  }
-  return y;
-}
-
-// sqrt(d) from y ~ 1/sqrt(d): r = d*y corrected by one fma-exact residual step
-// (branch-free; exact for perfect squares, within an ulp otherwise).
-__device__ __forceinline__ double sqrt_from_rsqrt(double d, double y) {
-  const double r = d * y;
-  const double e = fma(-r, r, d);
-  return fma(e, 0.5 * y, r);
-}
 
 template <int NMAX>
 struct P2 {
@@ -334,42 +311,13 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
 }
 
-__global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_batched(int layout, int batch, const int* d_n,
-                                                                   double* const* d_A, const int* d_lda, int* d_info) {
-  const int b = blockIdx.x;
-  if (b >= batch) return;
-  const int n = d_n[b];
-  const int lda = d_lda[b];
-  if (n < 0 || n > RELAPACK_BATCH_NMAX_) {
-    if (threadIdx.x == 0) d_info[b] = -2;
-    return;
-  }
-  if (lda < (n > 1 ? n : 1)) {
-    if (threadIdx.x == 0) d_info[b] = -4;
-    return;
-  }
-  extern __shared__ double s[];
-  __shared__ int fail_flag;
-  if (threadIdx.x == 0) fail_flag = 0;
-  double* A = d_A[b];
-  int fail = 0;
-  if (n > 0) {
-    copy_lower<64, true>(s, A, lda, layout, n);
-    __syncthreads();
-    fail = potf2_smem<64>(s, n, &fail_flag);
-    copy_lower<64, false>(s, A, lda, layout, n);
-  }
-  if (threadIdx.x == 0) d_info[b] = fail;
-}
-
 }  // namespace
 
 cudaError_t configure_potf2() {
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
   cudaError_t e = cudaFuncSetAttribute(k_potf2_base, attr, (int)P2<kBaseMax>::SMEM);
   if (e != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_potf2_base64, attr, (int)P2<64>::SMEM)) != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_potf2_batched, attr, (int)P2<64>::SMEM);
+  return cudaFuncSetAttribute(k_potf2_base64, attr, (int)P2<64>::SMEM);
 }
 
 cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, int info_base, cudaStream_t st) {
@@ -379,13 +327,6 @@ cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, 
     k_potf2_base64<<<1, P2<64>::THREADS, P2<64>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
   else
     k_potf2_base<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* const* d_A, const int* d_lda,
-                                 int* d_info, cudaStream_t st) {
-  if (batch <= 0) return cudaSuccess;
-  k_potf2_batched<<<batch, P2<64>::THREADS, P2<64>::SMEM, st>>>(layout, batch, d_n, d_A, d_lda, d_info);
   return cudaGetLastError();
 }
 
