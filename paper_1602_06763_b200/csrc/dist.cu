@@ -252,7 +252,7 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
         break;
       case OP_TRSM: {
         double* B = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
-        e = launch_trsm_base(A + lv_off(layout, op.a_i, op.a_j, lda), lda, B, ldc, layout, op.m, op.k, d_info, st);
+        e = launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, lda), lda, B, ldc, layout, op.m, op.k, d_info, st);
         break;
       }
       case OP_GEMM:
@@ -270,6 +270,8 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
         a.N = op.n;
         u.tile = update_tile_for(a.M, a.N, a.tri);
         a.tiles_m = (a.M + u.tile - 1) / u.tile;
+        a.ntiles = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * ((a.N + u.tile - 1) / u.tile);
+        a.ksplit = 1;
         a.A = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, dp.send, pad, nc, &lda_);
         a.lda = lda_;
         a.B = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, dp.send, pad, nc, &ldb);
@@ -575,7 +577,7 @@ int relapack_dist_schedule(int n, int c, int T, int nb, int dist_min, int rank, 
   PlanParams p;
   p.crossover = c;
   p.split_tile = T;
-  p.trsm_base = kTrsmMax;
+  p.trsm_base = kTrsmFusedMax;
   DistParams d;
   d.nranks = nranks;
   d.rank = rank;

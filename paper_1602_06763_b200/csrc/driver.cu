@@ -69,9 +69,11 @@ PlanParams current_params() {
   if (t != 8 && t != 16 && t != 32 && t != 64 && t != 128) t = 64;
   p.crossover = c;
   p.split_tile = t;
-  p.trsm_base = kTrsmMax;
+  p.trsm_base = kTrsmFusedMax;
   return p;
 }
+
+static bool splitk_enabled() { return env_int("RELAPACK_SPLITK", 1) != 0; }
 
 static bool graphs_enabled() {
   int g = g_graphs.load();
@@ -84,8 +86,12 @@ struct Plan {
   std::vector<PlanOp> ops;
   std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
   cudaGraphExec_t exec = nullptr;
+  double* splitk_ws = nullptr;  // split-K partial tiles (shared by the plan's sequential updates)
+  int* splitk_cnt = nullptr;    // per-tile arrival counters (self-resetting)
   ~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
+    if (splitk_ws) cudaFree(splitk_ws);
+    if (splitk_cnt) cudaFree(splitk_cnt);
   }
 };
 
@@ -150,12 +156,43 @@ static void fill_update(UpdateOp& u, const PlanOp& op, double* A, int64_t ld, in
   }
   u.tile = update_tile_for(a.M, a.N, a.tri);
   a.tiles_m = (a.M + u.tile - 1) / u.tile;
+  const int tiles_n = (a.N + u.tile - 1) / u.tile;
+  a.ntiles = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * tiles_n;
+  a.ksplit = 1;
   a.A = A + lv_off(layout, op.a_i, op.a_j, ld);
   a.lda = ld;
   a.B = A + lv_off(layout, op.b_i, op.b_j, ld);
   a.ldb = ld;
   u.use_tma = make_operand_map(&u.tmA, a.A, ld, layout, a.M, a.K, u.tile) &&
               make_operand_map(&u.tmB, a.B, ld, layout, a.N, a.K, u.tile);
+}
+
+// Enable split-K on the plan's small-grid / long-K updates and give them the
+// shared workspace (the plan's kernels run one after another).
+static cudaError_t setup_splitk(Plan& p) {
+  int64_t ws = 0;
+  int cnt = 0;
+  for (size_t i = 0; i < p.ops.size(); ++i) {
+    if (p.ops[i].kind != OP_GEMM && p.ops[i].kind != OP_SYRK) continue;
+    UpdateArgs& a = p.upd[i].args;
+    const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, p.upd[i].tile);
+    if (ks <= 1) continue;
+    a.ksplit = ks;
+    const int64_t e = update_ws_elems(a.M, a.N, a.tri, p.upd[i].tile, ks);
+    ws = e > ws ? e : ws;
+    cnt = a.ntiles > cnt ? a.ntiles : cnt;
+  }
+  if (ws == 0) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaMalloc(&p.splitk_ws, ws * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p.splitk_cnt, cnt * sizeof(int))) != cudaSuccess) return e;
+  if ((e = cudaMemset(p.splitk_cnt, 0, cnt * sizeof(int))) != cudaSuccess) return e;
+  for (size_t i = 0; i < p.ops.size(); ++i) {
+    if (p.ops[i].kind != OP_GEMM && p.ops[i].kind != OP_SYRK) continue;
+    p.upd[i].args.ws = p.splitk_ws;
+    p.upd[i].args.counters = p.splitk_cnt;
+  }
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ profiling
@@ -206,8 +243,8 @@ static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, in
         e = launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
         break;
       case OP_TRSM:
-        e = launch_trsm_base(A + lv_off(layout, op.a_i, op.a_j, ld), ld, A + lv_off(layout, op.c_i, op.c_j, ld), ld,
-                             layout, op.m, op.k, d_info, st);
+        e = launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, ld), ld, A + lv_off(layout, op.c_i, op.c_j, ld), ld,
+                            layout, op.m, op.k, d_info, st);
         break;
       case OP_GEMM:
       case OP_SYRK:
@@ -245,6 +282,7 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
     p->upd.resize(p->ops.size());
     for (size_t i = 0; i < p->ops.size(); ++i)
       if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
+    if (splitk_enabled() && (e = setup_splitk(*p)) != cudaSuccess) return cuda_fail(e, "split-K workspace");
     if (use_graph) {
       cudaGraph_t g = nullptr;
       if ((e = cudaStreamBeginCapture(ds->capture, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
@@ -515,7 +553,7 @@ int relapack_plan_ledger(int n, int c, int T, int levels, double* flops_by_level
   PlanParams p;
   p.crossover = c;
   p.split_tile = T;
-  p.trsm_base = kTrsmMax;
+  p.trsm_base = kTrsmFusedMax;
   std::vector<PlanOp> ops;
   build_potrf_plan(n, p, ops);
   if (flops_by_level)

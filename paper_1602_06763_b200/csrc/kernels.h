@@ -23,6 +23,13 @@ struct UpdateArgs {
   int64_t lda;
   const double* B;
   int64_t ldb;
+  // deterministic split-K: grid = ntiles * ksplit; split s covers k-tiles
+  // [s*per, (s+1)*per); partial tiles go to ws, the last CTA of a tile (per
+  // counters[tile], self-resetting) sums them in split order and applies C -=.
+  int ksplit;         // 1 = no split
+  int ntiles;
+  double* ws;         // ksplit * ntiles * tile^2 doubles
+  int* counters;      // ntiles ints, zero between launches
 };
 
 struct UpdateOp {
@@ -35,6 +42,10 @@ struct UpdateOp {
 cudaError_t launch_update(const UpdateOp& op, cudaStream_t st);
 bool make_operand_map(CUtensorMap* map, const double* base, int64_t ld, int layout, int rows, int K, int box_rows);
 int update_tile_for(int M, int N, int tri);
+// Split-K factor for an update of (M, N, K) on `tile` x `tile` CTA tiles (1 = none)
+// and the workspace it needs (doubles) — see update.cu.
+int update_ksplit_for(int M, int N, int K, int tri, int tile);
+int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit);
 
 // ---- K1 base-case potf2 (potf2.cu) ----
 // Factor the n x n L-view block at A (n <= kPotf2Max) in shared memory; on a
@@ -46,6 +57,19 @@ cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, 
 constexpr int kTrsmMax = 64;
 cudaError_t launch_trsm_base(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                              const int* d_info, cudaStream_t st);
+
+// ---- K5' fused TRSM base (trsm_fused.cu): t <= kTrsmFusedMax columns in one launch
+constexpr int kTrsmFusedMax = 256;
+cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
+                              const int* d_info, cudaStream_t st);
+cudaError_t configure_trsm_fused();
+// TRSM base dispatch (measured, profiles/): the row-parallel K5 for t <= 64 on
+// short panels, the chunked DMMA K5' otherwise.
+inline cudaError_t launch_trsm_any(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
+                                   const int* d_info, cudaStream_t st) {
+  return (t <= kTrsmMax && m < 2048) ? launch_trsm_base(L, ldl, B, ldb, layout, m, t, d_info, st)
+                                     : launch_trsm_fused(L, ldl, B, ldb, layout, m, t, d_info, st);
+}
 
 // ---- K2 batched potf2 (batched.cu)
 cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* const* d_A, const int* d_lda,
@@ -59,6 +83,7 @@ inline cudaError_t configure_kernels() {
   cudaError_t e = configure_update();
   if (e == cudaSuccess) e = configure_potf2();
   if (e == cudaSuccess) e = configure_trsm();
+  if (e == cudaSuccess) e = configure_trsm_fused();
   return e;
 }
 

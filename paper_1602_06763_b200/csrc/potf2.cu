@@ -90,32 +90,35 @@ __device__ __forceinline__ void trail_tiles(double* s, int j0, int r0, int tile_
 // the tiles (ti, 0) of the trailing grid, all in flight at once (warp 0).
 template <int NMAX, int LDS>
 __device__ __forceinline__ void strip_update(double* s, int n, int j0, int r0, int g, int t) {
-  constexpr int TMAX = NMAX / 8;
+  constexpr int TMAX = NMAX / 8, QB = TMAX < 8 ? TMAX : 8;  // tiles in flight (register budget)
   const int T = (n - r0 + 7) / 8;
-  double c0[TMAX], c1[TMAX];
+#pragma unroll 1
+  for (int q0 = 0; q0 < T; q0 += QB) {
+    double c0[QB], c1[QB];
 #pragma unroll
-  for (int q = 0; q < TMAX; ++q) {
-    if (q < T) {
-      c0[q] = s[(r0 + 8 * q + g) + (r0 + 2 * t) * LDS];
-      c1[q] = s[(r0 + 8 * q + g) + (r0 + 2 * t + 1) * LDS];
-    }
-  }
-#pragma unroll
-  for (int ks = 0; ks < 2; ++ks) {
-    const double b = s[(r0 + g) + (j0 + 4 * ks + t) * LDS];
-#pragma unroll
-    for (int q = 0; q < TMAX; ++q) {
-      if (q < T) {
-        const double a = -s[(r0 + 8 * q + g) + (j0 + 4 * ks + t) * LDS];
-        dmma_884(c0[q], c1[q], a, b);
+    for (int q = 0; q < QB; ++q) {
+      if (q0 + q < T) {
+        c0[q] = s[(r0 + 8 * (q0 + q) + g) + (r0 + 2 * t) * LDS];
+        c1[q] = s[(r0 + 8 * (q0 + q) + g) + (r0 + 2 * t + 1) * LDS];
       }
     }
-  }
 #pragma unroll
-  for (int q = 0; q < TMAX; ++q) {
-    if (q < T) {
-      s[(r0 + 8 * q + g) + (r0 + 2 * t) * LDS] = c0[q];
-      s[(r0 + 8 * q + g) + (r0 + 2 * t + 1) * LDS] = c1[q];
+    for (int ks = 0; ks < 2; ++ks) {
+      const double b = s[(r0 + g) + (j0 + 4 * ks + t) * LDS];
+#pragma unroll
+      for (int q = 0; q < QB; ++q) {
+        if (q0 + q < T) {
+          const double a = -s[(r0 + 8 * (q0 + q) + g) + (j0 + 4 * ks + t) * LDS];
+          dmma_884(c0[q], c1[q], a, b);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < QB; ++q) {
+      if (q0 + q < T) {
+        s[(r0 + 8 * (q0 + q) + g) + (r0 + 2 * t) * LDS] = c0[q];
+        s[(r0 + 8 * (q0 + q) + g) + (r0 + 2 * t + 1) * LDS] = c1[q];
+      }
     }
   }
 }
@@ -251,7 +254,9 @@ __device__ __forceinline__ void copy_lower(double* s, double* __restrict__ A, in
   using C = P2<NMAX>;
   constexpr int kBatch = 16;
   constexpr int kPer = NMAX * NMAX / C::THREADS;  // 32 (64) or 64 (128)
-#pragma unroll
+  // NMAX = 128: not unrolled, so the index math is recomputed per batch
+  // instead of being kept live (spilled) across the kernel for the copy back
+#pragma unroll(NMAX <= 64 ? kPer / kBatch : 1)
   for (int u0 = 0; u0 < kPer; u0 += kBatch) {
     double v[kBatch];
 #pragma unroll

@@ -1,0 +1,205 @@
+// trsm_fused.cu — K5: the base case of the recursive TRSM, up to 256 columns
+// in ONE launch (north_star subsystem (3); SPEC trsm
+// Right/Lower/Trans/NonUnit):
+//     B (m x t) := B * L^{-T},   t <= 256,
+// every row x of the result solving x L^T = b by forward substitution
+//     x_j = (b_j - sum_{k<j} x_k L_jk) * (1 / L_jj).
+//
+// Organisation.  A CTA owns 64 rows of B (8 warps x 8 rows); its slab stays in
+// shared memory for the whole solve.  Columns are walked in 64-wide chunks
+// (left-looking): a warp holds its 8 rows of the current chunk as eight 8x8
+// DMMA accumulator fragments (lane (g, t) holds X[g][2t], X[g][2t+1] of every
+// 8x8 sub-block) and
+//   (a) accumulates X_cb -= X_pb L_{cb,pb}^T for the earlier chunks pb on the
+//       FP64 tensor cores (mma.sync m8n8k4 f64, A from the slab, B from the
+//       staged 64x64 L block);
+//   (b) solves the chunk's diagonal block sub-block by sub-block: the 8 columns
+//       of a sub-block by quad shuffles (the owner lane of column c scales it,
+//       the 4 lanes of each row group update their two columns — one
+//       instruction stream serves 8 rows; chain = shuffle -> multiply -> FMA),
+//       then X_{s'} -= X_s L_{s',s}^T on DMMA for the later sub-blocks.
+// Shared-memory strides are 4 (mod 32) doubles so every fragment read hits
+// each bank pair exactly twice.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace relapack {
+
+namespace {
+
+constexpr int kFC = 64;                  // chunk width
+constexpr int kFTmax = kTrsmFusedMax;    // 256
+constexpr int kFRows = 64;               // rows per CTA
+constexpr int kFWarps = 8;               // 8 rows per warp
+constexpr int kFThreads = kFWarps * 32;
+constexpr int kFLdX = kFTmax + 4;        // slab row stride  (== 4 mod 32)
+constexpr int kFLdL = kFC + 4;           // L block row stride (== 4 mod 32)
+constexpr size_t kFSmem = sizeof(double) * ((size_t)kFRows * kFLdX + (size_t)kFC * kFLdL + kFC);
+
+#ifdef RELAPACK_PROBE  // phase timestamps for tools/microbench only
+__device__ long long g_tprobe[64];
+#define TPROBE(k) \
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_tprobe[k] = clock64();
+#else
+#define TPROBE(k)
+#endif
+
+// Stage the 64x64 block of L with rows [r0, r0+64) and cols [c0, c0+64) into
+// sL[j * kFLdL + k] = L(r0 + j, c0 + k), zero outside [0, t) and, for the
+// diagonal block, on/above the diagonal (1/L_jj goes to rinv).
+__device__ __forceinline__ void stage_L(double* sL, double* rinv, const double* __restrict__ L, int64_t ldl,
+                                        int layout, int t, int r0, int c0, bool diag) {
+  constexpr int kPer = kFC * kFC / kFThreads;  // 16
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = threadIdx.x + u * kFThreads;
+    const int a = e & (kFC - 1), b = e >> 6;  // a: contiguous index
+    const int j = layout == kLayoutN ? a : b, k = layout == kLayoutN ? b : a;
+    const int gi = r0 + j, gk = c0 + k;
+    v[u] = (gi < t && gk < t && (!diag || gi >= gk)) ? L[lv_off(layout, gi, gk, ldl)] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = threadIdx.x + u * kFThreads;
+    const int a = e & (kFC - 1), b = e >> 6;
+    const int j = layout == kLayoutN ? a : b, k = layout == kLayoutN ? b : a;
+    if (diag && j == k) rinv[j] = (r0 + j < t) ? 1.0 / v[u] : 0.0;
+    sL[j * kFLdL + k] = (diag && j <= k) ? 0.0 : v[u];
+  }
+}
+
+__global__ void __launch_bounds__(kFThreads, 1) k_trsm_fused(const double* __restrict__ L, int64_t ldl,
+                                                              double* __restrict__ B, int64_t ldb, int layout, int m,
+                                                              int t, const int* d_info) {
+  TPROBE(0);
+  if (ld_info(d_info) != 0) return;
+  extern __shared__ double smem_t[];
+  double* sX = smem_t;                   // sX[r * kFLdX + c]
+  double* sL = sX + kFRows * kFLdX;      // current 64x64 L block
+  double* sRinv = sL + kFC * kFLdL;      // 1 / L_jj of the current diagonal chunk
+  const int row0 = blockIdx.x * kFRows;
+  const int rows = min(kFRows, m - row0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wrow = warp * 8;             // this warp's first slab row
+
+  // ---- stage the slab (coalesced along the contiguous index; 16 loads in flight)
+  {
+    const int total = kFRows * t;
+    for (int e0 = tid; e0 < total; e0 += kFThreads * 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = e0 + u * kFThreads;
+        const int r = layout == kLayoutN ? e % kFRows : e / t, c = layout == kLayoutN ? e / kFRows : e % t;
+        v[u] = (e < total && r < rows) ? B[lv_off(layout, row0 + r, c, ldb)] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = e0 + u * kFThreads;
+        const int r = layout == kLayoutN ? e % kFRows : e / t, c = layout == kLayoutN ? e / kFRows : e % t;
+        if (e < total) sX[r * kFLdX + c] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  TPROBE(1);
+
+  const int nc = (t + kFC - 1) / kFC;
+  for (int cb = 0; cb < nc; ++cb) {
+    const int cbase = cb * kFC;
+    // this warp's 8 rows of chunk cb as eight 8x8 C fragments
+    double xs[8][2];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      xs[s][0] = sX[(wrow + g) * kFLdX + cbase + 8 * s + 2 * tq];
+      xs[s][1] = sX[(wrow + g) * kFLdX + cbase + 8 * s + 2 * tq + 1];
+    }
+    // ---- (a) X_cb -= X_pb L_{cb,pb}^T, pb < cb
+    for (int pb = 0; pb < cb; ++pb) {
+      __syncthreads();  // sL free
+      stage_L(sL, sRinv, L, ldl, layout, t, cbase, pb * kFC, false);
+      __syncthreads();
+#pragma unroll 4
+      for (int k0 = 0; k0 < kFC; k0 += 4) {
+        const double a = -sX[(wrow + g) * kFLdX + pb * kFC + k0 + tq];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) dmma_884(xs[s][0], xs[s][1], a, sL[(8 * s + g) * kFLdL + k0 + tq]);
+      }
+    }
+    // ---- (b) solve the diagonal chunk
+    __syncthreads();
+    stage_L(sL, sRinv, L, ldl, layout, t, cbase, cbase, true);
+    __syncthreads();
+    TPROBE(2 + 2 * cb);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      // columns 8s .. 8s+7: the owner lane (quad position c/2) of column c
+      // broadcasts x_c to its quad; each lane updates its columns 2t, 2t+1
+      double l0[8], l1[8], rc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        l0[c] = sL[(8 * s + 2 * tq) * kFLdL + 8 * s + c];      // L(8s+2t,   8s+c), 0 unless 2t > c
+        l1[c] = sL[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c];  // L(8s+2t+1, 8s+c)
+        rc[c] = sRinv[8 * s + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double xj = __shfl_sync(0xffffffffu, (c & 1) ? xs[s][1] : xs[s][0], (lane & ~3) | (c >> 1)) * rc[c];
+        xs[s][0] -= xj * l0[c];
+        xs[s][1] -= xj * l1[c];
+        if (tq == (c >> 1)) {
+          if (c & 1)
+            xs[s][1] = xj;
+          else
+            xs[s][0] = xj;
+        }
+      }
+      // X_{s'} -= X_s L_{s',s}^T for s' > s: A fragment of X_s from the quad
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int src = (lane & ~3) | (2 * ks + (tq >> 1));
+        const double e0 = __shfl_sync(0xffffffffu, xs[s][0], src);
+        const double e1 = __shfl_sync(0xffffffffu, xs[s][1], src);
+        const double a = -((tq & 1) ? e1 : e0);  // -X_s[g][4ks + tq]
+#pragma unroll
+        for (int s2 = s + 1; s2 < 8; ++s2)
+          dmma_884(xs[s2][0], xs[s2][1], a, sL[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      sX[(wrow + g) * kFLdX + cbase + 8 * s + 2 * tq] = xs[s][0];
+      sX[(wrow + g) * kFLdX + cbase + 8 * s + 2 * tq + 1] = xs[s][1];
+    }
+    TPROBE(3 + 2 * cb);
+  }
+  __syncthreads();
+  // ---- write the slab back
+  {
+    const int total = kFRows * t;
+    for (int e = tid; e < total; e += kFThreads) {
+      const int r = layout == kLayoutN ? e % kFRows : e / t, c = layout == kLayoutN ? e / kFRows : e % t;
+      if (r < rows) B[lv_off(layout, row0 + r, c, ldb)] = sX[r * kFLdX + c];
+    }
+  }
+  TPROBE(20);
+}
+
+}  // namespace
+
+cudaError_t configure_trsm_fused() {
+  return cudaFuncSetAttribute(k_trsm_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem);
+}
+
+cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
+                              const int* d_info, cudaStream_t st) {
+  if (m <= 0 || t <= 0) return cudaSuccess;
+  if (t > kFTmax) return cudaErrorInvalidValue;
+  const int grid = (m + kFRows - 1) / kFRows;
+  k_trsm_fused<<<grid, kFThreads, kFSmem, st>>>(L, ldl, B, ldb, layout, m, t, d_info);
+  return cudaGetLastError();
+}
+
+}  // namespace relapack

@@ -95,9 +95,9 @@ __device__ __forceinline__ void fill_tile_ldg(uint8_t* tile, const double* X, in
 
 template <int LAYOUT, int TBM>
 __device__ __forceinline__ void issue_stage(uint8_t* smem, uint64_t* full, const CUtensorMap* tmA,
-                                            const CUtensorMap* tmB, int kt, int m0, int n0) {
+                                            const CUtensorMap* tmB, int it, int kt, int m0, int n0) {
   using C = Cfg<TBM>;
-  const int s = kt % STAGES;
+  const int s = it % STAGES;
   uint8_t* sa = smem + s * C::STAGE_BYTES;
   uint8_t* sb = sa + C::TILE_BYTES;
   mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
@@ -146,18 +146,22 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
 
+  const int tile = blockIdx.x % args.ntiles, split = blockIdx.x / args.ntiles;
   int tm, tn;
   if (args.tri) {
-    tri_index(blockIdx.x, tm, tn);
+    tri_index(tile, tm, tn);
   } else {
-    tm = blockIdx.x % args.tiles_m;
-    tn = blockIdx.x / args.tiles_m;
+    tm = tile % args.tiles_m;
+    tn = tile / args.tiles_m;
   }
   const int m0 = tm * TBM, n0 = tn * TBM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp % C::WGM, wn = warp / C::WGM;
   const int g = lane >> 2, t = lane & 3;
-  const int KT = (args.K + BK - 1) / BK;
+  const int KT_all = (args.K + BK - 1) / BK;
+  const int kt_per = (KT_all + args.ksplit - 1) / args.ksplit;
+  const int kt0 = split * kt_per;
+  const int KT = max(0, min(KT_all, kt0 + kt_per) - kt0);  // k-tiles of this split, from kt0
 
   double acc[C::MT][C::NT][2];
 #pragma unroll
@@ -179,11 +183,12 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0)
-      for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, kt, m0, n0);
+      for (int it = 0; it < STAGES - 1 && it < KT; ++it)
+        issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, it, kt0 + it, m0, n0);
     for (int kt = 0; kt < KT; ++kt) {
       if (threadIdx.x == 0 && kt + STAGES - 1 < KT) {
         if (kt >= 1) mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
-        issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, kt + STAGES - 1, m0, n0);
+        issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, kt + STAGES - 1, kt0 + kt + STAGES - 1, m0, n0);
       }
       const int s = kt % STAGES;
       mbar_wait(&full[s], (kt / STAGES) & 1);
@@ -195,8 +200,8 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
   } else {
     for (int kt = 0; kt < KT; ++kt) {
       __syncthreads();
-      fill_tile_ldg<LAYOUT, TBM>(smem, args.A, args.lda, args.M, m0, args.K, kt * BK);
-      fill_tile_ldg<LAYOUT, TBM>(smem + C::TILE_BYTES, args.B, args.ldb, args.N, n0, args.K, kt * BK);
+      fill_tile_ldg<LAYOUT, TBM>(smem, args.A, args.lda, args.M, m0, args.K, (kt0 + kt) * BK);
+      fill_tile_ldg<LAYOUT, TBM>(smem + C::TILE_BYTES, args.B, args.ldb, args.N, n0, args.K, (kt0 + kt) * BK);
       __syncthreads();
       mma_stage<LAYOUT, TBM>(acc, smem, smem + C::TILE_BYTES, wm, wn, g, t);
     }
@@ -219,6 +224,45 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
         sC[LAYOUT == kLayoutN ? jl * C::CPAD + il : il * C::CPAD + jl] = acc[mt][nt][c];
       }
   __syncthreads();
+  if (args.ksplit > 1) {
+    // deterministic split-K reduction: publish this split's partial tile; the
+    // last CTA of the tile sums all partials in split order 0..ksplit-1.
+    constexpr int T2 = TBM * TBM;
+    double* wsl = args.ws + ((int64_t)split * args.ntiles + tile) * T2;
+    for (int e = threadIdx.x; e < T2; e += C::THREADS) wsl[e] = sC[(e / TBM) * C::CPAD + (e % TBM)];
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(&args.counters[tile], 1) == args.ksplit - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // 4 elements x all splits in flight per thread, summed in split order
+    constexpr int KSMAX = 16, EB = 4;
+    const int64_t sstride = (int64_t)args.ntiles * T2;
+    const double* wt = args.ws + (int64_t)tile * T2;
+    for (int e0 = threadIdx.x; e0 < T2; e0 += C::THREADS * EB) {
+      double v[EB][KSMAX];
+#pragma unroll
+      for (int q = 0; q < EB; ++q)
+#pragma unroll
+        for (int sp = 0; sp < KSMAX; ++sp) {
+          const int e = e0 + q * C::THREADS;
+          v[q][sp] = (sp < args.ksplit && e < T2) ? __ldcg(wt + sp * sstride + e) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < EB; ++q) {
+        const int e = e0 + q * C::THREADS;
+        double sum = 0.0;
+#pragma unroll
+        for (int sp = 0; sp < KSMAX; ++sp)
+          if (sp < args.ksplit) sum += v[q][sp];
+        if (e < T2) sC[(e / TBM) * C::CPAD + (e % TBM)] = sum;
+      }
+    }
+    if (threadIdx.x == 0) args.counters[tile] = 0;  // ready for the next launch / graph replay
+    __syncthreads();
+  }
   constexpr int SLOW_STEP = C::THREADS / TBM;  // 2
   const int f = threadIdx.x % TBM;             // fast index
   const int s0 = threadIdx.x / TBM;
@@ -257,8 +301,7 @@ cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const Updat
 template <int TBM>
 cudaError_t launch_tbm(const UpdateOp& op, cudaStream_t st) {
   const UpdateArgs& a = op.args;
-  const int tiles_m = (a.M + TBM - 1) / TBM, tiles_n = (a.N + TBM - 1) / TBM;
-  const int grid = a.tri ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  const int grid = a.ntiles * a.ksplit;
   if (a.layout == kLayoutN)
     return op.use_tma ? launch_one<kLayoutN, true, TBM>(op.tmA, op.tmB, a, grid, st)
                       : launch_one<kLayoutN, false, TBM>(op.tmA, op.tmB, a, grid, st);
@@ -285,6 +328,27 @@ int update_tile_for(int M, int N, int tri) {
   const long tm = (M + 127) / 128, tn = (N + 127) / 128;
   const long t128 = tri ? tm * (tm + 1) / 2 : tm * tn;
   return t128 >= 148 ? 128 : 64;
+}
+
+static long ntiles_of(int M, int N, int tri, int tile) {
+  const long tm = (M + tile - 1) / tile, tn = (N + tile - 1) / tile;
+  return tri ? tm * (tm + 1) / 2 : tm * tn;
+}
+
+// Split K when the tile grid leaves most of the 148 SMs idle and K is long:
+// aim for ~2 CTAs per SM, each split keeping >= 8 k-tiles (128 of K).
+int update_ksplit_for(int M, int N, int K, int tri, int tile) {
+  const long tiles = ntiles_of(M, N, tri, tile);
+  const int KT = (K + BK - 1) / BK;
+  if (tiles >= 148 || KT < 16) return 1;
+  int ks = (int)((2 * 148 + tiles - 1) / tiles);
+  ks = ks < KT / 8 ? ks : KT / 8;
+  ks = ks < 16 ? ks : 16;
+  return ks >= 2 ? ks : 1;
+}
+
+int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit) {
+  return ksplit > 1 ? (int64_t)ksplit * ntiles_of(M, N, tri, tile) * tile * tile : 0;
 }
 
 cudaError_t configure_update() {

@@ -5,6 +5,7 @@
 #define RELAPACK_PROBE 1
 #include "../../paper_1602_06763_b200/csrc/potf2.cu"
 #include "../../paper_1602_06763_b200/csrc/trsm.cu"
+#include "../../paper_1602_06763_b200/csrc/trsm_fused.cu"
 using namespace relapack;
 int main() {
   const int n = 4096;
@@ -12,7 +13,7 @@ int main() {
   for (int j = 0; j < n; ++j) for (int i = 0; i < n; ++i) h[(size_t)i + (size_t)j * n] = (i == j) ? n : 1.0 / (1 + i + j);
   double* d; cudaMalloc(&d, h.size() * 8);
   int* info; cudaMalloc(&info, 4); cudaMemset(info, 0, 4);
-  configure_potf2(); configure_trsm();
+  configure_potf2(); configure_trsm(); configure_trsm_fused();
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   auto time = [&](const char* name, auto fn) {
     for (int w = 0; w < 3; ++w) { cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice); fn(); }
@@ -42,6 +43,19 @@ int main() {
   for (int m : {64, 512, 2048, 8192}) for (int t : {16, 64}) {
     char nm[64]; snprintf(nm, 64, "trsm m=%d t=%d layout N", m, t);
     time(nm, [&] { launch_trsm_base(d, n, d + 64, n, kLayoutN, m, t, info, 0); });
+  }
+  for (int m : {64, 256, 2048, 8192}) for (int t : {64, 128, 256}) {
+    char nm[64]; snprintf(nm, 64, "trsm_fused m=%d t=%d layout N", m, t);
+    time(nm, [&] { launch_trsm_fused(d, n, d + 256, n, kLayoutN, m, t, info, 0); });
+  }
+  {
+    launch_trsm_fused(d, n, d + 256, n, kLayoutN, 8192, 256, info, 0);
+    cudaDeviceSynchronize();
+    long long pr[64];
+    cudaMemcpyFromSymbol(pr, g_tprobe, sizeof(pr));
+    printf("trsm_fused t=256 phases: slab %lld |", pr[1] - pr[0]);
+    for (int cb = 0; cb < 4; ++cb) printf(" cb%d upd+stage %lld solve %lld |", cb, pr[2 + 2 * cb] - pr[0], pr[3 + 2 * cb] - pr[0]);
+    printf(" end %lld\n", pr[20] - pr[0]);
   }
   time("trsm m=2048 t=64 layout T", [&] { launch_trsm_base(d, n, d + 64 * n, n, kLayoutT, 2048, 64, info, 0); });
   return 0;
