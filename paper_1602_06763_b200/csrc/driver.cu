@@ -70,8 +70,16 @@ PlanParams current_params() {
   p.crossover = c;
   p.split_tile = t;
   p.trsm_base = kTrsmFusedMax;
+  p.lookahead = env_int("RELAPACK_LOOKAHEAD", 1) != 0;
   return p;
 }
+
+// DAG capture: the graph's edges are the plan's footprint dependencies
+// (compute_deps) instead of the serial launch order.
+static bool dag_enabled() { return env_int("RELAPACK_DAG", 1) != 0; }
+// CTA cap of the deferred (lookahead) trailing updates: leaves SMs to the
+// next panel's chain; 0 = uncapped
+static int bulk_ctas() { return env_int("RELAPACK_BULK_CTAS", 132); }
 
 static bool splitk_enabled() { return env_int("RELAPACK_SPLITK", 1) != 0; }
 
@@ -86,8 +94,9 @@ struct Plan {
   std::vector<PlanOp> ops;
   std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
   cudaGraphExec_t exec = nullptr;
-  double* splitk_ws = nullptr;  // split-K partial tiles (shared by the plan's sequential updates)
-  int* splitk_cnt = nullptr;    // per-tile arrival counters (self-resetting)
+  double* splitk_ws = nullptr;  // split-K partial tiles, one slot per concurrently runnable update
+  int* splitk_cnt = nullptr;    // per-tile arrival counters (self-resetting; zeroed at every run start)
+  size_t cnt_bytes = 0;
   ~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (splitk_ws) cudaFree(splitk_ws);
@@ -95,7 +104,7 @@ struct Plan {
   }
 };
 
-using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, int, int, int>;
+using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, int, int, int, int>;
 
 struct DeviceState {
   std::mutex mu;          // guards the plan cache
@@ -167,12 +176,17 @@ static void fill_update(UpdateOp& u, const PlanOp& op, double* A, int64_t ld, in
               make_operand_map(&u.tmB, a.B, ld, layout, a.N, a.K, u.tile);
 }
 
-// Enable split-K on the plan's small-grid / long-K updates and give them the
-// shared workspace (the plan's kernels run one after another).
-static cudaError_t setup_splitk(Plan& p) {
+// Enable split-K on the plan's small-grid / long-K updates and give each a
+// workspace slot.  Two split-K updates share a slot only if one is an
+// ancestor of the other in the dependency DAG (`anc`, or the serial order
+// when anc is null), so concurrently runnable updates never share partials.
+static cudaError_t setup_splitk(Plan& p, const std::vector<uint64_t>* anc) {
+  const size_t nops = p.ops.size(), words = (nops + 63) / 64;
   int64_t ws = 0;
   int cnt = 0;
-  for (size_t i = 0; i < p.ops.size(); ++i) {
+  std::vector<int> slot_last;  // last op assigned to each slot
+  std::vector<int> slot_of(nops, -1);
+  for (size_t i = 0; i < nops; ++i) {
     if (p.ops[i].kind != OP_GEMM && p.ops[i].kind != OP_SYRK) continue;
     UpdateArgs& a = p.upd[i].args;
     const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, p.upd[i].tile);
@@ -181,16 +195,29 @@ static cudaError_t setup_splitk(Plan& p) {
     const int64_t e = update_ws_elems(a.M, a.N, a.tri, p.upd[i].tile, ks);
     ws = e > ws ? e : ws;
     cnt = a.ntiles > cnt ? a.ntiles : cnt;
+    int s = -1;
+    for (size_t q = 0; q < slot_last.size() && s < 0; ++q) {
+      const int l = slot_last[q];
+      if (!anc || ((*anc)[i * words + l / 64] >> (l % 64) & 1)) s = (int)q;
+    }
+    if (s < 0) {
+      s = (int)slot_last.size();
+      slot_last.push_back(0);
+    }
+    slot_last[s] = (int)i;
+    slot_of[i] = s;
   }
   if (ws == 0) return cudaSuccess;
+  const size_t nslots = slot_last.size();
   cudaError_t e;
-  if ((e = cudaMalloc(&p.splitk_ws, ws * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&p.splitk_cnt, cnt * sizeof(int))) != cudaSuccess) return e;
-  if ((e = cudaMemset(p.splitk_cnt, 0, cnt * sizeof(int))) != cudaSuccess) return e;
-  for (size_t i = 0; i < p.ops.size(); ++i) {
-    if (p.ops[i].kind != OP_GEMM && p.ops[i].kind != OP_SYRK) continue;
-    p.upd[i].args.ws = p.splitk_ws;
-    p.upd[i].args.counters = p.splitk_cnt;
+  if ((e = cudaMalloc(&p.splitk_ws, nslots * ws * sizeof(double))) != cudaSuccess) return e;
+  p.cnt_bytes = nslots * cnt * sizeof(int);
+  if ((e = cudaMalloc(&p.splitk_cnt, p.cnt_bytes)) != cudaSuccess) return e;
+  if ((e = cudaMemset(p.splitk_cnt, 0, p.cnt_bytes)) != cudaSuccess) return e;
+  for (size_t i = 0; i < nops; ++i) {
+    if (slot_of[i] < 0) continue;
+    p.upd[i].args.ws = p.splitk_ws + (size_t)slot_of[i] * ws;
+    p.upd[i].args.counters = p.splitk_cnt + (size_t)slot_of[i] * cnt;
   }
   return cudaSuccess;
 }
@@ -218,9 +245,35 @@ static cudaEvent_t prof_event() {
   return e;
 }
 
+static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
+                             cudaStream_t st) {
+  const PlanOp& op = pl.ops[i];
+  switch (op.kind) {
+    case OP_POTF2:
+      return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
+    case OP_TRSM:
+      return launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, ld), ld, A + lv_off(layout, op.c_i, op.c_j, ld), ld,
+                             layout, op.m, op.k, d_info, st);
+    case OP_GEMM:
+    case OP_SYRK:
+      return launch_update(pl.upd[i], st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+// Run-start nodes: reset info and (robustness after an early exit) the
+// split-K arrival counters.
+static cudaError_t run_prologue(const Plan& pl, int* d_info, cudaStream_t st) {
+  cudaError_t e = launch_set_int(d_info, 0, st);
+  if (e == cudaSuccess && pl.splitk_cnt) e = cudaMemsetAsync(pl.splitk_cnt, 0, pl.cnt_bytes, st);
+  return e;
+}
+
+// Serial execution in plan order (eager mode and the profiler).
 static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, int* d_info, cudaStream_t st,
                            bool profile) {
-  cudaError_t e = launch_set_int(d_info, 0, st);
+  cudaError_t e = run_prologue(pl, d_info, st);
   if (e != cudaSuccess) return e;
   std::unique_lock<std::mutex> plk(g_prof_mu, std::defer_lock);
   if (profile) plk.lock();
@@ -238,24 +291,69 @@ static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, in
       rec.level = op.level;
       cudaEventRecord(rec.start, st);
     }
-    switch (op.kind) {
-      case OP_POTF2:
-        e = launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
-        break;
-      case OP_TRSM:
-        e = launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, ld), ld, A + lv_off(layout, op.c_i, op.c_j, ld), ld,
-                            layout, op.m, op.k, d_info, st);
-        break;
-      case OP_GEMM:
-      case OP_SYRK:
-        e = launch_update(pl.upd[i], st);
-        break;
-    }
-    if (e != cudaSuccess) return e;
+    if ((e = launch_op(pl, i, A, ld, layout, d_info, st)) != cudaSuccess) return e;
     if (profile) {
       cudaEventRecord(rec.stop, st);
       g_prof.push_back(rec);
     }
+  }
+  return cudaSuccess;
+}
+
+// Capture the plan as a DAG on one stream: before each op the capture
+// dependencies are set to the graph nodes of the op's footprint
+// dependencies, so independent ops (the lookahead trailing updates and the
+// next panel's chain) become parallel branches of the graph.  Deferred ops
+// get the lowest node priority, the rest the highest.
+static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int>>& deps, double* A, int64_t ld,
+                               int layout, int* d_info, cudaStream_t st, std::vector<cudaGraphNode_t>& nodes,
+                               std::vector<char>& deferred_node) {
+  cudaError_t e = run_prologue(pl, d_info, st);
+  if (e != cudaSuccess) return e;
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* cur = nullptr;
+  size_t ncur = 0;
+  if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;
+  if (ncur != 1) return cudaErrorStreamCaptureInvalidated;
+  const cudaGraphNode_t root = cur[0];
+  nodes.assign(pl.ops.size(), nullptr);
+  std::vector<cudaGraphNode_t> want;
+  for (size_t i = 0; i < pl.ops.size(); ++i) {
+    want.clear();
+    for (int d : deps[i]) want.push_back(nodes[d]);
+    if (want.empty()) want.push_back(root);
+    if ((e = cudaStreamUpdateCaptureDependencies(st, want.data(), want.size(), cudaStreamSetCaptureDependencies)) !=
+        cudaSuccess)
+      return e;
+    if ((e = launch_op(pl, i, A, ld, layout, d_info, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;
+    if (ncur != 1) return cudaErrorStreamCaptureInvalidated;
+    nodes[i] = cur[0];
+    deferred_node.push_back((char)pl.ops[i].deferred);
+  }
+  // join every sink so the capture ends on one node
+  std::vector<char> has_succ(pl.ops.size(), 0);
+  for (size_t i = 0; i < pl.ops.size(); ++i)
+    for (int d : deps[i]) has_succ[d] = 1;
+  want.clear();
+  for (size_t i = 0; i < pl.ops.size(); ++i)
+    if (!has_succ[i]) want.push_back(nodes[i]);
+  if (!want.empty())
+    e = cudaStreamUpdateCaptureDependencies(st, want.data(), want.size(), cudaStreamSetCaptureDependencies);
+  return e;
+}
+
+static cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes, const std::vector<char>& deferred) {
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e != cudaSuccess) return e;
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    cudaGraphNodeType t;
+    if ((e = cudaGraphNodeGetType(nodes[i], &t)) != cudaSuccess) return e;
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeAttrValue v{};
+    v.priority = deferred[i] ? least : greatest;
+    if ((e = cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -269,8 +367,10 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const bool use_graph = graphs_enabled() && !profile;
   std::lock_guard<std::mutex> lk(ds->mu);
   if ((e = ensure_device(ds)) != cudaSuccess) return cuda_fail(e, "device setup");
+  const bool use_dag = use_graph && dag_enabled();
+  const int bulk = bulk_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, use_graph ? 1 : 0};
+              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0), bulk};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
   if (it != ds->index.end()) {
@@ -281,20 +381,34 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
     build_potrf_plan(n, pp, p->ops);
     p->upd.resize(p->ops.size());
     for (size_t i = 0; i < p->ops.size(); ++i)
-      if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
-    if (splitk_enabled() && (e = setup_splitk(*p)) != cudaSuccess) return cuda_fail(e, "split-K workspace");
+      if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) {
+        fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
+        if (use_dag && p->ops[i].deferred) p->upd[i].max_ctas = bulk;
+      }
+    std::vector<std::vector<int>> deps;
+    std::vector<uint64_t> anc;
+    if (use_dag) compute_deps(p->ops, deps, &anc);
+    if (splitk_enabled() && (e = setup_splitk(*p, use_dag ? &anc : nullptr)) != cudaSuccess)
+      return cuda_fail(e, "split-K workspace");
     if (use_graph) {
       cudaGraph_t g = nullptr;
+      std::vector<cudaGraphNode_t> nodes;
+      std::vector<char> deferred;
       if ((e = cudaStreamBeginCapture(ds->capture, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return cuda_fail(e, "begin capture");
-      cudaError_t er = run_ops(*p, A, ld, layout, d_info, ds->capture, false);
+      cudaError_t er = use_dag ? capture_dag(*p, deps, A, ld, layout, d_info, ds->capture, nodes, deferred)
+                               : run_ops(*p, A, ld, layout, d_info, ds->capture, false);
       e = cudaStreamEndCapture(ds->capture, &g);
       if (er != cudaSuccess) {
         if (g) cudaGraphDestroy(g);
         return cuda_fail(er, "launch during capture");
       }
       if (e != cudaSuccess) return cuda_fail(e, "end capture");
-      e = cudaGraphInstantiate(&p->exec, g, 0);
+      if (use_dag && (e = set_node_priorities(nodes, deferred)) != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return cuda_fail(e, "graph node priority");
+      }
+      e = cudaGraphInstantiateWithFlags(&p->exec, g, use_dag ? cudaGraphInstantiateFlagUseNodePriority : 0);
       cudaGraphDestroy(g);
       if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
     }

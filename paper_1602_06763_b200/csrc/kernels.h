@@ -36,7 +36,8 @@ struct UpdateOp {
   UpdateArgs args;
   CUtensorMap tmA, tmB;
   bool use_tma;
-  int tile;  // CTA tile (128 or 64), see update_tile_for
+  int tile;      // CTA tile (128 or 64), see update_tile_for
+  int max_ctas;  // > 0: persistent launch with at most this many CTAs
 };
 
 cudaError_t launch_update(const UpdateOp& op, cudaStream_t st);

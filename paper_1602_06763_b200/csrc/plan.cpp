@@ -72,15 +72,38 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
   const int n1 = split_point(n, p.split_tile), n2 = n - n1;
   build_potrf(off, n1, level + 1, info_base, p, ops);
   build_trsm(off, BUF_A, off + n1, off, n2, n1, level + 1, p, ops);
-  PlanOp s{};
-  s.kind = OP_SYRK;
-  s.level = level + 1;
-  s.c_i = off + n1; s.c_j = off + n1;
-  s.a_i = off + n1; s.a_j = off;
-  s.b_i = off + n1; s.b_j = off;
-  s.n = n2; s.m = n2; s.k = n1;
-  s.flops = (double)n2 * n2 * n1;
-  ops.push_back(s);
+  auto syrk = [&](int r0, int nn) {
+    PlanOp s{};
+    s.kind = OP_SYRK;
+    s.level = level + 1;
+    s.c_i = r0; s.c_j = r0;
+    s.a_i = r0; s.a_j = off;
+    s.b_i = r0; s.b_j = off;
+    s.n = nn; s.m = nn; s.k = n1;
+    s.flops = (double)nn * nn * n1;
+    ops.push_back(s);
+  };
+  if (p.lookahead && n2 > p.crossover) {
+    // A22 = [B11 .; B21 B22] along the child's split n1c: the same update, in
+    // three footprints (B11 first: the child's potrf(B11) depends only on it)
+    const int n1c = split_point(n2, p.split_tile), n2c = n2 - n1c;
+    const int r0 = off + n1, r1 = off + n1 + n1c;
+    syrk(r0, n1c);
+    PlanOp g{};
+    g.kind = OP_GEMM;
+    g.level = level + 1;
+    g.c_i = r1; g.c_j = r0;   // B21 (n2c x n1c)
+    g.a_i = r1; g.a_j = off;  // A21 rows of B2
+    g.b_i = r0; g.b_j = off;  // A21 rows of B1
+    g.m = n2c; g.n = n1c; g.k = n1;
+    g.flops = 2.0 * n2c * n1c * n1;
+    g.deferred = 1;
+    ops.push_back(g);
+    syrk(r1, n2c);
+    ops.back().deferred = 1;
+  } else {
+    syrk(off + n1, n2);
+  }
   build_potrf(off + n1, n2, level + 1, info_base + n1, p, ops);
 }
 
@@ -98,6 +121,65 @@ void append_potrf(int off, int n, int level, int info_base, const PlanParams& p,
 void append_trsm(int l_off, int b_buf, int b_i, int b_j, int m, int k, int level, const PlanParams& p,
                  std::vector<PlanOp>& ops) {
   build_trsm(l_off, b_buf, b_i, b_j, m, k, level, p, ops);
+}
+
+// ---------------------------------------------------------------- dependencies
+void op_regions(const PlanOp& op, Rect* w, Rect* r1, Rect* r2) {
+  const Rect none{-1, 0, 0, 0, 0};
+  *r1 = none;
+  *r2 = none;
+  switch (op.kind) {
+    case OP_POTF2:
+      *w = Rect{BUF_A, op.c_i, op.c_i + op.n, op.c_j, op.c_j + op.n};
+      break;
+    case OP_TRSM:
+      *w = Rect{op.c_buf, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.k};
+      *r1 = Rect{BUF_A, op.a_i, op.a_i + op.k, op.a_j, op.a_j + op.k};
+      break;
+    case OP_GEMM:
+      *w = Rect{op.c_buf, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.n};
+      *r1 = Rect{op.a_buf, op.a_i, op.a_i + op.m, op.a_j, op.a_j + op.k};
+      *r2 = Rect{op.b_buf, op.b_i, op.b_i + op.n, op.b_j, op.b_j + op.k};
+      break;
+    case OP_SYRK:
+      *w = Rect{op.c_buf, op.c_i, op.c_i + op.n, op.c_j, op.c_j + op.n};
+      *r1 = Rect{op.a_buf, op.a_i, op.a_i + op.n, op.a_j, op.a_j + op.k};
+      break;
+    default:  // pack / all-gather / unpack: treat as a barrier over everything
+      *w = Rect{-2, 0, 0, 0, 0};
+      break;
+  }
+}
+
+static bool overlap(const Rect& a, const Rect& b) {
+  if (a.buf == -2 || b.buf == -2) return true;
+  if (a.buf < 0 || b.buf < 0 || a.buf != b.buf) return false;
+  return a.r0 < b.r1 && b.r0 < a.r1 && a.c0 < b.c1 && b.c0 < a.c1;
+}
+
+void compute_deps(const std::vector<PlanOp>& ops, std::vector<std::vector<int>>& deps,
+                  std::vector<uint64_t>* anc_out) {
+  const size_t n = ops.size();
+  deps.assign(n, {});
+  std::vector<Rect> W(n), R1(n), R2(n);
+  for (size_t i = 0; i < n; ++i) op_regions(ops[i], &W[i], &R1[i], &R2[i]);
+  // ancestors as bitsets (n is a few thousand at most)
+  const size_t words = (n + 63) / 64;
+  std::vector<uint64_t> anc(n * words, 0);
+  for (size_t j = 0; j < n; ++j) {
+    uint64_t* aj = &anc[j * words];
+    for (size_t ii = j; ii-- > 0;) {
+      if (aj[ii / 64] >> (ii % 64) & 1) continue;  // already implied
+      const bool conflict = overlap(W[ii], W[j]) || overlap(W[ii], R1[j]) || overlap(W[ii], R2[j]) ||
+                            overlap(R1[ii], W[j]) || overlap(R2[ii], W[j]);
+      if (!conflict) continue;
+      deps[j].push_back((int)ii);
+      const uint64_t* ai = &anc[ii * words];
+      for (size_t q = 0; q < words; ++q) aj[q] |= ai[q];
+      aj[ii / 64] |= uint64_t(1) << (ii % 64);
+    }
+  }
+  if (anc_out) anc_out->swap(anc);
 }
 
 // ---------------------------------------------------------------- multi-GPU

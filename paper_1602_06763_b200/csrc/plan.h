@@ -42,6 +42,7 @@ struct PlanOp {
   int info_base;   // POTF2 only
   double flops;    // leading-term algorithmic flops of this op
   int c_buf = BUF_A, a_buf = BUF_A, b_buf = BUF_A;
+  int deferred = 0;  // lookahead trailing update (off the next panel's chain): low priority
   // PACK/UNPACK: rows [c_i, c_i + m) x cols [c_j, c_j + k) of the matrix,
   // block-cyclic ownership with row block nb over nranks (rows counted from 0)
   // ALLGATHER: m = rows per rank (padded), k = columns
@@ -51,7 +52,24 @@ struct PlanParams {
   int crossover = 64;   // c: base case when n <= c
   int split_tile = 64;  // T: n1 = T floor(n / 2T)
   int trsm_base = 64;   // t_base: TRSM base case when k <= t_base
+  // lookahead: split SYRK(A22) along the child's split into SYRK(B11) +
+  // GEMM(B21) + SYRK(B22), so potrf(B11) only waits for SYRK(B11) and the
+  // bulk of the trailing update can run concurrently with it
+  bool lookahead = false;
 };
+
+// Rectangle of an op's footprint in L-view coordinates of buffer `buf`.
+struct Rect {
+  int buf, r0, r1, c0, c1;  // rows [r0, r1), cols [c0, c1)
+};
+// Footprint of a compute op: written rect and up to two read-only rects.
+void op_regions(const PlanOp& op, Rect* w, Rect* r1, Rect* r2);
+// Transitively reduced dependency lists (indices of earlier ops) from
+// read/write footprint overlaps; the op order itself is a valid serial order.
+// If `anc` is given it receives the ancestor bitsets (ops.size() rows of
+// (ops.size() + 63) / 64 words): bit i of row j set iff op i precedes op j.
+void compute_deps(const std::vector<PlanOp>& ops, std::vector<std::vector<int>>& deps,
+                  std::vector<uint64_t>* anc = nullptr);
 
 int split_point(int n, int align);
 void build_potrf_plan(int n, const PlanParams& p, std::vector<PlanOp>& ops);

@@ -135,18 +135,16 @@ __device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::
   }
 }
 
+// One work item (tile, split) of the update; the CTA may process several
+// (persistent launch with a capped grid, see launch_tbm).
 template <int LAYOUT, bool USE_TMA, int TBM>
-__global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
-    k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args) {
+__device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtensorMap& tmB, const UpdateArgs& args,
+                                            uint8_t* smem, int work) {
   using C = Cfg<TBM>;
-  if (ld_info(args.d_info) != 0) return;  // dpotrf2 semantics: stop after a failed pivot
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
 
-  const int tile = blockIdx.x % args.ntiles, split = blockIdx.x / args.ntiles;
+  const int tile = work % args.ntiles, split = work / args.ntiles;
   int tm, tn;
   if (args.tri) {
     tri_index(tile, tm, tn);
@@ -293,6 +291,19 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
 }
 
 template <int LAYOUT, bool USE_TMA, int TBM>
+__global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
+    k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args) {
+  if (ld_info(args.d_info) != 0) return;  // dpotrf2 semantics: stop after a failed pivot
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nwork = args.ntiles * args.ksplit;
+  for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+    if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
+    update_item<LAYOUT, USE_TMA, TBM>(tmA, tmB, args, smem, work);
+  }
+}
+
+template <int LAYOUT, bool USE_TMA, int TBM>
 cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const UpdateArgs& a, int grid, cudaStream_t st) {
   k_update<LAYOUT, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a);
   return cudaGetLastError();
@@ -301,7 +312,8 @@ cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const Updat
 template <int TBM>
 cudaError_t launch_tbm(const UpdateOp& op, cudaStream_t st) {
   const UpdateArgs& a = op.args;
-  const int grid = a.ntiles * a.ksplit;
+  int grid = a.ntiles * a.ksplit;
+  if (op.max_ctas > 0 && grid > op.max_ctas) grid = op.max_ctas;  // persistent, leaves SMs to other streams
   if (a.layout == kLayoutN)
     return op.use_tma ? launch_one<kLayoutN, true, TBM>(op.tmA, op.tmB, a, grid, st)
                       : launch_one<kLayoutN, false, TBM>(op.tmA, op.tmB, a, grid, st);
