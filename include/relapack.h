@@ -177,6 +177,24 @@ RELAPACK_API int relapack_split_point(int n, int align);
 RELAPACK_API int relapack_plan_ledger(int n, int c, int T, int levels, double* flops_by_level, int* count);
 
 /*
+ * relapack_plan_schedule(n, c, T, lookahead, ops, max_ops, dep_off, dep_idx,
+ *                        max_deps)
+ *   host-only view of the single-GPU plan the executor captures (knobs as
+ *   arguments; lookahead 0/1 splits every trailing SYRK along the child's
+ *   split point).  ops (may be NULL): 16 int64 per kernel launch, in the
+ *   serial plan order — (kind, level, c_i, c_j, a_i, a_j, b_i, b_j, m, n, k,
+ *   info_base, c_buf, a_buf, b_buf, deferred), L-view coordinates as in
+ *   relapack_dist_schedule; deferred = 1 for the lookahead trailing updates.
+ *   dep_off (max_ops + 1 ints) / dep_idx (max_deps ints), may be NULL: CSR
+ *   list of each launch's direct predecessors in the dependency DAG the
+ *   graph is captured with (read/write footprint overlaps, transitively
+ *   reduced).  Returns the launch count (the arrays are filled only if they
+ *   are large enough; *dep_off[count] = total edges), or -1 on bad arguments.
+ */
+RELAPACK_API int relapack_plan_schedule(int n, int c, int T, int lookahead, int64_t* ops, int max_ops, int* dep_off,
+                                        int* dep_idx, int max_deps);
+
+/*
  * Per-kernel-class profiling (bench.py's roofline line).  While enabled, the
  * executor launches the plan without a CUDA graph and brackets every kernel
  * with CUDA events on the launch stream.  relapack_profile_read(kind, ...)

@@ -100,6 +100,9 @@ def lib():
         L.relapack_dist_schedule.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                              ctypes.POINTER(ctypes.c_int64), c_int]
         L.relapack_dist_schedule.restype = c_int
+        L.relapack_plan_schedule.argtypes = [c_int, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_int64), c_int,
+                                             ctypes.POINTER(c_int), ctypes.POINTER(c_int), c_int]
+        L.relapack_plan_schedule.restype = c_int
         _lib = L
     return _lib
 
@@ -190,6 +193,28 @@ def dist_schedule(n: int, rank: int, nranks: int, nb: int = 512, dist_min: int =
         d["kind"] = DIST_KINDS[d["kind"]]
         out.append(d)
     return out
+
+
+def plan_schedule(n: int, c: int = 64, T: int = 64, lookahead: bool = True):
+    """Host-only: (ops, deps) of the single-GPU plan — ops as dicts (DIST_FIELDS + deferred),
+    deps[i] = direct predecessors of launch i in the captured dependency DAG."""
+    L = lib()
+    cnt = L.relapack_plan_schedule(n, c, T, int(lookahead), None, 0, None, None, 0)
+    if cnt < 0:
+        raise ValueError("bad plan arguments")
+    buf = (ctypes.c_int64 * (16 * max(cnt, 1)))()
+    off = (ctypes.c_int * (cnt + 1))()
+    L.relapack_plan_schedule(n, c, T, int(lookahead), buf, cnt, off, None, 0)
+    idx = (ctypes.c_int * max(off[cnt], 1))()
+    L.relapack_plan_schedule(n, c, T, int(lookahead), buf, cnt, off, idx, off[cnt])
+    ops = []
+    for i in range(cnt):
+        row = buf[16 * i: 16 * i + 16]
+        d = dict(zip(DIST_FIELDS + ("deferred",), (int(v) for v in row)))
+        d["kind"] = DIST_KINDS[d["kind"]]
+        ops.append(d)
+    deps = [list(idx[off[i]:off[i + 1]]) for i in range(cnt)]
+    return ops, deps
 
 
 def _locate_nccl() -> None:

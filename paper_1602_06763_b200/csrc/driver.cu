@@ -683,6 +683,41 @@ int relapack_plan_ledger(int n, int c, int T, int levels, double* flops_by_level
   return plan_depth(n, p);
 }
 
+int relapack_plan_schedule(int n, int c, int T, int lookahead, int64_t* out, int max_ops, int* dep_off,
+                           int* dep_idx, int max_deps) {
+  if (n < 0 || c < 1 || T < 1 || max_ops < 0 || max_deps < 0) return -1;
+  PlanParams p;
+  p.crossover = c;
+  p.split_tile = T;
+  p.trsm_base = kTrsmFusedMax;
+  p.lookahead = lookahead != 0;
+  std::vector<PlanOp> ops;
+  build_potrf_plan(n, p, ops);
+  const int cnt = (int)ops.size();
+  if (out && cnt <= max_ops)
+    for (int i = 0; i < cnt; ++i) {
+      const PlanOp& o = ops[i];
+      int64_t* w = out + 16 * i;
+      w[0] = o.kind; w[1] = o.level; w[2] = o.c_i; w[3] = o.c_j; w[4] = o.a_i; w[5] = o.a_j; w[6] = o.b_i;
+      w[7] = o.b_j; w[8] = o.m; w[9] = o.n; w[10] = o.k; w[11] = o.info_base; w[12] = o.c_buf; w[13] = o.a_buf;
+      w[14] = o.b_buf; w[15] = o.deferred;
+    }
+  if (dep_off && cnt <= max_ops) {
+    std::vector<std::vector<int>> deps;
+    compute_deps(ops, deps);
+    int tot = 0;
+    for (int i = 0; i < cnt; ++i) {
+      dep_off[i] = tot;
+      for (int d : deps[i]) {
+        if (dep_idx && tot < max_deps) dep_idx[tot] = d;
+        ++tot;
+      }
+    }
+    dep_off[cnt] = tot;
+  }
+  return cnt;
+}
+
 int relapack_profile_enable(int on) {
   g_prof_on.store(on ? 1 : 0);
   return 0;
