@@ -4,22 +4,36 @@
 //
 // The batch is HBM-bound in aggregate but every single factorization is a
 // latency-bound chain (one pivot -> rsqrt -> update per column), so the design
-// maximises matrices in flight per SM and strips integer overhead:
+// keeps the load of the next matrix in flight while the current one is
+// factored, and keeps enough matrices per SM to cover the chains:
 //  * a bucketing pass sorts the matrices into size classes NMAX in
 //    {16, 32, 48, 64} (validating n / lda and writing info -2 / -4 on the way);
-//  * one kernel per class, one WARP per matrix, persistent grid-stride over the
-//    class list, no CTA-wide barriers;
-//  * the matrix sits in shared memory padded with the identity beyond n, so
-//    every loop runs at the compile-time size NMAX (factor of [A 0; 0 I] =
-//    [L 0; 0 I]); NMAX >= 48 as a packed lower triangle (12 matrices per SM),
-//    smaller classes as an odd-stride square;
+//    its lists live in a library-owned workspace (no per-call allocation);
+//  * one persistent kernel per class, one WARP per matrix, grid-stride over the
+//    class list, no CTA-wide barriers; each warp owns TWO shared-memory slots:
+//    while it factors matrix k in one slot, matrix k+1 streams into the other
+//    with bulk async copies (cp.async.bulk, one per column of the lower
+//    triangle, completion on an mbarrier);
+//  * a slot holds the lower triangle "even-packed": column j of L (layout N)
+//    or row i of L (layout T) starts at the even index below/at it, so every
+//    bulk copy is 16-byte aligned and a multiple of 16 bytes; the slot is padded
+//    with the identity beyond n, so every loop runs at the compile-time size
+//    NMAX (the factor of [A 0; 0 I] is [L 0; 0 I]);
 //  * panels of 8 columns are factored in registers (lane l holds rows l and
 //    l+32; pivot and l_kj broadcast by shuffles; rsqrt chain as in potf2.cu),
 //    the rank-8 trailing update runs on the FP64 tensor cores (DMMA.8x8x4 on
 //    8x8 tiles of the lower triangle, K = 8), all tiles of a tile row in flight;
-//  * cp.async loads / coalesced stores along the contiguous index of either layout.
+//  * odd n, odd lda or a base not 16-byte aligned take a plain-load path into
+//    the same slot layout.
+#include <mutex>
+
+#include "chol_regs.cuh"
 #include "common.cuh"
 #include "kernels.h"
+
+#ifndef RELAPACK_BATCH_MODE
+#define RELAPACK_BATCH_MODE 0
+#endif
 
 namespace relapack {
 
@@ -28,117 +42,25 @@ namespace {
 constexpr int kPanel = 8;
 constexpr int kClasses = 4;  // NMAX = 16 (c + 1)
 
-template <int NMAX>
+template <int NMAX, int LAYOUT>
 struct BC {
-  static constexpr int LDS = NMAX + 1;
-  static constexpr int R = (NMAX + 31) / 32;                 // panel rows per lane
-  static constexpr int WPC = 4;                              // warps (matrices) per CTA
-  // NMAX >= 48: packed lower triangle (column j at colbase(j) + i), so 12+
-  // matrices stay resident per SM; smaller classes: odd-stride square.
-  static constexpr bool PACKED = NMAX >= 48;
-  static constexpr int PER_WARP = PACKED ? NMAX * (NMAX + 1) / 2 : NMAX * LDS;
-  static constexpr size_t SMEM = sizeof(double) * PER_WARP * WPC;
-  // offset of element (i, j), i >= j for the packed layout
+  static constexpr int TN = NMAX / 8;
+  static constexpr int WPC = 4;  // warps (matrices in flight) per CTA
+  // even-packed lower triangle: NMAX (NMAX/2 + 1) doubles per prefetch slot
+  static constexpr int SLOT = NMAX * (NMAX / 2 + 1);
+  static constexpr size_t SMEM = sizeof(double) * SLOT * WPC;
+  // layout N: column j of L from row (j & ~1), columns back to back;
+  // layout T: row i of L, columns 0 .. (i | 1), rows back to back.
+  static __device__ __forceinline__ int base(int x) {
+    const int m = x >> 1;
+    if (LAYOUT == kLayoutN) return 2 * (m * NMAX - m * (m - 1)) + ((x & 1) ? NMAX - 2 * m : 0);
+    return 2 * m * (m + 1) + ((x & 1) ? 2 * m + 2 : 0);
+  }
+  // offset of L(i, j), i >= j
   static __device__ __forceinline__ int off(int i, int j) {
-    return PACKED ? j * NMAX - ((j * (j + 1)) >> 1) + i : i + j * LDS;
+    return LAYOUT == kLayoutN ? base(j) + i - (j & ~1) : base(i) + j;
   }
 };
-
-// Factor the NMAX x NMAX lower triangle in s (s[i + j*LDS]); returns the
-// 1-based first failing column (< n by construction of the padding) or 0.
-template <int NMAX>
-__device__ int factor_warp(double* s, int lane) {
-  using C = BC<NMAX>;
-  constexpr int R = C::R;
-  const int g = lane >> 2, t = lane & 3;
-  int fail = 0;
-#pragma unroll(NMAX <= 32 ? NMAX / kPanel : 1)
-  for (int j0 = 0; j0 < NMAX; j0 += kPanel) {
-    // ---- panel [j0, j0 + 8): rows i_r = lane + 32 r in registers
-    double x[R][kPanel];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = lane + 32 * r;
-#pragma unroll
-      for (int c = 0; c < kPanel; ++c) x[r][c] = (i < NMAX && i >= j0 + c) ? s[C::off(i, j0 + c)] : 0.0;
-    }
-    double dpiv[kPanel], rpiv[kPanel];
-    double dnext = (R > 1 && j0 >= 32) ? x[R - 1][0] : x[0][0];
-#pragma unroll
-    for (int c = 0; c < kPanel; ++c) {
-      const int j = j0 + c;
-      const double d = __shfl_sync(0xffffffffu, dnext, j & 31);
-      dpiv[c] = d;
-      const double rinv = rsqrt_nr(d);
-      rpiv[c] = rinv;
-#pragma unroll
-      for (int r = 0; r < R; ++r) x[r][c] *= rinv;
-      if (c + 1 < kPanel) {
-        const int jn = j + 1;
-        const double xn = (R > 1 && jn >= 32) ? x[R - 1][c] : x[0][c];
-        const double an = (R > 1 && jn >= 32) ? x[R - 1][c + 1] : x[0][c + 1];
-        dnext = an - xn * xn;
-#pragma unroll
-        for (int c2 = c + 1; c2 < kPanel; ++c2) {
-          const int jj = j0 + c2;
-          const double l = __shfl_sync(0xffffffffu, (R > 1 && jj >= 32) ? x[R - 1][c] : x[0][c], jj & 31);
-#pragma unroll
-          for (int r = 0; r < R; ++r) x[r][c2] -= x[r][c] * l;
-        }
-      }
-    }
-#pragma unroll
-    for (int c = kPanel - 1; c >= 0; --c)
-      if (!(dpiv[c] > 0.0)) fail = j0 + c + 1;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = lane + 32 * r;
-#pragma unroll
-      for (int c = 0; c < kPanel; ++c) {
-        if (i == j0 + c) x[r][c] = sqrt_from_rsqrt(dpiv[c], rpiv[c]);
-        if (i < NMAX && i >= j0 + c) s[C::off(i, j0 + c)] = x[r][c];
-      }
-    }
-    __syncwarp();
-    if (fail) return fail;
-    // ---- trailing update A22 -= P2 P2^T on 8x8 tiles (lower), K = 8; the
-    // tiles of one tile row are independent DMMA chains issued together
-    const int r0 = j0 + kPanel;
-    constexpr int TK = NMAX / 8 - 1;
-    for (int ti = 0; r0 + 8 * ti < NMAX; ++ti) {
-      const int ia = r0 + 8 * ti + g;
-      double a[2];
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) a[ks] = -s[C::off(ia, j0 + 4 * ks + t)];
-      double c0[TK], c1[TK];
-#pragma unroll
-      for (int tk = 0; tk < TK; ++tk) {
-        // positions above the diagonal (diagonal tile, g < 2t + c) are don't-care;
-        // the packed layout does not store them at all
-        const int jc = r0 + 8 * tk + 2 * t;
-        if (tk <= ti) {
-          c0[tk] = (jc <= ia) ? s[C::off(ia, jc)] : 0.0;
-          c1[tk] = (jc + 1 <= ia) ? s[C::off(ia, jc + 1)] : 0.0;
-        }
-      }
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-#pragma unroll
-        for (int tk = 0; tk < TK; ++tk) {
-          if (tk <= ti) dmma_884(c0[tk], c1[tk], a[ks], s[C::off(r0 + 8 * tk + g, j0 + 4 * ks + t)]);
-        }
-      }
-#pragma unroll
-      for (int tk = 0; tk < TK; ++tk) {
-        const int jc = r0 + 8 * tk + 2 * t;
-        if (tk <= ti && jc <= ia) s[C::off(ia, jc)] = c0[tk];
-        if (tk <= ti && jc + 1 <= ia) s[C::off(ia, jc + 1)] = c1[tk];
-      }
-    }
-    __syncwarp();
-  }
-  return fail;
-}
 
 // Pass 1: validate, bucket by size class (list[c * batch + pos]).
 __global__ void k_bucket(int batch, const int* __restrict__ d_n, const int* __restrict__ d_lda, int* d_info,
@@ -163,112 +85,225 @@ __global__ void k_bucket(int batch, const int* __restrict__ d_n, const int* __re
   lists[(size_t)c * batch + pos] = b;
 }
 
-template <int NMAX>
-__global__ void __launch_bounds__(BC<NMAX>::WPC * 32) k_batched_cls(int layout, int batch, const int* counts,
-                                                                     const int* lists, double* const* d_A,
-                                                                     const int* d_n, const int* d_lda, int* d_info) {
-  using C = BC<NMAX>;
-  constexpr int WPC = C::WPC;
-  extern __shared__ double smem_b[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* s = smem_b + warp * C::PER_WARP;
-  const uint32_t sbase = smem_u32(s);
-  const int cls = NMAX / 16 - 1;
-  const int count = counts[cls];
-  const int* list = lists + (size_t)cls * batch;
-  for (int pos = blockIdx.x * WPC + warp; pos < count; pos += gridDim.x * WPC) {
-    const int b = list[pos];
-    const int n = d_n[b];
-    const int64_t lda = d_lda[b];
-    double* A = d_A[b];
-    // ---- stage: identity padding, then cp.async of the lower triangle
-    for (int e = lane; e < NMAX * NMAX; e += 32) {
-      const int i = e % NMAX, j = e / NMAX;
-      if ((i >= n || j >= n) && i >= j) s[C::off(i, j)] = (i == j) ? 1.0 : 0.0;
+// 1-D bulk async copy global -> shared, completion (bytes) on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NMAX, int LAYOUT>
+__device__ __forceinline__ bool bulk_ok(const double* A, int n, int64_t lda) {
+  return ((n & 1) == 0) && ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+}
+
+// Start the load of matrix (A, n, lda) into slot s: one bulk copy per column
+// (layout N) / row (layout T) of L, issued by the lanes; lane 0 registers the
+// byte count first.  Plain-load matrices (see bulk_ok) are loaded at wait time.
+template <int NMAX, int LAYOUT>
+__device__ __forceinline__ void issue_load(double* s, uint64_t* bar, const double* A, int n, int64_t lda, int lane) {
+  using C = BC<NMAX, LAYOUT>;
+  if (!bulk_ok<NMAX, LAYOUT>(A, n, lda)) return;
+  fence_proxy_async_smem();  // this warp's earlier generic accesses of the slot precede the async writes
+  if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(8 * n * (n / 2 + 1)));
+  __syncwarp();
+  for (int x = lane; x < n; x += 32) {
+    if (LAYOUT == kLayoutN) {
+      const int js = x & ~1;  // column x of L: rows js .. n-1
+      bulk_g2s(s + C::base(x), A + x * lda + js, (uint32_t)(8 * (n - js)), bar);
+    } else {
+      const int cnt = (x + 2) & ~1;  // row x of L = column x of A: elements 0 .. cnt-1 (cnt <= n, n even)
+      bulk_g2s(s + C::base(x), A + x * lda, (uint32_t)(8 * cnt), bar);
     }
-    for (int o = 0; o < n; ++o) {
-      const int cnt = layout == kLayoutN ? n - o : o + 1;
-      for (int q = lane; q < cnt; q += 32) {
-        const int i = layout == kLayoutN ? o + q : o, j = layout == kLayoutN ? o : q;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * (uint32_t)C::off(i, j)),
-                     "l"(A + lv_off(layout, i, j, lda))
-                     : "memory");
-      }
-    }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncwarp();
-    const int fail = factor_warp<NMAX>(s, lane);
-    for (int o = 0; o < n; ++o) {
-      const int cnt = layout == kLayoutN ? n - o : o + 1;
-      for (int q = lane; q < cnt; q += 32) {
-        const int i = layout == kLayoutN ? o + q : o, j = layout == kLayoutN ? o : q;
-        A[lv_off(layout, i, j, lda)] = s[C::off(i, j)];
-      }
-    }
-    if (lane == 0) d_info[b] = fail;
-    __syncwarp();
   }
 }
 
-template <int NMAX>
-cudaError_t launch_cls(int layout, int batch, const int* counts, const int* lists, double* const* d_A, const int* d_n,
-                       const int* d_lda, int* d_info, cudaStream_t st) {
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_batched_cls<NMAX>, BC<NMAX>::WPC * 32,
-                                                                BC<NMAX>::SMEM);
-  if (e != cudaSuccess) return e;
-  int sms = 148;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = sms * (per_sm > 0 ? per_sm : 1);
-  const int need = (batch + BC<NMAX>::WPC - 1) / BC<NMAX>::WPC;
+// Registers <- the matrix (from the prefetch slot when it was bulk-loaded,
+// else straight from global memory); identity beyond n, 0 above the diagonal.
+template <int NMAX, int LAYOUT>
+__device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], const double* s, bool from_slot,
+                                          const double* A, int n, int64_t lda, int lane) {
+  using C = BC<NMAX, LAYOUT>;
+  using T = RegTri<NMAX / 8>;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < C::TN; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+        double x = (r == c) ? 1.0 : 0.0;
+        if (r < n && c < n && r >= c) x = from_slot ? s[C::off(r, c)] : A[lv_off(LAYOUT, r, c, lda)];
+        v[T::id(i, k)][q] = x;
+      }
+}
+
+template <int NMAX, int LAYOUT>
+__global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32)
+    k_batched_cls(int batch, const int* counts, const int* lists, double* const* d_A, const int* d_n,
+                  const int* d_lda, int* d_info) {
+  using C = BC<NMAX, LAYOUT>;
+  using T = RegTri<NMAX / 8>;
+  constexpr int WPC = C::WPC;
+  extern __shared__ __align__(16) double smem_b[];
+  __shared__ uint64_t bars[WPC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double* const slot = smem_b + warp * C::SLOT;
+  uint64_t* bar = &bars[warp];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const int cls = NMAX / 16 - 1;
+  const int count = counts[cls];
+  const int* list = lists + (size_t)cls * batch;
+  const int stride = gridDim.x * WPC;
+  int pos = blockIdx.x * WPC + warp;
+  if (pos >= count) return;
+  int b = list[pos];
+  int n = d_n[b];
+  int64_t lda = d_lda[b];
+  double* A = d_A[b];
+  issue_load<NMAX, LAYOUT>(slot, bar, A, n, lda, lane);
+  uint32_t parity = 0;
+  while (pos < count) {
+    double v[T::NT][2];
+    const bool bulk = bulk_ok<NMAX, LAYOUT>(A, n, lda);
+    if (bulk) {
+      mbar_wait(bar, parity);
+      parity ^= 1u;
+    }
+    load_regs<NMAX, LAYOUT>(v, slot, bulk, A, n, lda, lane);
+    // prefetch this warp's next matrix into the (now consumed) slot
+    const int npos = pos + stride;
+    int nb = 0, nn = 0;
+    int64_t nlda = 0;
+    double* nA = nullptr;
+    if (npos < count) {
+      nb = list[npos];
+      nn = d_n[nb];
+      nlda = d_lda[nb];
+      nA = d_A[nb];
+      issue_load<NMAX, LAYOUT>(slot, bar, nA, nn, nlda, lane);
+    }
+#if RELAPACK_BATCH_MODE == 1  // tools/microbench only: memory phases alone
+    const int fail = 0;
+#else
+    const int fail = reg_potrf<NMAX / 8>(v, lane);
+#endif
+    // store the lower triangle of L (only the uplo triangle is written)
+#pragma unroll
+    for (int i = 0; i < C::TN; ++i)
+#pragma unroll
+      for (int k = 0; k <= i; ++k)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+          if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q];
+        }
+    if (lane == 0) d_info[b] = fail;
+    pos = npos;
+    b = nb;
+    n = nn;
+    lda = nlda;
+    A = nA;
+  }
+}
+
+template <int NMAX, int LAYOUT>
+cudaError_t launch_cls(int batch, const int* counts, const int* lists, double* const* d_A, const int* d_n,
+                       const int* d_lda, int* d_info, int dev, int sms, cudaStream_t st) {
+  using C = BC<NMAX, LAYOUT>;
+  static int occ[kMaxDevices] = {};  // CTAs per SM of this instantiation (0: not configured on that device)
+  int& per_sm = occ[dev];
+  cudaError_t e;
+  if (per_sm == 0) {
+    if ((e = cudaFuncSetAttribute(k_batched_cls<NMAX, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)C::SMEM)) != cudaSuccess)
+      return e;
+    int p = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, k_batched_cls<NMAX, LAYOUT>, C::WPC * 32, C::SMEM)) !=
+        cudaSuccess)
+      return e;
+    per_sm = p > 0 ? p : 1;
+  }
+  int grid = sms * per_sm;
+  const int need = (batch + C::WPC - 1) / C::WPC;
   if (grid > need) grid = need;
-  k_batched_cls<NMAX><<<grid, BC<NMAX>::WPC * 32, BC<NMAX>::SMEM, st>>>(layout, batch, counts, lists, d_A, d_n, d_lda,
-                                                                       d_info);
+  k_batched_cls<NMAX, LAYOUT><<<grid, C::WPC * 32, C::SMEM, st>>>(batch, counts, lists, d_A, d_n, d_lda, d_info);
   return cudaGetLastError();
 }
 
-template <int NMAX>
-cudaError_t configure_cls() {
-  return cudaFuncSetAttribute(k_batched_cls<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BC<NMAX>::SMEM);
+template <int LAYOUT>
+cudaError_t launch_classes(int batch, const int* counts, const int* lists, double* const* d_A, const int* d_n,
+                           const int* d_lda, int* d_info, int dev, int sms, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = launch_cls<64, LAYOUT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, sms, st)) != cudaSuccess) return e;
+  if ((e = launch_cls<48, LAYOUT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, sms, st)) != cudaSuccess) return e;
+  if ((e = launch_cls<32, LAYOUT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, sms, st)) != cudaSuccess) return e;
+  return launch_cls<16, LAYOUT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, sms, st);
 }
+
+// Library-owned bucketing workspace per device (grown on demand; growing
+// synchronizes the device once so no in-flight launch still uses the old one).
+struct BatchWs {
+  std::mutex mu;
+  int* buf = nullptr;
+  size_t cap = 0;  // batch entries
+  int sms = 0;
+};
+BatchWs g_bws[kMaxDevices];
 
 }  // namespace
-
-cudaError_t configure_batched() {
-  cudaError_t e;
-  if ((e = configure_cls<16>()) != cudaSuccess) return e;
-  if ((e = configure_cls<32>()) != cudaSuccess) return e;
-  if ((e = configure_cls<48>()) != cudaSuccess) return e;
-  return configure_cls<64>();
-}
 
 cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* const* d_A, const int* d_lda,
                                  int* d_info, cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
-  static bool configured[kMaxDevices] = {};
   int dev = 0;
-  cudaGetDevice(&dev);
   cudaError_t e;
-  if (dev >= 0 && dev < kMaxDevices && !configured[dev]) {
-    if ((e = configure_batched()) != cudaSuccess) return e;
-    configured[dev] = true;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  BatchWs& w = g_bws[dev];
+  std::lock_guard<std::mutex> lk(w.mu);
+  if (w.sms == 0 && (e = cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((size_t)batch > w.cap) {
+    if (w.buf) {
+      if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+      cudaFree(w.buf);
+      w.buf = nullptr;
+      w.cap = 0;
+    }
+    if ((e = cudaMalloc(&w.buf, sizeof(int) * (kClasses + (size_t)kClasses * batch))) != cudaSuccess) return e;
+    w.cap = (size_t)batch;
   }
-  // stream-ordered workspace: 4 class counters + 4 lists of up to `batch` indices
-  int* ws = nullptr;
-  const size_t bytes = sizeof(int) * (kClasses + (size_t)kClasses * batch);
-  if ((e = cudaMallocAsync(&ws, bytes, st)) != cudaSuccess) return e;
-  int* counts = ws;
-  int* lists = ws + kClasses;
+  // the lists are indexed with stride `batch` of this call
+  int* counts = w.buf;
+  int* lists = w.buf + kClasses;
   if ((e = cudaMemsetAsync(counts, 0, kClasses * sizeof(int), st)) != cudaSuccess) return e;
   k_bucket<<<(batch + 255) / 256, 256, 0, st>>>(batch, d_n, d_lda, d_info, counts, lists);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = launch_cls<64>(layout, batch, counts, lists, d_A, d_n, d_lda, d_info, st)) != cudaSuccess) return e;
-  if ((e = launch_cls<48>(layout, batch, counts, lists, d_A, d_n, d_lda, d_info, st)) != cudaSuccess) return e;
-  if ((e = launch_cls<32>(layout, batch, counts, lists, d_A, d_n, d_lda, d_info, st)) != cudaSuccess) return e;
-  if ((e = launch_cls<16>(layout, batch, counts, lists, d_A, d_n, d_lda, d_info, st)) != cudaSuccess) return e;
-  return cudaFreeAsync(ws, st);
+  return layout == kLayoutN ? launch_classes<kLayoutN>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st)
+                            : launch_classes<kLayoutT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st);
+}
+
+void release_batched_workspace() {
+  for (int d = 0; d < kMaxDevices; ++d) {
+    std::lock_guard<std::mutex> lk(g_bws[d].mu);
+    if (g_bws[d].buf) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(d);
+      cudaFree(g_bws[d].buf);
+      cudaSetDevice(cur);
+    }
+    g_bws[d].buf = nullptr;
+    g_bws[d].cap = 0;
+  }
 }
 
 }  // namespace relapack

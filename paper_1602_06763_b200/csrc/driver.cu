@@ -639,6 +639,7 @@ void relapack_finalize(void) {
     g_dev[d] = nullptr;
   }
   cudaSetDevice(cur);
+  release_batched_workspace();
 }
 
 int relapack_set_crossover(int c) {

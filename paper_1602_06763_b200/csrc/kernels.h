@@ -75,6 +75,7 @@ inline cudaError_t launch_trsm_any(const double* L, int64_t ldl, double* B, int6
 // ---- K2 batched potf2 (batched.cu)
 cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* const* d_A, const int* d_lda,
                                  int* d_info, cudaStream_t st);
+void release_batched_workspace();
 
 // ---- one-time per-device kernel attributes (max dynamic smem); call before graph capture
 cudaError_t configure_update();

@@ -271,3 +271,55 @@ def test_batched_bad_sizes():
     assert rl.dpotrf_batched(ns, ptrs, ldas, infos, "L") == 0
     torch.cuda.synchronize()
     assert infos.cpu().tolist() == [0, -2, -2, -4, 0]
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_batched_ragged_layouts(uplo):
+    """Every n in 1..64 (odd n take the plain-load path), lda > n for some,
+    bases that are only 8-byte aligned for some; NaN sentinels in the other
+    triangle and the lda padding must stay bitwise untouched."""
+    rng = np.random.default_rng(123)
+    ns, ldas, offs, mats = [], [], [], []
+    off = 1  # first matrix starts at an odd double: not 16-byte aligned
+    for k in range(400):
+        n = int(k % 64) + 1
+        lda = n + (3 if k % 5 == 0 else (1 if k % 7 == 0 else 0))
+        A = np.full((lda, n), np.nan)
+        A[:n, :n] = gen.spd(n, 100 + k)
+        if k % 3 == 0:
+            kk = int(rng.integers(0, n))
+            A[kk, kk] = -A[kk, kk]
+        ns.append(n)
+        ldas.append(lda)
+        offs.append(off)
+        mats.append(A)
+        off += lda * n + (1 if k % 4 == 0 else 0)
+    buf = np.full(off, np.nan)
+    for A, o in zip(mats, offs):
+        lda, n = A.shape
+        buf[o:o + lda * n] = A.T.reshape(-1)
+    ns, ldas, offs = np.array(ns, np.int32), np.array(ldas, np.int32), np.array(offs, np.int64)
+    dbuf = torch.from_numpy(buf).cuda()
+    ptrs = (dbuf.data_ptr() + 8 * torch.from_numpy(offs)).cuda()
+    infos = torch.full((len(ns),), -99, dtype=torch.int32, device="cuda")
+    assert rl.dpotrf_batched(torch.from_numpy(ns).cuda(), ptrs, torch.from_numpy(ldas).cuda(), infos, uplo) == 0
+    torch.cuda.synchronize()
+    ref = buf.copy()
+    rinfo = oracle.dpotrf_batched(uplo, ns, ref, offs, ldas)
+    ginfo = infos.cpu().numpy()
+    assert np.array_equal(ginfo, rinfo)
+    G = dbuf.cpu().numpy()
+    outside = np.ones(off, bool)
+    for i in range(len(ns)):
+        n, lda, o = int(ns[i]), int(ldas[i]), int(offs[i])
+        g = G[o:o + lda * n].reshape(n, lda).T
+        r = ref[o:o + lda * n].reshape(n, lda).T
+        A0 = mats[i]
+        tri = np.tril(np.ones((n, n), bool)) if uplo == "L" else np.triu(np.ones((n, n), bool))
+        untouched = np.ones((lda, n), bool)
+        untouched[:n, :n] = ~tri
+        assert np.array_equal(g[untouched], A0[untouched], equal_nan=True), i
+        if rinfo[i] == 0:
+            assert floored_rel_err(lower_of(g[:n, :n], uplo), lower_of(r[:n, :n], uplo), A0[:n, :n]) <= TOL, i
+        outside[o:o + lda * n] = False
+    assert np.all(np.isnan(G[outside]))
