@@ -323,3 +323,34 @@ def test_batched_ragged_layouts(uplo):
             assert floored_rel_err(lower_of(g[:n, :n], uplo), lower_of(r[:n, :n], uplo), A0[:n, :n]) <= TOL, i
         outside[o:o + lda * n] = False
     assert np.all(np.isnan(G[outside]))
+
+
+def test_batched_integer_exact():
+    """P1 through the batched kernel: integer L (diag 1..4, off-diagonal -2..2),
+    A = L L^T, every size class; the factor comes back bitwise."""
+    ns, offs, mats, Ls = [], [], [], []
+    off = 0
+    for k, n in enumerate([8, 13, 16, 24, 32, 40, 48, 56, 64] * 3):
+        A, L = gen.integer_L(n, 200 + k)
+        ns.append(n)
+        offs.append(off)
+        mats.append(A)
+        Ls.append(L)
+        off += n * n
+    buf = np.zeros(off)
+    for A, o in zip(mats, offs):
+        n = A.shape[0]
+        buf[o:o + n * n] = np.asfortranarray(A).T.reshape(-1)
+    ns, offs = np.array(ns, np.int32), np.array(offs, np.int64)
+    dbuf = torch.from_numpy(buf).cuda()
+    ptrs = (dbuf.data_ptr() + 8 * torch.from_numpy(offs)).cuda()
+    infos = torch.full((len(ns),), -99, dtype=torch.int32, device="cuda")
+    dn = torch.from_numpy(ns).cuda()
+    assert rl.dpotrf_batched(dn, ptrs, dn, infos, "L") == 0
+    torch.cuda.synchronize()
+    G = dbuf.cpu().numpy()
+    assert infos.cpu().numpy().tolist() == [0] * len(ns)
+    for i in range(len(ns)):
+        n, o = int(ns[i]), int(offs[i])
+        g = G[o:o + n * n].reshape(n, n).T
+        assert np.array_equal(np.tril(g), Ls[i]), (i, n)

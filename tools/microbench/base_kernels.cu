@@ -44,18 +44,9 @@ int main() {
     char nm[64]; snprintf(nm, 64, "trsm m=%d t=%d layout N", m, t);
     time(nm, [&] { launch_trsm_base(d, n, d + 64, n, kLayoutN, m, t, info, 0); });
   }
-  for (int m : {64, 256, 2048, 8192}) for (int t : {64, 128, 256}) {
+  for (int m : {64, 256, 2048, 8192, 16384}) for (int t : {64, 128, 256}) {
     char nm[64]; snprintf(nm, 64, "trsm_fused m=%d t=%d layout N", m, t);
     time(nm, [&] { launch_trsm_fused(d, n, d + 256, n, kLayoutN, m, t, info, 0); });
-  }
-  {
-    launch_trsm_fused(d, n, d + 256, n, kLayoutN, 8192, 256, info, 0);
-    cudaDeviceSynchronize();
-    long long pr[64];
-    cudaMemcpyFromSymbol(pr, g_tprobe, sizeof(pr));
-    printf("trsm_fused t=256 phases: slab %lld |", pr[1] - pr[0]);
-    for (int cb = 0; cb < 4; ++cb) printf(" cb%d upd+stage %lld solve %lld |", cb, pr[2 + 2 * cb] - pr[0], pr[3 + 2 * cb] - pr[0]);
-    printf(" end %lld\n", pr[20] - pr[0]);
   }
   time("trsm m=2048 t=64 layout T", [&] { launch_trsm_base(d, n, d + 64 * n, n, kLayoutT, 2048, 64, info, 0); });
   return 0;
