@@ -272,6 +272,7 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
     upd_fl = res["gemm"][1] + res["syrk"][1]
     upd_n = res["gemm"][2] + res["syrk"][2]
     achieved = upd_fl / (upd_ms / 1e3) / 1e12 if upd_ms > 0 else 0.0
+    traffic, traffic_note = _committed_traffic(W.shape[0])
     roofline = {
         "kernel": "k_update (SYRK + recursive-TRSM GEMM, DMMA.8x8x4)",
         "bound": "fp64_tensor",
@@ -279,7 +280,8 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
         "peak": FP64_PEAK_TFLOPS_DATASHEET,
         "unit": "TFLOP/s",
         "frac": round(achieved / FP64_PEAK_TFLOPS_DATASHEET, 4),
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_note": traffic_note,
         "launches_per_step": upd_n,
         "peak_note": "FP64 datasheet 37 TF (measured DMMA microbenchmark 37.05 TF at 1965 MHz, "
                      "profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 entry",
@@ -291,6 +293,22 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
     share["graph_step_ms"] = round(ms_per_step, 3)
     share["profiled_kernel_sum_ms"] = round(total_prof, 3)
     return roofline, share
+
+
+def _committed_traffic(n):
+    """DRAM bytes per k_update launch from the committed ncu capture of this
+    workload (profiles/ncu_update_traffic_n<n>_*.json), or (None, why)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_update_traffic_n{n}_*.json")))
+    if not files:
+        return None, "no committed ncu capture for this n"
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return (round(d["dram_bytes_per_launch_avg"]),
+            f"dram__bytes_read+write per k_update launch, mean over the {d['launches_per_step']} launches of one "
+            f"step ({os.path.basename(files[-1])}); per step {d['dram_read_bytes_per_step'] + d['dram_write_bytes_per_step']:.3e} B "
+            f"= {d['traffic_over_algorithmic']:.2f}x the algorithmic bytes")
 
 
 def e2e_host(rl, P, n, uplo, steps, st, dev):

@@ -71,6 +71,7 @@ PlanParams current_params() {
   p.split_tile = t;
   p.trsm_base = kTrsmFusedMax;
   p.lookahead = env_int("RELAPACK_LOOKAHEAD", 1) != 0;
+  p.trsm_rows = env_int("RELAPACK_TRSM_ROWS", 0);
   return p;
 }
 
@@ -245,9 +246,23 @@ static cudaEvent_t prof_event() {
   return e;
 }
 
+__global__ void k_noop() {}
+
+// Timing experiments only (tools/): RELAPACK_DEBUG_SKIP = bit mask of op kinds
+// (1 potf2, 2 trsm, 4 gemm, 8 syrk) replaced by an empty kernel.  The result
+// is then not a factorization.
+static int debug_skip_mask() {
+  static const int m = env_int("RELAPACK_DEBUG_SKIP", 0);
+  return m;
+}
+
 static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
                              cudaStream_t st) {
   const PlanOp& op = pl.ops[i];
+  if (debug_skip_mask() & (1 << (int)op.kind)) {
+    k_noop<<<1, 32, 0, st>>>();
+    return cudaGetLastError();
+  }
   switch (op.kind) {
     case OP_POTF2:
       return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
@@ -370,7 +385,7 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const bool use_dag = use_graph && dag_enabled();
   const int bulk = bulk_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0), bulk};
+              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3), bulk};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
   if (it != ds->index.end()) {
@@ -692,6 +707,7 @@ int relapack_plan_schedule(int n, int c, int T, int lookahead, int64_t* out, int
   p.split_tile = T;
   p.trsm_base = kTrsmFusedMax;
   p.lookahead = lookahead != 0;
+  p.trsm_rows = current_params().trsm_rows;
   std::vector<PlanOp> ops;
   build_potrf_plan(n, p, ops);
   const int cnt = (int)ops.size();

@@ -71,7 +71,12 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
   }
   const int n1 = split_point(n, p.split_tile), n2 = n - n1;
   build_potrf(off, n1, level + 1, info_base, p, ops);
-  build_trsm(off, BUF_A, off + n1, off, n2, n1, level + 1, p, ops);
+  if (p.trsm_rows > 0 && n2 > p.trsm_rows) {
+    for (int r = 0; r < n2; r += p.trsm_rows)
+      build_trsm(off, BUF_A, off + n1 + r, off, std::min(p.trsm_rows, n2 - r), n1, level + 1, p, ops);
+  } else {
+    build_trsm(off, BUF_A, off + n1, off, n2, n1, level + 1, p, ops);
+  }
   auto syrk = [&](int r0, int nn) {
     PlanOp s{};
     s.kind = OP_SYRK;

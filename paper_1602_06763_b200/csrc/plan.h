@@ -56,6 +56,10 @@ struct PlanParams {
   // GEMM(B21) + SYRK(B22), so potrf(B11) only waits for SYRK(B11) and the
   // bulk of the trailing update can run concurrently with it
   bool lookahead = false;
+  // > 0: the TRSM of a node's A21 is issued as independent row panels of this
+  // many rows (rows of B are independent), so the DAG can overlap the panels'
+  // chains with each other and start the trailing updates of finished rows
+  int trsm_rows = 0;
 };
 
 // Rectangle of an op's footprint in L-view coordinates of buffer `buf`.

@@ -20,6 +20,8 @@
 //       then X_{s'} -= X_s L_{s',s}^T on DMMA for the later sub-blocks.
 // Shared-memory strides are 4 (mod 32) doubles so every fragment read hits
 // each bank pair exactly twice.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -29,12 +31,18 @@ namespace {
 
 constexpr int kFC = 64;                  // chunk width
 constexpr int kFTmax = kTrsmFusedMax;    // 256
-constexpr int kFRows = 64;               // rows per CTA
-constexpr int kFWarps = 8;               // 8 rows per warp
-constexpr int kFThreads = kFWarps * 32;
-constexpr int kFLdX = kFTmax + 4;        // slab row stride  (== 4 mod 32)
 constexpr int kFLdL = kFC + 4;           // L block row stride (== 4 mod 32)
-constexpr size_t kFSmem = sizeof(double) * ((size_t)kFRows * kFLdX + (size_t)kFC * kFLdL + kFC);
+
+// NW warps x 8 rows per CTA; slab row stride for t columns = a multiple of 32
+// plus 4 (== 4 mod 32); shared memory sized for t.
+template <int NW>
+struct TF {
+  static constexpr int ROWS = 8 * NW, THREADS = 32 * NW;
+  static __host__ __device__ int ldx(int t) { return ((t + 31) & ~31) + 4; }
+  static __host__ __device__ size_t smem(int t) {
+    return sizeof(double) * ((size_t)ROWS * ldx(t) + (size_t)kFC * kFLdL + kFC);
+  }
+};
 
 #ifdef RELAPACK_PROBE  // phase timestamps for tools/microbench only
 __device__ long long g_tprobe[64];
@@ -47,9 +55,11 @@ __device__ long long g_tprobe[64];
 // Stage the 64x64 block of L with rows [r0, r0+64) and cols [c0, c0+64) into
 // sL[j * kFLdL + k] = L(r0 + j, c0 + k), zero outside [0, t) and, for the
 // diagonal block, on/above the diagonal (1/L_jj goes to rinv).
+template <int NW>
 __device__ __forceinline__ void stage_L(double* sL, double* rinv, const double* __restrict__ L, int64_t ldl,
                                         int layout, int t, int r0, int c0, bool diag) {
-  constexpr int kPer = kFC * kFC / kFThreads;  // 16
+  constexpr int kFThreads = TF<NW>::THREADS;
+  constexpr int kPer = kFC * kFC / kFThreads;
   double v[kPer];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
@@ -69,12 +79,15 @@ __device__ __forceinline__ void stage_L(double* sL, double* rinv, const double* 
   }
 }
 
-__global__ void __launch_bounds__(kFThreads, 1) k_trsm_fused(const double* __restrict__ L, int64_t ldl,
-                                                              double* __restrict__ B, int64_t ldb, int layout, int m,
-                                                              int t, const int* d_info) {
+template <int NW>
+__global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
+    k_trsm_fused(const double* __restrict__ L, int64_t ldl, double* __restrict__ B, int64_t ldb, int layout, int m,
+                 int t, const int* d_info) {
+  constexpr int kFRows = TF<NW>::ROWS, kFThreads = TF<NW>::THREADS;
   TPROBE(0);
   if (ld_info(d_info) != 0) return;
   extern __shared__ double smem_t[];
+  const int kFLdX = TF<NW>::ldx(t);
   double* sX = smem_t;                   // sX[r * kFLdX + c]
   double* sL = sX + kFRows * kFLdX;      // current 64x64 L block
   double* sRinv = sL + kFC * kFLdL;      // 1 / L_jj of the current diagonal chunk
@@ -119,7 +132,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_trsm_fused(const double* __res
     // ---- (a) X_cb -= X_pb L_{cb,pb}^T, pb < cb
     for (int pb = 0; pb < cb; ++pb) {
       __syncthreads();  // sL free
-      stage_L(sL, sRinv, L, ldl, layout, t, cbase, pb * kFC, false);
+      stage_L<NW>(sL, sRinv, L, ldl, layout, t, cbase, pb * kFC, false);
       __syncthreads();
 #pragma unroll 4
       for (int k0 = 0; k0 < kFC; k0 += 4) {
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_trsm_fused(const double* __res
     }
     // ---- (b) solve the diagonal chunk
     __syncthreads();
-    stage_L(sL, sRinv, L, ldl, layout, t, cbase, cbase, true);
+    stage_L<NW>(sL, sRinv, L, ldl, layout, t, cbase, cbase, true);
     __syncthreads();
     TPROBE(2 + 2 * cb);
 #pragma unroll
@@ -187,19 +200,41 @@ __global__ void __launch_bounds__(kFThreads, 1) k_trsm_fused(const double* __res
   TPROBE(20);
 }
 
+template <int NW>
+cudaError_t launch_nw(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
+                      const int* d_info, cudaStream_t st) {
+  const int grid = (m + TF<NW>::ROWS - 1) / TF<NW>::ROWS;
+  k_trsm_fused<NW><<<grid, TF<NW>::THREADS, TF<NW>::smem(t), st>>>(L, ldl, B, ldb, layout, m, t, d_info);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t configure_trsm_fused() {
-  return cudaFuncSetAttribute(k_trsm_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem);
+  cudaError_t e =
+      cudaFuncSetAttribute(k_trsm_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF<8>::smem(kFTmax));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_trsm_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)TF<4>::smem(kFTmax));
+}
+
+// 32-row CTAs (4 warps; two CTAs share an SM, so one CTA's staging and
+// substitution latency overlaps the other's DMMA work) unless
+// RELAPACK_TRSM_NW=8 asks for the 64-row CTAs.
+static int trsm_nw() {
+  static const int nw = [] {
+    const char* v = getenv("RELAPACK_TRSM_NW");
+    return (v && atoi(v) == 8) ? 8 : 4;
+  }();
+  return nw;
 }
 
 cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                               const int* d_info, cudaStream_t st) {
   if (m <= 0 || t <= 0) return cudaSuccess;
   if (t > kFTmax) return cudaErrorInvalidValue;
-  const int grid = (m + kFRows - 1) / kFRows;
-  k_trsm_fused<<<grid, kFThreads, kFSmem, st>>>(L, ldl, B, ldb, layout, m, t, d_info);
-  return cudaGetLastError();
+  return trsm_nw() == 8 ? launch_nw<8>(L, ldl, B, ldb, layout, m, t, d_info, st)
+                        : launch_nw<4>(L, ldl, B, ldb, layout, m, t, d_info, st);
 }
 
 }  // namespace relapack

@@ -149,8 +149,17 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
   if (args.tri) {
     tri_index(tile, tm, tn);
   } else {
-    tm = tile % args.tiles_m;
-    tn = tile / args.tiles_m;
+    // grouped raster: kGroupM tile rows at a time, so the CTAs resident at
+    // once share ~12 A panels and ~12 B panels in L2 instead of streaming all
+    // of A once per wave of tile columns
+    constexpr int kGroupM = 12;
+    const int tiles_n = args.ntiles / args.tiles_m;
+    const int per_group = kGroupM * tiles_n;
+    const int first_m = (tile / per_group) * kGroupM;
+    const int gm = min(args.tiles_m - first_m, kGroupM);
+    const int local = tile % per_group;
+    tm = first_m + local % gm;
+    tn = local / gm;
   }
   const int m0 = tm * TBM, n0 = tn * TBM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
