@@ -17,6 +17,9 @@
 // tensor cores (DMMA.8x8x4 on 8x8 tiles, lower triangle only) with a one-panel
 // lookahead: warp 0 updates and factors the next panel while the other warps
 // update the rest.  One __syncthreads per panel.
+#include <cstdlib>
+
+#include "chol_regs.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -125,10 +128,9 @@ __device__ __forceinline__ void strip_update(double* s, int n, int j0, int r0, i
 
 // Factor panel [j0, j0 + 8) (rows j0..n-1, already fully updated) in warp 0's
 // registers and store it.  Returns the 1-based failing column or 0.
-template <int NMAX>
+template <int NMAX, int LDS>
 __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) {
-  using C = P2<NMAX>;
-  constexpr int LDS = C::LDS, R = C::RPL;
+  constexpr int R = P2<NMAX>::RPL;
   const int w = min(kPanel, n - j0);
   double x[R][kPanel];
 #pragma unroll
@@ -208,14 +210,12 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
 // the other warps apply the current panel to the rest of the trailing
 // matrix, so one __syncthreads per panel and the bulk update is off the
 // critical path.
-template <int NMAX>
+template <int NMAX, int LDS, int NW>
 __device__ int potf2_smem(double* s, int n, int* fail_flag) {
-  using C = P2<NMAX>;
-  constexpr int LDS = C::LDS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   if (warp == 0) {
-    const int f = factor_panel<NMAX>(s, n, 0, lane);
+    const int f = factor_panel<NMAX, LDS>(s, n, 0, lane);
     if (lane == 0 && f) *fail_flag = f;
   }
   __syncthreads();
@@ -226,7 +226,7 @@ __device__ int potf2_smem(double* s, int n, int* fail_flag) {
     if (warp == 0) {
       strip_update<NMAX, LDS>(s, n, j0, r0, g, t);
       __syncwarp();
-      const int f = factor_panel<NMAX>(s, n, r0, lane);
+      const int f = factor_panel<NMAX, LDS>(s, n, r0, lane);
       if (lane == 0 && f) *fail_flag = f;
     } else {
       // tiles of the trailing grid with tk >= 1 (columns >= r0 + 8)
@@ -236,7 +236,7 @@ __device__ int potf2_smem(double* s, int n, int* fail_flag) {
       if (T > 1) {
         const int T2 = T - 1;
         const int nt2 = T2 * (T2 + 1) / 2;  // lower tiles of the grid rooted at (r0+8, r0+8)
-        trail_tiles<LDS>(s, j0, r0 + 8, warp - 1, nt2, C::NW - 1, g, t);
+        trail_tiles<LDS>(s, j0, r0 + 8, warp - 1, nt2, NW - 1, g, t);
       }
       (void)ntiles;
     }
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   copy_lower<kBaseMax, true>(s, A, ld, layout, n);
   __syncthreads();
   PROBE(1);
-  const int fail = potf2_smem<kBaseMax>(s, n, &fail_flag);
+  const int fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
   copy_lower<kBaseMax, false>(s, A, ld, layout, n);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
   PROBE(63);
@@ -311,9 +311,193 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   if (threadIdx.x == 0) fail_flag = 0;
   copy_lower<64, true>(s, A, ld, layout, n);
   __syncthreads();
-  const int fail = potf2_smem<64>(s, n, &fail_flag);
+  const int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
   copy_lower<64, false>(s, A, ld, layout, n);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+}
+
+// ---- K1' base case for 64 < n <= 128: the recursion's 128-node in ONE CTA.
+// The block is split at 64 exactly as a recursion node: factor
+// A11 (potf2_smem), A21 := A21 L11^{-T} (substitution, quad shuffles + DMMA
+// between 8-column sub-blocks), A22 -= A21 A21^T (DMMA, lower tiles), factor
+// A22 — four phases in shared memory instead of four kernel launches.
+constexpr int kN1 = 64;
+
+// A21 (rows kN1 .. kN1+n2) := A21 L11^{-T}; warp w owns rows kN1 + 8w .. +7.
+template <int LDS>
+__device__ __forceinline__ void trsm_in_smem(double* s, int n2) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  if (8 * warp >= n2) return;
+  double* X = s + kN1 + 8 * warp;  // X(r, c) = X[r + c * LDS]
+  double xs[8][2];
+#pragma unroll
+  for (int sb = 0; sb < 8; ++sb) {
+    xs[sb][0] = X[g + (8 * sb + 2 * tq) * LDS];
+    xs[sb][1] = X[g + (8 * sb + 2 * tq + 1) * LDS];
+  }
+#pragma unroll
+  for (int sb = 0; sb < 8; ++sb) {
+    double l0[8], l1[8], rc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int col = 8 * sb + c, r0 = 8 * sb + 2 * tq;
+      // the upper half of the diagonal tiles holds don't-care values: mask
+      l0[c] = (2 * tq > c) ? s[r0 + col * LDS] : 0.0;
+      l1[c] = (2 * tq + 1 > c) ? s[r0 + 1 + col * LDS] : 0.0;
+      rc[c] = 1.0 / s[col + col * LDS];
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double xj = __shfl_sync(0xffffffffu, (c & 1) ? xs[sb][1] : xs[sb][0], (lane & ~3) | (c >> 1)) * rc[c];
+      xs[sb][0] -= xj * l0[c];
+      xs[sb][1] -= xj * l1[c];
+      if (tq == (c >> 1)) {
+        if (c & 1)
+          xs[sb][1] = xj;
+        else
+          xs[sb][0] = xj;
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int src = (lane & ~3) | (2 * ks + (tq >> 1));
+      const double e0 = __shfl_sync(0xffffffffu, xs[sb][0], src);
+      const double e1 = __shfl_sync(0xffffffffu, xs[sb][1], src);
+      const double a = -((tq & 1) ? e1 : e0);  // -X_sb[g][4ks + tq]
+#pragma unroll
+      for (int s2 = sb + 1; s2 < 8; ++s2)
+        dmma_884(xs[s2][0], xs[s2][1], a, s[(8 * s2 + g) + (8 * sb + 4 * ks + tq) * LDS]);
+    }
+  }
+#pragma unroll
+  for (int sb = 0; sb < 8; ++sb) {
+    X[g + (8 * sb + 2 * tq) * LDS] = xs[sb][0];
+    X[g + (8 * sb + 2 * tq + 1) * LDS] = xs[sb][1];
+  }
+}
+
+// A22 -= A21 A21^T on the lower 8x8 tiles of the n2 x n2 block (K = 64); each
+// warp keeps all its tiles' DMMA chains in flight.
+template <int LDS, int NW>
+__device__ __forceinline__ void syrk_in_smem(double* s, int n2) {
+  constexpr int kMaxPer = (36 + NW - 1) / NW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int T = (n2 + 7) / 8, ntiles = T * (T + 1) / 2;
+  double* L21 = s + kN1;             // L21(r, k) = L21[r + k * LDS]
+  double* C = s + kN1 + kN1 * LDS;   // A22(r, c) = C[r + c * LDS]
+  int ti[kMaxPer], tk[kMaxPer];
+  double acc[kMaxPer][2];
+#pragma unroll
+  for (int q = 0; q < kMaxPer; ++q) {
+    const int x = warp + q * NW;
+    int r = 0;
+    while ((r + 1) * (r + 2) / 2 <= x) ++r;
+    ti[q] = r;
+    tk[q] = x - r * (r + 1) / 2;
+    const bool ok = x < ntiles;
+    acc[q][0] = ok ? C[(8 * ti[q] + g) + (8 * tk[q] + 2 * tq) * LDS] : 0.0;
+    acc[q][1] = ok ? C[(8 * ti[q] + g) + (8 * tk[q] + 2 * tq + 1) * LDS] : 0.0;
+  }
+#pragma unroll 4
+  for (int k0 = 0; k0 < kN1; k0 += 4) {
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      if (warp + q * NW < ntiles) {
+        const double a = -L21[(8 * ti[q] + g) + (k0 + tq) * LDS];
+        const double b = L21[(8 * tk[q] + g) + (k0 + tq) * LDS];
+        dmma_884(acc[q][0], acc[q][1], a, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kMaxPer; ++q) {
+    if (warp + q * NW < ntiles) {
+      C[(8 * ti[q] + g) + (8 * tk[q] + 2 * tq) * LDS] = acc[q][0];
+      C[(8 * ti[q] + g) + (8 * tk[q] + 2 * tq + 1) * LDS] = acc[q][1];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double* A, int64_t ld, int layout, int n,
+                                                                          int* d_info, int info_base) {
+  constexpr int LDS = P2<kBaseMax>::LDS, NW = P2<kBaseMax>::NW;
+  if (ld_info(d_info) != 0) return;
+  extern __shared__ double s[];
+  __shared__ int fail_flag;
+  if (threadIdx.x == 0) fail_flag = 0;
+  copy_lower<kBaseMax, true>(s, A, ld, layout, n);
+  __syncthreads();
+  int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
+  if (fail == 0) {
+    const int n2 = n - kN1;
+    trsm_in_smem<LDS>(s, n2);
+    __syncthreads();
+    syrk_in_smem<LDS, NW>(s, n2);
+    __syncthreads();
+    fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
+    if (fail) fail += kN1;
+  }
+  copy_lower<kBaseMax, false>(s, A, ld, layout, n);
+  if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+}
+
+// One warp, the whole block in registers (chol_regs.cuh): n <= 8 TN.  The
+// block is read straight from global memory into the DMMA tile layout
+// (identity beyond n, nothing above the diagonal is read) and written back the
+// same way.
+template <int TN>
+__global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int layout, int n, int* d_info,
+                                                      int info_base) {
+  using T = RegTri<TN>;
+  if (ld_info(d_info) != 0) return;
+  const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  double v[T::NT][2];
+#pragma unroll
+  for (int i = 0; i < TN; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+        v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(layout, r, c, ld)] : (r == c ? 1.0 : 0.0);
+      }
+  const int fail = reg_potrf<TN>(v, lane);
+#pragma unroll
+  for (int i = 0; i < TN; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+        if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q];
+      }
+  if (fail && fail <= n && lane == 0) *d_info = info_base + fail;
+}
+
+// Register kernel for n <= 32 (measured faster: 6.2 vs 10.3 us at n = 32),
+// the shared-memory lookahead kernel for 32 < n <= 64 (15.9 vs 16.4 us);
+// RELAPACK_POTF2=smem|reg forces one of them (A/B measurements).
+static int potf2_regs_max() {
+  static const int r = [] {
+    const char* v = getenv("RELAPACK_POTF2");
+    if (v && v[0] == 's') return 0;
+    if (v && v[0] == 'r') return 64;
+    return 32;
+  }();
+  return r;
+}
+static bool potf2_use_regs(int n) { return n <= potf2_regs_max(); }
+
+// 64 < n <= 128: the in-CTA recursion node (default) or the flat right-looking
+// kernel (RELAPACK_NODE128=0).
+static bool potf2_node128() {
+  static const bool r = [] {
+    const char* v = getenv("RELAPACK_NODE128");
+    return !(v && v[0] == '0');
+  }();
+  return r;
 }
 
 }  // namespace
@@ -322,14 +506,28 @@ cudaError_t configure_potf2() {
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
   cudaError_t e = cudaFuncSetAttribute(k_potf2_base, attr, (int)P2<kBaseMax>::SMEM);
   if (e != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_potf2_node128, attr, (int)P2<kBaseMax>::SMEM)) != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_potf2_base64, attr, (int)P2<64>::SMEM);
 }
 
 cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, int info_base, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (n > kPotf2Max) return cudaErrorInvalidValue;
-  if (n <= 64)
+  if (potf2_use_regs(n)) {
+    switch ((n + 7) / 8) {
+      case 1: k_potf2_reg<1><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 2: k_potf2_reg<2><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 3: k_potf2_reg<3><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 4: k_potf2_reg<4><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 5: k_potf2_reg<5><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 6: k_potf2_reg<6><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 7: k_potf2_reg<7><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      default: k_potf2_reg<8><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+    }
+  } else if (n <= 64)
     k_potf2_base64<<<1, P2<64>::THREADS, P2<64>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
+  else if (potf2_node128())
+    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
   else
     k_potf2_base<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
   return cudaGetLastError();

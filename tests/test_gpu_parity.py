@@ -178,13 +178,14 @@ def test_graphs_off_same_bits():
     assert torch.equal(d1, d2)  # same kernels, same order: deterministic
 
 
-@pytest.mark.parametrize("c", [16, 24, 32, 48])
+@pytest.mark.parametrize("c", [16, 24, 32, 48, 96, 128])
 def test_crossover_values(c):
+    old = rl.get_crossover()
     rl.set_crossover(c)
     try:
         check_spd(gen.spd(517, c), "L")
     finally:
-        rl.set_crossover(64)
+        rl.set_crossover(old)
 
 
 # ---------------------------------------------------------------- other entry points
@@ -354,3 +355,34 @@ def test_batched_integer_exact():
         n, o = int(ns[i]), int(offs[i])
         g = G[o:o + n * n].reshape(n, n).T
         assert np.array_equal(np.tril(g), Ls[i]), (i, n)
+
+
+# ---------------------------------------------------------------- 64 < n <= 128 base case (in-CTA node)
+@pytest.mark.parametrize("n", [65, 72, 100, 127, 128])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_node128_base_case(n, uplo):
+    old = rl.get_crossover()
+    rl.set_crossover(128)
+    try:
+        check_spd(gen.spd(n, 40 + n), uplo)
+        A, L = gen.integer_L(n, 3 + n)
+        G, info, _, _ = run_both(A, uplo)
+        assert info == 0
+        assert np.array_equal(lower_of(G, uplo), L)  # exact: integer factor, perfect-square pivots
+    finally:
+        rl.set_crossover(old)
+
+
+@pytest.mark.parametrize("k", [5, 63, 64, 90, 127])
+def test_node128_info(k):
+    """A negated diagonal at k makes pivot k the first failure (closed form R11)."""
+    n = 128
+    A = np.array(gen.spd(n, 9), order="F")
+    A[k, k] = -A[k, k]
+    old = rl.get_crossover()
+    rl.set_crossover(128)
+    try:
+        _, info, _, rinfo = run_both(A, "L")
+    finally:
+        rl.set_crossover(old)
+    assert info == rinfo == k + 1
