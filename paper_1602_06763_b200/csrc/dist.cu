@@ -577,7 +577,7 @@ int relapack_dist_schedule(int n, int c, int T, int nb, int dist_min, int rank, 
   PlanParams p;
   p.crossover = c;
   p.split_tile = T;
-  p.trsm_base = kTrsmFusedMax;
+  p.trsm_base = trsm_base_cols();
   DistParams d;
   d.nranks = nranks;
   d.rank = rank;

@@ -59,6 +59,14 @@ cudaStream_t current_stream_or(cudaStream_t fallback) {
   return g_stream_set.load() ? reinterpret_cast<cudaStream_t>(g_stream.load()) : fallback;
 }
 
+// Column width of the TRSM base case (RELAPACK_TRSM_BASE, 64 .. kTrsmFusedMax;
+// default 128: the whole L of the base fits shared memory next to the row
+// slab, staged once — measured best at n = 4096 and 16384, profiles/).
+int trsm_base_cols() {
+  int b = env_int("RELAPACK_TRSM_BASE", 128);
+  return b < 64 ? 64 : (b > kTrsmFusedMax ? kTrsmFusedMax : b);
+}
+
 PlanParams current_params() {
   PlanParams p;
   int c = g_crossover.load();
@@ -69,7 +77,7 @@ PlanParams current_params() {
   if (t != 8 && t != 16 && t != 32 && t != 64 && t != 128) t = 64;
   p.crossover = c;
   p.split_tile = t;
-  p.trsm_base = kTrsmFusedMax;
+  p.trsm_base = trsm_base_cols();
   p.lookahead = env_int("RELAPACK_LOOKAHEAD", 1) != 0;
   p.trsm_rows = env_int("RELAPACK_TRSM_ROWS", 0);
   return p;
@@ -683,7 +691,7 @@ int relapack_plan_ledger(int n, int c, int T, int levels, double* flops_by_level
   PlanParams p;
   p.crossover = c;
   p.split_tile = T;
-  p.trsm_base = kTrsmFusedMax;
+  p.trsm_base = trsm_base_cols();
   std::vector<PlanOp> ops;
   build_potrf_plan(n, p, ops);
   if (flops_by_level)
@@ -705,7 +713,7 @@ int relapack_plan_schedule(int n, int c, int T, int lookahead, int64_t* out, int
   PlanParams p;
   p.crossover = c;
   p.split_tile = T;
-  p.trsm_base = kTrsmFusedMax;
+  p.trsm_base = trsm_base_cols();
   p.lookahead = lookahead != 0;
   p.trsm_rows = current_params().trsm_rows;
   std::vector<PlanOp> ops;

@@ -10,6 +10,7 @@ namespace relapack {
 void set_error(const std::string& s);
 int cuda_fail(cudaError_t e, const char* what);
 PlanParams current_params();
+int trsm_base_cols();
 // Enqueue the whole recursive factorization of the device L-view matrix A on st.
 int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st);
 // The stream set with relapack_set_stream, or `fallback` if none was set.

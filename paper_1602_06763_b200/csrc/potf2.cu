@@ -305,14 +305,18 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
 // Same kernel sized for n <= 64 (4 warps, 33 KB): used when the block is small.
 __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int64_t ld, int layout, int n,
                                                                   int* d_info, int info_base) {
+  PROBE(0);
   if (ld_info(d_info) != 0) return;
   extern __shared__ double s[];
   __shared__ int fail_flag;
   if (threadIdx.x == 0) fail_flag = 0;
   copy_lower<64, true>(s, A, ld, layout, n);
   __syncthreads();
+  PROBE(1);
   const int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
+  PROBE(62);
   copy_lower<64, false>(s, A, ld, layout, n);
+  PROBE(63);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
 }
 

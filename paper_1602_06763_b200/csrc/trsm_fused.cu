@@ -39,8 +39,11 @@ template <int NW>
 struct TF {
   static constexpr int ROWS = 8 * NW, THREADS = 32 * NW;
   static __host__ __device__ int ldx(int t) { return ((t + 31) & ~31) + 4; }
+  // t <= 128: every L block the solve needs (two diagonal, one below) is
+  // staged once up front; t > 128: one block at a time
+  static __host__ __device__ int lblocks(int t) { return t <= 2 * kFC ? 3 : 1; }
   static __host__ __device__ size_t smem(int t) {
-    return sizeof(double) * ((size_t)ROWS * ldx(t) + (size_t)kFC * kFLdL + kFC);
+    return sizeof(double) * ((size_t)ROWS * ldx(t) + (size_t)lblocks(t) * kFC * kFLdL + 2 * kFC);
   }
 };
 
@@ -79,6 +82,43 @@ __device__ __forceinline__ void stage_L(double* sL, double* rinv, const double* 
   }
 }
 
+// t <= 128: stage L(0:64, 0:64), L(64:128, 64:128) (diagonal blocks) and
+// L(64:128, 0:64) in one pass of asynchronous 8-byte copies (cp.async: no
+// registers held, every copy of a thread in flight), then one fix-up pass
+// moves the diagonal into 1/L_jj and zeroes it.  Ends with a barrier.
+template <int NW>
+__device__ __forceinline__ void stage_L_all(double* sL, double* rinv, const double* __restrict__ L, int64_t ldl,
+                                            int layout, int t) {
+  constexpr int kFThreads = TF<NW>::THREADS;
+  constexpr int kPer = kFC * kFC / kFThreads;
+#pragma unroll
+  for (int bk = 0; bk < 3; ++bk) {
+    const int r0 = bk == 0 ? 0 : kFC, c0 = bk == 1 ? kFC : 0;
+#pragma unroll 4
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + u * kFThreads;
+      const int a = e & (kFC - 1), b = e >> 6;
+      const int j = layout == kLayoutN ? a : b, k = layout == kLayoutN ? b : a;
+      const int gi = r0 + j, gk = c0 + k;
+      double* dst = sL + bk * kFC * kFLdL + j * kFLdL + k;
+      if (gi < t && gk < t && (bk == 2 || gi >= gk))
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)),
+                     "l"(L + lv_off(layout, gi, gk, ldl))
+                     : "memory");
+      else
+        *dst = 0.0;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 2 * kFC) {
+    const int bk = threadIdx.x / kFC, j = threadIdx.x % kFC;
+    double* d = sL + bk * kFC * kFLdL + j * kFLdL + j;
+    rinv[bk * kFC + j] = (bk * kFC + j < t) ? 1.0 / *d : 0.0;
+    *d = 0.0;
+  }
+}
+
 template <int NW>
 __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
     k_trsm_fused(const double* __restrict__ L, int64_t ldl, double* __restrict__ B, int64_t ldb, int layout, int m,
@@ -89,8 +129,9 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
   extern __shared__ double smem_t[];
   const int kFLdX = TF<NW>::ldx(t);
   double* sX = smem_t;                   // sX[r * kFLdX + c]
-  double* sL = sX + kFRows * kFLdX;      // current 64x64 L block
-  double* sRinv = sL + kFC * kFLdL;      // 1 / L_jj of the current diagonal chunk
+  const bool pre = TF<NW>::lblocks(t) == 3;
+  double* sL = sX + kFRows * kFLdX;      // current 64x64 L block (pre: the three blocks)
+  double* sRinv = sL + TF<NW>::lblocks(t) * kFC * kFLdL;  // 1 / L_jj of the diagonal chunk(s)
   const int row0 = blockIdx.x * kFRows;
   const int rows = min(kFRows, m - row0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -116,6 +157,7 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
       }
     }
   }
+  if (pre) stage_L_all<NW>(sL, sRinv, L, ldl, layout, t);
   __syncthreads();
   TPROBE(1);
 
@@ -131,20 +173,27 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
     }
     // ---- (a) X_cb -= X_pb L_{cb,pb}^T, pb < cb
     for (int pb = 0; pb < cb; ++pb) {
-      __syncthreads();  // sL free
-      stage_L<NW>(sL, sRinv, L, ldl, layout, t, cbase, pb * kFC, false);
-      __syncthreads();
+      const double* sLb = pre ? sL + 2 * kFC * kFLdL : sL;
+      if (!pre) {
+        __syncthreads();  // sL free
+        stage_L<NW>(sL, sRinv, L, ldl, layout, t, cbase, pb * kFC, false);
+        __syncthreads();
+      }
 #pragma unroll 4
       for (int k0 = 0; k0 < kFC; k0 += 4) {
         const double a = -sX[(wrow + g) * kFLdX + pb * kFC + k0 + tq];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) dmma_884(xs[s][0], xs[s][1], a, sL[(8 * s + g) * kFLdL + k0 + tq]);
+        for (int s = 0; s < 8; ++s) dmma_884(xs[s][0], xs[s][1], a, sLb[(8 * s + g) * kFLdL + k0 + tq]);
       }
     }
     // ---- (b) solve the diagonal chunk
-    __syncthreads();
-    stage_L<NW>(sL, sRinv, L, ldl, layout, t, cbase, cbase, true);
-    __syncthreads();
+    const double* sLd = pre ? sL + cb * kFC * kFLdL : sL;
+    const double* sRd = pre ? sRinv + cb * kFC : sRinv;
+    if (!pre) {
+      __syncthreads();
+      stage_L<NW>(sL, sRinv, L, ldl, layout, t, cbase, cbase, true);
+      __syncthreads();
+    }
     TPROBE(2 + 2 * cb);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -153,9 +202,9 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
       double l0[8], l1[8], rc[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        l0[c] = sL[(8 * s + 2 * tq) * kFLdL + 8 * s + c];      // L(8s+2t,   8s+c), 0 unless 2t > c
-        l1[c] = sL[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c];  // L(8s+2t+1, 8s+c)
-        rc[c] = sRinv[8 * s + c];
+        l0[c] = sLd[(8 * s + 2 * tq) * kFLdL + 8 * s + c];      // L(8s+2t,   8s+c), 0 unless 2t > c
+        l1[c] = sLd[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c];  // L(8s+2t+1, 8s+c)
+        rc[c] = sRd[8 * s + c];
       }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -178,7 +227,7 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
         const double a = -((tq & 1) ? e1 : e0);  // -X_s[g][4ks + tq]
 #pragma unroll
         for (int s2 = s + 1; s2 < 8; ++s2)
-          dmma_884(xs[s2][0], xs[s2][1], a, sL[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
+          dmma_884(xs[s2][0], xs[s2][1], a, sLd[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
       }
     }
 #pragma unroll
@@ -210,30 +259,37 @@ cudaError_t launch_nw(const double* L, int64_t ldl, double* B, int64_t ldb, int 
 
 }  // namespace
 
-cudaError_t configure_trsm_fused() {
-  cudaError_t e =
-      cudaFuncSetAttribute(k_trsm_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF<8>::smem(kFTmax));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_trsm_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)TF<4>::smem(kFTmax));
+template <int NW>
+size_t max_smem() {
+  size_t m = 0;
+  for (int t = 8; t <= kFTmax; t += 8) m = TF<NW>::smem(t) > m ? TF<NW>::smem(t) : m;
+  return m;
 }
 
-// 32-row CTAs (4 warps; two CTAs share an SM, so one CTA's staging and
-// substitution latency overlaps the other's DMMA work) unless
-// RELAPACK_TRSM_NW=8 asks for the 64-row CTAs.
-static int trsm_nw() {
-  static const int nw = [] {
+cudaError_t configure_trsm_fused() {
+  cudaError_t e =
+      cudaFuncSetAttribute(k_trsm_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem<8>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_trsm_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem<4>());
+}
+
+// 64-row CTAs (8 warps) for tall panels (m >= 4096), 32-row CTAs (4 warps, two
+// CTAs per SM, twice the CTAs) for shorter ones — measured, profiles/
+// (RELAPACK_TRSM_NW=4|8 forces one).
+static int trsm_nw(int m) {
+  static const int forced = [] {
     const char* v = getenv("RELAPACK_TRSM_NW");
-    return (v && atoi(v) == 8) ? 8 : 4;
+    return v ? atoi(v) : 0;
   }();
-  return nw;
+  if (forced == 4 || forced == 8) return forced;
+  return m >= 4096 ? 8 : 4;
 }
 
 cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                               const int* d_info, cudaStream_t st) {
   if (m <= 0 || t <= 0) return cudaSuccess;
   if (t > kFTmax) return cudaErrorInvalidValue;
-  return trsm_nw() == 8 ? launch_nw<8>(L, ldl, B, ldb, layout, m, t, d_info, st)
+  return trsm_nw(m) == 8 ? launch_nw<8>(L, ldl, B, ldb, layout, m, t, d_info, st)
                         : launch_nw<4>(L, ldl, B, ldb, layout, m, t, d_info, st);
 }
 
