@@ -41,7 +41,7 @@ template <int NMAX>
 struct P2 {
   static constexpr int NW = NMAX / 16;         // 4 warps (64) / 8 warps (128)
   static constexpr int THREADS = NW * 32;
-  static constexpr int LDS = NMAX + 1;         // odd column stride
+  static constexpr int LDS = NMAX + 4;         // column stride == 4 (mod 16 doubles): every DMMA fragment access at most 2-way bank-conflicted
   static constexpr int RPL = NMAX / 32;        // panel rows per lane
   static constexpr size_t SMEM = sizeof(double) * NMAX * LDS;
 };
@@ -146,18 +146,18 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
   // turns the rest of the panel into NaN/garbage; it is detected once per
   // panel from the saved pivots (first failing column).
   double dpiv[kPanel], rpiv[kPanel];
-  double dnext;
+  double dsh;  // the next pivot, already broadcast
   {
     double own = x[0][0];
 #pragma unroll
     for (int r = 1; r < R; ++r)
       if ((j0 >> 5) == r) own = x[r][0];
-    dnext = own;  // lane (j0 & 31) holds a_{j0,j0}
+    dsh = __shfl_sync(0xffffffffu, own, j0 & 31);  // lane (j0 & 31) holds a_{j0,j0}
   }
 #pragma unroll
   for (int c = 0; c < kPanel; ++c) {
     const int j = j0 + c;
-    const double d = __shfl_sync(0xffffffffu, dnext, j & 31);
+    const double d = dsh;
     dpiv[c] = d;
     const double rinv = rsqrt_nr(d);
     rpiv[c] = rinv;
@@ -173,7 +173,9 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
           xn = x[r][c];
           an = x[r][c + 1];
         }
-      dnext = an - xn * xn;
+      // broadcast the next pivot before the remaining column updates, so the
+      // in-order issue of those does not delay the chain
+      dsh = __shfl_sync(0xffffffffu, an - xn * xn, jn & 31);
 #pragma unroll
       for (int c2 = c + 1; c2 < kPanel; ++c2) {
         const int jj = j0 + c2;
@@ -427,23 +429,30 @@ __device__ __forceinline__ void syrk_in_smem(double* s, int n2) {
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double* A, int64_t ld, int layout, int n,
                                                                           int* d_info, int info_base) {
   constexpr int LDS = P2<kBaseMax>::LDS, NW = P2<kBaseMax>::NW;
+  PROBE(50);
   if (ld_info(d_info) != 0) return;
   extern __shared__ double s[];
   __shared__ int fail_flag;
   if (threadIdx.x == 0) fail_flag = 0;
   copy_lower<kBaseMax, true>(s, A, ld, layout, n);
   __syncthreads();
+  PROBE(51);
   int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
+  PROBE(52);
   if (fail == 0) {
     const int n2 = n - kN1;
     trsm_in_smem<LDS>(s, n2);
     __syncthreads();
+    PROBE(53);
     syrk_in_smem<LDS, NW>(s, n2);
     __syncthreads();
+    PROBE(54);
     fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
     if (fail) fail += kN1;
   }
+  PROBE(55);
   copy_lower<kBaseMax, false>(s, A, ld, layout, n);
+  PROBE(56);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
 }
 

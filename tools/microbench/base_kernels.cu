@@ -32,6 +32,18 @@ int main() {
   {
     long long pr[64];
     cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
+    launch_potf2(d, n, kLayoutN, 64, info, 0, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
+    printf("potf2 n=64 phases (cycles from start): stage-in %lld |", pr[1] - pr[0]);
+    for (int p = 0; p < 8; ++p) printf(" P%d %lld |", p, pr[2 + p] - pr[0]);
+    printf(" factor-end %lld end %lld\n", pr[62] - pr[0], pr[63] - pr[0]);
+    launch_potf2(d, n, kLayoutN, 128, info, 0, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
+    printf("node128 phases (cycles): load %lld | potf2(A11) %lld | trsm %lld | syrk %lld | potf2(A22) %lld | store %lld\n",
+           pr[51] - pr[50], pr[52] - pr[51], pr[53] - pr[52], pr[54] - pr[53], pr[55] - pr[54], pr[56] - pr[55]);
+    setenv("RELAPACK_NODE128", "0", 1);
     launch_potf2(d, n, kLayoutN, 128, info, 0, 0);
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
