@@ -322,6 +322,49 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
 }
 
+// Copy the lower-triangle part (i >= j, i < n) of the L-view rectangle rows
+// [r0, r0+R) x cols [c0, c0+C) between global and shared memory (stride LDS),
+// coalesced along the contiguous index.  MODE 0: synchronous load (zero
+// outside), 1: asynchronous load (cp.async; wait with cp.async.wait_all),
+// 2: store.
+template <int R, int C, int LDS, int THREADS, int MODE>
+__device__ __forceinline__ void copy_rect(double* s, double* __restrict__ A, int64_t ld, int layout, int n, int r0,
+                                          int c0) {
+  constexpr int kTot = R * C, kPer = (kTot + THREADS - 1) / THREADS, kBatch = 16;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kPer; u0 += kBatch) {
+    double v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int e = threadIdx.x + (u0 + u) * THREADS;
+      const int a = layout == kLayoutN ? e % R : e % C, b = layout == kLayoutN ? e / R : e / C;
+      const int i = r0 + (layout == kLayoutN ? a : b), j = c0 + (layout == kLayoutN ? b : a);
+      const bool in = u0 + u < kPer && e < kTot;
+      const bool ok = in && i < n && i >= j;
+      if (MODE == 0) v[u] = ok ? A[lv_off(layout, i, j, ld)] : 0.0;
+      if (MODE == 1 && in) {
+        if (ok)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s + i + j * LDS)),
+                       "l"(A + lv_off(layout, i, j, ld))
+                       : "memory");
+        else
+          s[i + j * LDS] = 0.0;
+      }
+      if (MODE == 2 && ok) v[u] = s[i + j * LDS];
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int e = threadIdx.x + (u0 + u) * THREADS;
+      const int a = layout == kLayoutN ? e % R : e % C, b = layout == kLayoutN ? e / R : e / C;
+      const int i = r0 + (layout == kLayoutN ? a : b), j = c0 + (layout == kLayoutN ? b : a);
+      const bool in = u0 + u < kPer && e < kTot;
+      const bool ok = in && i < n && i >= j;
+      if (MODE == 0 && in) s[i + j * LDS] = v[u];
+      if (MODE == 2 && ok) A[lv_off(layout, i, j, ld)] = v[u];
+    }
+  }
+}
+
 // ---- K1' base case for 64 < n <= 128: the recursion's 128-node in ONE CTA.
 // The block is split at 64 exactly as a recursion node: factor
 // A11 (potf2_smem), A21 := A21 L11^{-T} (substitution, quad shuffles + DMMA
@@ -331,7 +374,7 @@ constexpr int kN1 = 64;
 
 // A21 (rows kN1 .. kN1+n2) := A21 L11^{-T}; warp w owns rows kN1 + 8w .. +7.
 template <int LDS>
-__device__ __forceinline__ void trsm_in_smem(double* s, int n2) {
+__device__ __forceinline__ void trsm_in_smem(double* s, const double* rinv, int n2) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   if (8 * warp >= n2) return;
@@ -351,7 +394,7 @@ __device__ __forceinline__ void trsm_in_smem(double* s, int n2) {
       // the upper half of the diagonal tiles holds don't-care values: mask
       l0[c] = (2 * tq > c) ? s[r0 + col * LDS] : 0.0;
       l1[c] = (2 * tq + 1 > c) ? s[r0 + 1 + col * LDS] : 0.0;
-      rc[c] = 1.0 / s[col + col * LDS];
+      rc[c] = rinv[col];
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -433,25 +476,38 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   if (ld_info(d_info) != 0) return;
   extern __shared__ double s[];
   __shared__ int fail_flag;
+  __shared__ double rinv[kN1];
   if (threadIdx.x == 0) fail_flag = 0;
-  copy_lower<kBaseMax, true>(s, A, ld, layout, n);
+  constexpr int TH = P2<kBaseMax>::THREADS;
+  // A11 now; A21 and A22 stream in (cp.async) while A11 is factored
+  copy_rect<kN1, kN1, LDS, TH, 0>(s, A, ld, layout, n, 0, 0);
+  copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, n, kN1, 0);
   __syncthreads();
   PROBE(51);
   int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
   PROBE(52);
   if (fail == 0) {
     const int n2 = n - kN1;
-    trsm_in_smem<LDS>(s, n2);
+    if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    trsm_in_smem<LDS>(s, rinv, n2);
     __syncthreads();
     PROBE(53);
+    // L11 and L21 are final: write them back while A22 is finished
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
     syrk_in_smem<LDS, NW>(s, n2);
     __syncthreads();
     PROBE(54);
     fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
     if (fail) fail += kN1;
+    PROBE(55);
+    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1);
+  } else {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    PROBE(55);
+    copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
   }
-  PROBE(55);
-  copy_lower<kBaseMax, false>(s, A, ld, layout, n);
   PROBE(56);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
 }
