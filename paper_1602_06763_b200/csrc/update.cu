@@ -22,6 +22,7 @@
 //  * non-TMA fallback (odd ld or a base not 16-B aligned): the CTA fills the
 //    same swizzled layout with plain loads, one stage at a time.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -358,10 +359,39 @@ static long ntiles_of(int M, int N, int tri, int tile) {
 
 // Split K when the tile grid leaves most of the 148 SMs idle and K is long:
 // aim for ~2 CTAs per SM, each split keeping >= 8 k-tiles (128 of K).
+// Mid-size grids (1..8 waves of 148 tiles) may also split by 2..4 when that
+// shortens the last-wave tail: modelled time = waves(tiles * ks) * (KT / ks +
+// 1.5) k-tiles (1.5 = writing one partial tile) + the final sum, against
+// waves(tiles) * KT.  Off by default (RELAPACK_SPLITK_MID=1 turns it on):
+// measured slower inside the DAG (n = 16384: 49.6 vs 48.6 ms), where
+// concurrent launches already fill the tail SMs (tools/exp9.sh).
+static bool splitk_mid_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("RELAPACK_SPLITK_MID");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 int update_ksplit_for(int M, int N, int K, int tri, int tile) {
   const long tiles = ntiles_of(M, N, tri, tile);
   const int KT = (K + BK - 1) / BK;
-  if (tiles >= 148 || KT < 16) return 1;
+  if (tiles >= 148) {
+    const long w1 = (tiles + 147) / 148;
+    if (!splitk_mid_enabled() || w1 > 8 || KT < 32) return 1;
+    double best = (double)w1 * KT;
+    int bks = 1;
+    for (int ks = 2; ks <= 4; ++ks) {
+      const long w = (tiles * ks + 147) / 148;
+      const double tcost = (double)w * ((double)KT / ks + 1.5) + 1.5 * (ks + 1);
+      if (tcost < 0.95 * best) {
+        best = tcost;
+        bks = ks;
+      }
+    }
+    return bks;
+  }
+  if (KT < 16) return 1;
   int ks = (int)((2 * 148 + tiles - 1) / tiles);
   ks = ks < KT / 8 ? ks : KT / 8;
   ks = ks < 16 ? ks : 16;
