@@ -101,6 +101,8 @@ static bool graphs_enabled() {
 // ------------------------------------------------------------------ per-device state
 struct Plan {
   std::vector<PlanOp> ops;
+  const double* host = nullptr;  // host-matrix path: the caller's pinned matrix (OP_H2D / OP_D2H ops)
+  int64_t hld = 0;
   std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
   cudaGraphExec_t exec = nullptr;
   double* splitk_ws = nullptr;  // split-K partial tiles, one slot per concurrently runnable update
@@ -113,7 +115,7 @@ struct Plan {
   }
 };
 
-using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, int, int, int, int>;
+using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, int, int, int, int, uintptr_t, int64_t>;
 
 struct DeviceState {
   std::mutex mu;          // guards the plan cache
@@ -272,6 +274,19 @@ static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, in
     return cudaGetLastError();
   }
   switch (op.kind) {
+    case OP_H2D:
+    case OP_D2H: {
+      // L-view block rows [c_i, c_i+m) x cols [c_j, c_j+k) as one 2-D copy
+      const size_t width = sizeof(double) * (layout == kLayoutN ? op.m : op.k);
+      const size_t height = layout == kLayoutN ? op.k : op.m;
+      double* dev = A + lv_off(layout, op.c_i, op.c_j, ld);
+      double* host = const_cast<double*>(pl.host) + lv_off(layout, op.c_i, op.c_j, pl.hld);
+      return op.kind == OP_H2D
+                 ? cudaMemcpy2DAsync(dev, ld * sizeof(double), host, pl.hld * sizeof(double), width, height,
+                                     cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(host, pl.hld * sizeof(double), dev, ld * sizeof(double), width, height,
+                                     cudaMemcpyDeviceToHost, st);
+    }
     case OP_POTF2:
       return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
     case OP_TRSM:
@@ -303,7 +318,8 @@ static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, in
   for (size_t i = 0; i < pl.ops.size(); ++i) {
     const PlanOp& op = pl.ops[i];
     ProfRecord rec{};
-    if (profile) {
+    const bool rec_this = profile && op.kind < OP_H2D;
+    if (rec_this) {
       rec.start = prof_event();
       rec.stop = prof_event();
       rec.kind = (int)op.kind;
@@ -315,7 +331,7 @@ static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, in
       cudaEventRecord(rec.start, st);
     }
     if ((e = launch_op(pl, i, A, ld, layout, d_info, st)) != cudaSuccess) return e;
-    if (profile) {
+    if (rec_this) {
       cudaEventRecord(rec.stop, st);
       g_prof.push_back(rec);
     }
@@ -381,8 +397,12 @@ static cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes
   return cudaSuccess;
 }
 
+// Host-matrix copy blocks: column panels x row chunks of the lower L-view.
+constexpr int kCopyPanel = 512, kCopyRows = 2048;
+
 // Enqueue the factorization of the device matrix A (already validated).
-int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st) {
+int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st, const double* host,
+                  int64_t hld) {
   DeviceState* ds = device_state(dev);
   cudaError_t e;
   PlanParams pp = current_params();
@@ -393,7 +413,8 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const bool use_dag = use_graph && dag_enabled();
   const int bulk = bulk_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3), bulk};
+              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3), bulk,
+              reinterpret_cast<uintptr_t>(host), hld};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
   if (it != ds->index.end()) {
@@ -402,6 +423,18 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   } else {
     auto p = std::make_unique<Plan>();
     build_potrf_plan(n, pp, p->ops);
+    if (host) {
+      // host-matrix path: H2D blocks first, D2H blocks last; the footprint
+      // DAG lets the first leaves start on the first blocks and each block go
+      // back as soon as its last writer is done
+      std::vector<PlanOp> all;
+      append_copies(n, kCopyPanel, kCopyRows, OP_H2D, all);
+      all.insert(all.end(), p->ops.begin(), p->ops.end());
+      append_copies(n, kCopyPanel, kCopyRows, OP_D2H, all);
+      p->ops.swap(all);
+      p->host = host;
+      p->hld = hld;
+    }
     p->upd.resize(p->ops.size());
     for (size_t i = 0; i < p->ops.size(); ++i)
       if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) {
@@ -478,6 +511,15 @@ static bool is_device_pointer(const void* p, int* dev) {
   return false;
 }
 
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 // Copy the uplo triangle between a host matrix (ld_h) and a device matrix
 // (ld_d) in column panels: only the triangle (plus the diagonal blocks of the
 // panels) crosses PCIe.
@@ -549,6 +591,7 @@ void relapack_dpotrf(const char* uplo, const int* n_, double* A, const int* lda_
   }
   double* dA = A;
   int64_t ld = lda;
+  bool pinned = false;
   if (!on_device) {
     // stage through a library-owned device buffer (ld rounded up for TMA alignment)
     const int64_t ldd = ((int64_t)n + 31) / 32 * 32;
@@ -565,17 +608,21 @@ void relapack_dpotrf(const char* uplo, const int* n_, double* A, const int* lda_
     }
     dA = ds->stage;
     ld = ldd;
-    if ((e = copy_triangle(dA, ld, A, lda, n, layout, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+    pinned = is_pinned_host(A);
+    if (!pinned && (e = copy_triangle(dA, ld, A, lda, n, layout, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
       *info = cuda_fail(e, "H2D");
       return;
     }
   }
-  int r = enqueue_potrf(dev, dA, n, ld, layout, ds->d_info, st);
+  // pinned host matrix: the copies are nodes of the captured DAG, overlapped
+  // with the factorization; pageable: staged before and after
+  int r = pinned ? enqueue_potrf(dev, dA, n, ld, layout, ds->d_info, st, A, lda)
+                 : enqueue_potrf(dev, dA, n, ld, layout, ds->d_info, st);
   if (r != 0) {
     *info = r;
     return;
   }
-  if (!on_device) {
+  if (!on_device && !pinned) {
     if ((e = copy_triangle(A, lda, dA, ld, n, layout, cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
       *info = cuda_fail(e, "D2H");
       return;

@@ -150,6 +150,13 @@ void op_regions(const PlanOp& op, Rect* w, Rect* r1, Rect* r2) {
       *w = Rect{op.c_buf, op.c_i, op.c_i + op.n, op.c_j, op.c_j + op.n};
       *r1 = Rect{op.a_buf, op.a_i, op.a_i + op.n, op.a_j, op.a_j + op.k};
       break;
+    case OP_H2D:
+      *w = Rect{BUF_A, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.k};
+      break;
+    case OP_D2H:
+      *w = none;
+      *r1 = Rect{BUF_A, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.k};
+      break;
     default:  // pack / all-gather / unpack: treat as a barrier over everything
       *w = Rect{-2, 0, 0, 0, 0};
       break;
@@ -317,6 +324,21 @@ void build_dist_plan(int n, const PlanParams& p, const DistParams& d, std::vecto
   if (send_elems) *send_elems = x.send_elems;
   if (max_rows) *max_rows = x.max_rows;
   if (max_cols) *max_cols = x.max_cols;
+}
+
+void append_copies(int n, int w, int rows, OpKind kind, std::vector<PlanOp>& ops) {
+  for (int j0 = 0; j0 < n; j0 += w) {
+    const int jw = n - j0 < w ? n - j0 : w;
+    for (int r0 = j0; r0 < n; r0 += rows) {
+      PlanOp op{};
+      op.kind = kind;
+      op.c_i = r0;
+      op.c_j = j0;
+      op.m = n - r0 < rows ? n - r0 : rows;
+      op.k = jw;
+      ops.push_back(op);
+    }
+  }
 }
 
 int plan_depth(int n, const PlanParams& p) {

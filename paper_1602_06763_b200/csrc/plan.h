@@ -25,7 +25,11 @@ enum OpKind : int {
   // multi-GPU steps (dist schedule only)
   OP_PACK = 10,       // gather this rank's owned rows of a block into the send buffer
   OP_ALLGATHER = 11,  // ncclAllGather(send, recv, m * k doubles per rank)
-  OP_UNPACK = 12      // scatter every rank's packed rows back into the matrix
+  OP_UNPACK = 12,     // scatter every rank's packed rows back into the matrix
+  // host-matrix path: copies of L-view blocks between the caller's pinned host
+  // matrix and the device staging buffer, captured into the same DAG
+  OP_H2D = 20,        // block rows [c_i, c_i + m) x cols [c_j, c_j + k): host -> device
+  OP_D2H = 21         // same block: device -> host
 };
 
 // Buffers an op can address (L-view, same layout as the matrix).
@@ -84,6 +88,10 @@ void append_potrf(int off, int n, int level, int info_base, const PlanParams& p,
 void append_trsm(int l_off, int b_buf, int b_i, int b_j, int m, int k, int level, const PlanParams& p,
                  std::vector<PlanOp>& ops);
 int plan_depth(int n, const PlanParams& p);
+// Copy ops covering the lower triangle of the n x n L-view in column panels of
+// `w` columns split into row chunks of `rows` (each block a 2-D copy; the
+// w x w diagonal block of a panel goes whole).
+void append_copies(int n, int w, int rows, OpKind kind, std::vector<PlanOp>& ops);
 
 // ---- multi-GPU schedule ----
 // Row-block-cyclic ownership of L-view rows, "snake" order so every rank gets

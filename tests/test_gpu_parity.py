@@ -190,21 +190,29 @@ def test_crossover_values(c):
 
 # ---------------------------------------------------------------- other entry points
 @pytest.mark.parametrize("uplo", ["L", "U"])
-def test_host_matrix_path(uplo):
-    """relapack_dpotrf with a HOST pointer stages the triangle through the GPU."""
-    n = 450
-    A = gen.spd(n, 12, lda=452)
+@pytest.mark.parametrize("pinned,n", [(False, 450), (True, 450), (True, 2600)])
+def test_host_matrix_path(uplo, pinned, n):
+    """relapack_dpotrf with a HOST pointer stages the triangle through the GPU;
+    a pinned matrix takes the overlapped path (copies are nodes of the DAG)."""
+    lda = n + 2
+    A = gen.spd(n, 12, lda=lda)
     R = np.array(A, order="F", copy=True)
     rinfo = oracle.dpotrf(R, uplo, n=n)
-    H_full = torch.from_numpy(np.array(A.T, order="C", copy=True)).t()  # own CPU buffer (452 x n), column-major
-    H = H_full[:n, :]  # (n, n) view with lda 452
-    info = rl.dpotrf(H, uplo)
-    assert info == rinfo == 0
-    G = np.asfortranarray(H_full.numpy())
-    assert floored_rel_err(lower_of(G[:n], uplo), lower_of(R[:n], uplo), A[:n]) <= TOL
-    other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
-    assert np.array_equal(G[:n][other], A[:n][other])
-    assert np.all(np.isnan(G[n:]))
+    H_full = torch.from_numpy(np.array(A.T, order="C", copy=True)).t()  # own CPU buffer (lda x n), column-major
+    if pinned:
+        H_full = H_full.t().contiguous().pin_memory().t()
+        assert H_full.is_pinned()
+    H = H_full[:n, :]  # (n, n) view with lda
+    for rep in range(2):  # second call replays the cached plan
+        if rep:
+            H_full.copy_(torch.from_numpy(np.array(A.T, order="C", copy=True)).t())
+        info = rl.dpotrf(H, uplo)
+        assert info == rinfo == 0
+        G = np.asfortranarray(H_full.numpy())
+        assert floored_rel_err(lower_of(G[:n], uplo), lower_of(R[:n], uplo), A[:n]) <= TOL
+        other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+        assert np.array_equal(G[:n][other], A[:n][other])
+        assert np.all(np.isnan(G[n:]))
 
 
 def test_async_entry_point():
