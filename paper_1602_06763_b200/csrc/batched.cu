@@ -128,17 +128,29 @@ __device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], 
   using C = BC<NMAX, LAYOUT>;
   using T = RegTri<NMAX / 8>;
   const int g = lane >> 2, t = lane & 3;
+  // two separate loops (warp-uniform branch): a select between the shared and
+  // the global load would issue both
+  if (from_slot) {
 #pragma unroll
-  for (int i = 0; i < C::TN; ++i)
+    for (int i = 0; i < C::TN; ++i)
 #pragma unroll
-    for (int k = 0; k <= i; ++k)
+      for (int k = 0; k <= i; ++k)
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-        double x = (r == c) ? 1.0 : 0.0;
-        if (r < n && c < n && r >= c) x = from_slot ? s[C::off(r, c)] : A[lv_off(LAYOUT, r, c, lda)];
-        v[T::id(i, k)][q] = x;
-      }
+        for (int q = 0; q < 2; ++q) {
+          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+          v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? s[C::off(r, c)] : (r == c ? 1.0 : 0.0);
+        }
+  } else {
+#pragma unroll
+    for (int i = 0; i < C::TN; ++i)
+#pragma unroll
+      for (int k = 0; k <= i; ++k)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+          v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(LAYOUT, r, c, lda)] : (r == c ? 1.0 : 0.0);
+        }
+  }
 }
 
 template <int NMAX, int LAYOUT>
@@ -197,15 +209,31 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32)
     const int fail = reg_potrf<NMAX / 8>(v, lane);
 #endif
     // store the lower triangle of L (only the uplo triangle is written)
+    if (n == NMAX) {
+      // full class size: only diagonal tiles need a predicate; one lane base
+      // pointer, tile offsets are (i, k) multiples of 8 rows / columns
+      double* Al = A + lv_off(LAYOUT, g, 2 * t, lda);
+      const int64_t cs = LAYOUT == kLayoutN ? lda : 1, rs = LAYOUT == kLayoutN ? 1 : lda;  // column / row stride
 #pragma unroll
-    for (int i = 0; i < C::TN; ++i)
+      for (int k = 0; k < C::TN; ++k) {
+        double* Ak = Al + 8 * k * cs;
 #pragma unroll
-      for (int k = 0; k <= i; ++k)
+        for (int i = k; i < C::TN; ++i)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-          if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q];
-        }
+          for (int q = 0; q < 2; ++q)
+            if (i > k || g >= 2 * t + q) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < C::TN; ++i)
+#pragma unroll
+        for (int k = 0; k <= i; ++k)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+            if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q];
+          }
+    }
     if (lane == 0) d_info[b] = fail;
     pos = npos;
     b = nb;
