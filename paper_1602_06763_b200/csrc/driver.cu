@@ -80,6 +80,7 @@ PlanParams current_params() {
   p.trsm_base = trsm_base_cols();
   p.lookahead = env_int("RELAPACK_LOOKAHEAD", 1) != 0;
   p.trsm_rows = env_int("RELAPACK_TRSM_ROWS", 0);
+  p.lookahead_depth = env_int("RELAPACK_LOOKAHEAD_DEPTH", 1);
   return p;
 }
 
@@ -413,7 +414,7 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const bool use_dag = use_graph && dag_enabled();
   const int bulk = bulk_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3), bulk,
+              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24), bulk,
               reinterpret_cast<uintptr_t>(host), hld};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
@@ -763,6 +764,7 @@ int relapack_plan_schedule(int n, int c, int T, int lookahead, int64_t* out, int
   p.trsm_base = trsm_base_cols();
   p.lookahead = lookahead != 0;
   p.trsm_rows = current_params().trsm_rows;
+  p.lookahead_depth = current_params().lookahead_depth;
   std::vector<PlanOp> ops;
   build_potrf_plan(n, p, ops);
   const int cnt = (int)ops.size();

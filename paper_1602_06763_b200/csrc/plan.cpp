@@ -2,6 +2,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <functional>
 
 namespace relapack {
 
@@ -89,23 +90,31 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
     ops.push_back(s);
   };
   if (p.lookahead && n2 > p.crossover) {
-    // A22 = [B11 .; B21 B22] along the child's split n1c: the same update, in
-    // three footprints (B11 first: the child's potrf(B11) depends only on it)
-    const int n1c = split_point(n2, p.split_tile), n2c = n2 - n1c;
-    const int r0 = off + n1, r1 = off + n1 + n1c;
-    syrk(r0, n1c);
-    PlanOp g{};
-    g.kind = OP_GEMM;
-    g.level = level + 1;
-    g.c_i = r1; g.c_j = r0;   // B21 (n2c x n1c)
-    g.a_i = r1; g.a_j = off;  // A21 rows of B2
-    g.b_i = r0; g.b_j = off;  // A21 rows of B1
-    g.m = n2c; g.n = n1c; g.k = n1;
-    g.flops = 2.0 * n2c * n1c * n1;
-    g.deferred = 1;
-    ops.push_back(g);
-    syrk(r1, n2c);
-    ops.back().deferred = 1;
+    // A22 = [B11 .; B21 B22] along the child's split: the same update in three
+    // footprints, B11 first (the child's potrf(B11) depends only on it), B11
+    // itself split again lookahead_depth - 1 times
+    std::function<void(int, int, int)> trailing = [&](int r0, int nn, int depth) {
+      if (depth == 0 || nn <= p.crossover) {
+        syrk(r0, nn);
+        return;
+      }
+      const int n1c = split_point(nn, p.split_tile), n2c = nn - n1c;
+      const int r1 = r0 + n1c;
+      trailing(r0, n1c, depth - 1);
+      PlanOp g{};
+      g.kind = OP_GEMM;
+      g.level = level + 1;
+      g.c_i = r1; g.c_j = r0;   // rows of B2 x cols of B1
+      g.a_i = r1; g.a_j = off;  // A21 rows of B2
+      g.b_i = r0; g.b_j = off;  // A21 rows of B1
+      g.m = n2c; g.n = n1c; g.k = n1;
+      g.flops = 2.0 * n2c * n1c * n1;
+      g.deferred = 1;
+      ops.push_back(g);
+      syrk(r1, n2c);
+      ops.back().deferred = 1;
+    };
+    trailing(off + n1, n2, p.lookahead_depth < 1 ? 1 : p.lookahead_depth);
   } else {
     syrk(off + n1, n2);
   }

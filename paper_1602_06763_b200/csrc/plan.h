@@ -60,6 +60,10 @@ struct PlanParams {
   // GEMM(B21) + SYRK(B22), so potrf(B11) only waits for SYRK(B11) and the
   // bulk of the trailing update can run concurrently with it
   bool lookahead = false;
+  // lookahead depth: the top-left part B11 of the split is itself split the
+  // same way this many times (1 = one split), so the first leaf of potrf(A22)
+  // waits only for the update of its own corner
+  int lookahead_depth = 1;
   // > 0: the TRSM of a node's A21 is issued as independent row panels of this
   // many rows (rows of B are independent), so the DAG can overlap the panels'
   // chains with each other and start the trailing updates of finished rows
