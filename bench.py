@@ -275,7 +275,8 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
     traffic, traffic_note = _committed_traffic(W.shape[0])
     roofline = {
         "kernel": "k_update (SYRK + recursive-TRSM GEMM, DMMA.8x8x4)",
-        "bound": "fp64_tensor",
+        "bound": "tensor",
+        "pipe": "FP64 DMMA (mma.sync m8n8k4 f64; sm_100a has no tcgen05 FP64 kind)",
         "achieved": round(achieved, 3),
         "peak": FP64_PEAK_TFLOPS_DATASHEET,
         "unit": "TFLOP/s",
@@ -387,6 +388,26 @@ def run_batch(args, rank, world, dev):
         times = [step() for _ in range(args.steps)]
     exp = b["expected_info"][lo:hi]
     assert np.array_equal(d_info.cpu().numpy(), exp), "per-matrix info mismatch"
+    # end to end: the pinned host batch goes over, is factored, and the
+    # matrices and per-matrix info come back, all inside the timed region
+    H_in = torch.from_numpy(host).pin_memory()
+    H_out = torch.empty_like(H_in).pin_memory()
+    h_info = torch.empty(len(ns), dtype=torch.int32).pin_memory()
+    e2e_times = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        W.copy_(H_in, non_blocking=True)
+        rl.dpotrf_batched(d_ns, ptrs, d_ld, d_info, "L", stream=st)
+        H_out.copy_(W, non_blocking=True)
+        h_info.copy_(d_info, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        if i > 0:
+            e2e_times.append(e0.elapsed_time(e1))
+    assert np.array_equal(h_info.numpy(), exp)
+    e2e_ms = _max_over_ranks(sum(e2e_times) / max(1, len(e2e_times)), world, dev) if e2e_times else None
     ms = sum(times) / len(times)
     ms_max = _max_over_ranks(ms, world, dev)
     tot_flops = float((b["ns"].astype(np.float64) ** 3).sum() / 3.0)
@@ -408,7 +429,11 @@ def run_batch(args, rank, world, dev):
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
                      "note": "algorithmic bytes = lower triangles read + written once (8 n(n+1) per matrix)"},
         "gb_per_s": round(tot_bytes / (ms_max / 1e3) / 1e9, 1),
-        "gpu_launches": args.steps, "step_times_ms": [round(t, 4) for t in times], "clocks": clk.summary(),
+        "gpu_launches": 5 * args.steps, "step_times_ms": [round(t, 4) for t in times], "clocks": clk.summary(),
+        "e2e": ({"value": round(tot_flops / (e2e_ms / 1e3) / 1e9, 2), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
+                 "h2d_bytes_per_step": int(host.nbytes) * world, "d2h_bytes_per_step": int(host.nbytes + 4 * len(ns)) * world,
+                 "steps": len(e2e_times), "api": "relapack_dpotrf_batched on a pinned host batch copied in and out"}
+                if e2e_ms else None),
         "info_parity": "per-matrix info == closed form (k+1 for the 1% negated diagonals)",
     }
     print(json.dumps(out))
@@ -480,6 +505,9 @@ def run_dist(args, rank, world, dev, n, uplo, dist):
         "pct_fp64_peak_per_gpu": round(100 * gflops / 1e3 / FP64_PEAK_TFLOPS_DATASHEET / world, 2),
         "gpu_launches": launches * args.steps, "step_times_ms": [round(t, 4) for t in times],
         "clocks": clk.summary(),
+        "roofline": None,
+        "e2e": None,
+        "e2e_note": "relapack_dpotrf_dist takes device buffers (SPMD, one replica per rank); no host-matrix path",
     }
     print(json.dumps(out))
     return 0

@@ -32,6 +32,10 @@ namespace relapack {
 namespace {
 
 constexpr int BK = 16, STAGES = 4;
+#ifndef RELAPACK_PREFETCH_C
+#define RELAPACK_PREFETCH_C 1
+#endif
+constexpr bool kPrefetchC = RELAPACK_PREFETCH_C != 0;
 
 template <int TBM>
 struct Cfg {
@@ -170,6 +174,22 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
   const int kt_per = (KT_all + args.ksplit - 1) / args.ksplit;
   const int kt0 = split * kt_per;
   const int KT = max(0, min(KT_all, kt0 + kt_per) - kt0);  // k-tiles of this split, from kt0
+
+  // Pull this tile of C towards L2 now, so the epilogue's read-modify-write
+  // does not start with a DRAM round trip (matters for short K).  Lines along
+  // the contiguous dimension; diagonal SYRK tiles are skipped (their upper
+  // half belongs to the other triangle).
+  if (kPrefetchC && split == 0 && !(args.tri && tm == tn)) {
+    const int flim = LAYOUT == kLayoutN ? args.M : args.N, slim = LAYOUT == kLayoutN ? args.N : args.M;
+    const int f0 = LAYOUT == kLayoutN ? m0 : n0, s0 = LAYOUT == kLayoutN ? n0 : m0;
+    const int fext = min(TBM, flim - f0), sext = min(TBM, slim - s0);
+    constexpr int kLineD = 16;  // doubles per 128-byte line
+    const int lines = (fext + kLineD - 1) / kLineD;
+    for (int e = threadIdx.x; e < lines * sext; e += C::THREADS) {
+      const double* pc = args.C + (f0 + (e % lines) * kLineD) + (int64_t)(s0 + e / lines) * args.ldc;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pc));
+    }
+  }
 
   double acc[C::MT][C::NT][2];
 #pragma unroll
@@ -391,9 +411,14 @@ int update_ksplit_for(int M, int N, int K, int tri, int tile) {
     }
     return bks;
   }
-  if (KT < 16) return 1;
+  static const int min_kt = [] {  // k-tiles per split (RELAPACK_SPLITK_KT, default 8)
+    const char* v = getenv("RELAPACK_SPLITK_KT");
+    const int x = v ? atoi(v) : 8;
+    return x < 1 ? 1 : x;
+  }();
+  if (KT < 2 * min_kt) return 1;
   int ks = (int)((2 * 148 + tiles - 1) / tiles);
-  ks = ks < KT / 8 ? ks : KT / 8;
+  ks = ks < KT / min_kt ? ks : KT / min_kt;
   ks = ks < 16 ? ks : 16;
   return ks >= 2 ? ks : 1;
 }
