@@ -99,6 +99,17 @@ def dpotrf_cols(A: np.ndarray, uplo: str, ncols: int) -> int:
     return _load().oracle_dpotrf_cols(uplo.encode(), A.shape[1], _ptr(A), max(1, A.shape[0]), ncols)
 
 
+def dpotrf_cols_panel(P: np.ndarray, ncols: int) -> int:
+    """uplo='L' only: the first `ncols` columns of the factorization of an
+    n x n matrix given only its first ncols columns P (n x ncols, Fortran, lda
+    = n).  The left-looking loop for column j reads columns < j and column j
+    only, so the trailing columns it never touches need not exist."""
+    _check_f64_fortran(P, "P")
+    n, w = P.shape
+    assert ncols <= w
+    return _load().oracle_dpotrf_cols(b"L", n, _ptr(P), max(1, n), ncols)
+
+
 def dpotrf_batched(uplo: str, ns: np.ndarray, buf: np.ndarray, offsets: np.ndarray, ldas: np.ndarray) -> np.ndarray:
     """Per-matrix Cholesky of a packed batch; returns the per-matrix info array."""
     ns = np.ascontiguousarray(ns, dtype=np.int32)
