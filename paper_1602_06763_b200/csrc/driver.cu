@@ -259,6 +259,65 @@ static cudaEvent_t prof_event() {
 
 __global__ void k_noop() {}
 
+// 2-D copy dst[c * dld + r] = src[c * sld + r], r < w (contiguous), c < h; one
+// of the two is pinned host memory addressed through UVA.  16-byte accesses
+// when both sides allow them, many loads in flight per thread.
+__global__ void __launch_bounds__(256) k_copy2d(double* __restrict__ dst, int64_t dld,
+                                                const double* __restrict__ src, int64_t sld, int64_t w, int64_t h,
+                                                int vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    const int64_t w2 = w / 2, tot = w2 * h;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < tot; e0 += 4 * stride) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * stride;
+        if (e < tot) v[u] = reinterpret_cast<const double2*>(src + (e / w2) * sld)[e % w2];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * stride;
+        if (e < tot) reinterpret_cast<double2*>(dst + (e / w2) * dld)[e % w2] = v[u];
+      }
+    }
+  } else {
+    const int64_t tot = w * h;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < tot; e0 += 4 * stride) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * stride;
+        if (e < tot) v[u] = src[(e / w) * sld + e % w];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * stride;
+        if (e < tot) dst[(e / w) * dld + e % w] = v[u];
+      }
+    }
+  }
+}
+
+static cudaError_t launch_copy2d(double* dst, int64_t dld, const double* src, int64_t sld, int64_t w, int64_t h,
+                                 cudaStream_t st) {
+  const bool vec = (w % 2 == 0) && (dld % 2 == 0) && (sld % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  const int64_t items = vec ? (w / 2) * h : w * h;
+  int grid = (int)((items + 256 * 4 - 1) / (256 * 4));
+  grid = grid < 8 ? (grid < 1 ? 1 : grid) : 8;  // 8 CTAs keep ~32 KB of PCIe requests in flight
+  k_copy2d<<<grid, 256, 0, st>>>(dst, dld, src, sld, w, h, vec ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// Host-matrix copies as cudaMemcpy2DAsync nodes (default) or SM kernels
+// (RELAPACK_COPY_KERNEL=1; measured slower: n = 16384 e2e 78.8 vs 65.4 ms,
+// tools/exp15.sh).
+static bool copy_kernels() {
+  static const bool on = env_int("RELAPACK_COPY_KERNEL", 0) != 0;
+  return on;
+}
+
 // Timing experiments only (tools/): RELAPACK_DEBUG_SKIP = bit mask of op kinds
 // (1 potf2, 2 trsm, 4 gemm, 8 syrk) replaced by an empty kernel.  The result
 // is then not a factorization.
@@ -282,6 +341,13 @@ static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, in
       const size_t height = layout == kLayoutN ? op.k : op.m;
       double* dev = A + lv_off(layout, op.c_i, op.c_j, ld);
       double* host = const_cast<double*>(pl.host) + lv_off(layout, op.c_i, op.c_j, pl.hld);
+      if (copy_kernels()) {
+        // SM-driven copy through the pinned mapping: H2D and D2H blocks run
+        // concurrently (both link directions) as ordinary DAG kernel nodes
+        const int64_t w = (int64_t)(width / sizeof(double)), h = (int64_t)height;
+        return op.kind == OP_H2D ? launch_copy2d(dev, ld, host, pl.hld, w, h, st)
+                                 : launch_copy2d(host, pl.hld, dev, ld, w, h, st);
+      }
       return op.kind == OP_H2D
                  ? cudaMemcpy2DAsync(dev, ld * sizeof(double), host, pl.hld * sizeof(double), width, height,
                                      cudaMemcpyHostToDevice, st)

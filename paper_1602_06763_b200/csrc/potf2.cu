@@ -47,40 +47,41 @@ struct P2 {
 };
 
 // Apply the rank-8 update of panel columns [j0, j0+8) to the 8x8 tiles
-// (ti, tk), tile index range [t_beg, t_end) of the lower-triangular tile grid
-// whose first row/column is r0; tiles with tk < tk_min are skipped.  Two tiles
-// are in flight per warp (DMMA.8x8x4, K = 8 -> 2 dependent DMMA per tile).
+// (ti, tk), tile index range [t_beg, t_end) (stride tile_step) of the
+// lower-triangular tile grid whose first row/column is r0.  Four tiles are in
+// flight per warp (DMMA.8x8x4, K = 8 -> 2 dependent DMMA per tile).
 template <int LDS>
 __device__ __forceinline__ void trail_tiles(double* s, int j0, int r0, int tile_beg, int tile_end, int tile_step,
                                             int g, int t) {
-  for (int base = tile_beg; base < tile_end; base += 2 * tile_step) {
-    double c0[2], c1[2];
-    int ii[2], kk[2];
+  constexpr int QB = 4;
+  for (int base = tile_beg; base < tile_end; base += QB * tile_step) {
+    double c0[QB], c1[QB], a[QB][2], b[QB][2];
+    int ii[QB], kk[QB];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < QB; ++q) {
       const int tile = base + q * tile_step;
-      int ti = 0;
-      while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+      int ti = (int)((sqrtf(8.0f * (float)tile + 1.0f) - 1.0f) * 0.5f);
+      ti += ((ti + 1) * (ti + 2) / 2 <= tile);
+      ti -= (ti * (ti + 1) / 2 > tile);
       const int tk = tile - ti * (ti + 1) / 2;
       ii[q] = r0 + 8 * ti;
       kk[q] = r0 + 8 * tk;
       const bool ok = tile < tile_end;
-      c0[q] = ok ? s[(ii[q] + g) + (kk[q] + 2 * t) * LDS] : 0.0;
-      c1[q] = ok ? s[(ii[q] + g) + (kk[q] + 2 * t + 1) * LDS] : 0.0;
-    }
+      if (!ok) ii[q] = kk[q] = r0;  // in-range addresses, results discarded
+      c0[q] = s[(ii[q] + g) + (kk[q] + 2 * t) * LDS];
+      c1[q] = s[(ii[q] + g) + (kk[q] + 2 * t + 1) * LDS];
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (base + q * tile_step < tile_end) {
-          const double a = -s[(ii[q] + g) + (j0 + 4 * ks + t) * LDS];
-          const double b = s[(kk[q] + g) + (j0 + 4 * ks + t) * LDS];
-          dmma_884(c0[q], c1[q], a, b);
-        }
+      for (int ks = 0; ks < 2; ++ks) {
+        a[q][ks] = -s[(ii[q] + g) + (j0 + 4 * ks + t) * LDS];
+        b[q][ks] = s[(kk[q] + g) + (j0 + 4 * ks + t) * LDS];
       }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int q = 0; q < QB; ++q) dmma_884(c0[q], c1[q], a[q][ks], b[q][ks]);
+#pragma unroll
+    for (int q = 0; q < QB; ++q) {
       if (base + q * tile_step < tile_end) {
         s[(ii[q] + g) + (kk[q] + 2 * t) * LDS] = c0[q];
         s[(ii[q] + g) + (kk[q] + 2 * t + 1) * LDS] = c1[q];
