@@ -155,6 +155,17 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
       if ((j0 >> 5) == r) own = x[r][0];
     dsh = __shfl_sync(0xffffffffu, own, j0 & 31);  // lane (j0 & 31) holds a_{j0,j0}
   }
+  // Column c's update of column c+1 is done at once (it feeds the next
+  // pivot); its updates of columns c+2.. are deferred into iteration c+1,
+  // where they are issued behind that column's rsqrt chain instead of in
+  // front of it (in-order issue).
+  auto row_val = [&](int c, int row) -> double {  // x[row][c] as held by lane row & 31
+    double v = x[0][c];
+#pragma unroll
+    for (int r = 1; r < R; ++r)
+      if ((row >> 5) == r) v = x[r][c];
+    return v;
+  };
 #pragma unroll
   for (int c = 0; c < kPanel; ++c) {
     const int j = j0 + c;
@@ -162,32 +173,25 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
     dpiv[c] = d;
     const double rinv = rsqrt_nr(d);
     rpiv[c] = rinv;
+    if (c >= 1) {
+#pragma unroll
+      for (int c2 = c + 1; c2 < kPanel; ++c2) {
+        const int jj = j0 + c2;
+        const double l = __shfl_sync(0xffffffffu, row_val(c - 1, jj), jj & 31);  // l_{jj, j-1}
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r][c2] -= x[r][c - 1] * l;
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r][c] *= rinv;
     if (c + 1 < kPanel) {
       // the lane holding row j+1 forms the next pivot from its own registers
       const int jn = j + 1;
-      double xn = x[0][c], an = x[0][c + 1];
-#pragma unroll
-      for (int r = 1; r < R; ++r)
-        if ((jn >> 5) == r) {
-          xn = x[r][c];
-          an = x[r][c + 1];
-        }
-      // broadcast the next pivot before the remaining column updates, so the
-      // in-order issue of those does not delay the chain
+      const double xn = row_val(c, jn), an = row_val(c + 1, jn);
       dsh = __shfl_sync(0xffffffffu, an - xn * xn, jn & 31);
+      const double l = __shfl_sync(0xffffffffu, xn, jn & 31);  // l_{j+1, j}
 #pragma unroll
-      for (int c2 = c + 1; c2 < kPanel; ++c2) {
-        const int jj = j0 + c2;
-        double src = x[0][c];
-#pragma unroll
-        for (int r = 1; r < R; ++r)
-          if ((jj >> 5) == r) src = x[r][c];
-        const double l = __shfl_sync(0xffffffffu, src, jj & 31);  // l_{jj, j}
-#pragma unroll
-        for (int r = 0; r < R; ++r) x[r][c2] -= x[r][c] * l;
-      }
+      for (int r = 0; r < R; ++r) x[r][c + 1] -= x[r][c] * l;
     }
   }
   int fail = 0;

@@ -38,6 +38,8 @@ int main() {
     printf("potf2 n=64 phases (cycles from start): stage-in %lld |", pr[1] - pr[0]);
     for (int p = 0; p < 8; ++p) printf(" P%d %lld |", p, pr[2 + p] - pr[0]);
     printf(" factor-end %lld end %lld\n", pr[62] - pr[0], pr[63] - pr[0]);
+    printf("potf2 n=64 panel j0=16 (warp 0): strip_update %lld | factor_panel %lld | barrier wait %lld\n",
+           pr[41] - pr[40], pr[42] - pr[41], pr[43] - pr[42]);
     launch_potf2(d, n, kLayoutN, 128, info, 0, 0);
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
