@@ -40,6 +40,12 @@ constexpr bool kPrefetchC = RELAPACK_PREFETCH_C != 0;
 template <int TBM>
 struct Cfg {
   static constexpr int NUM_WARPS = TBM == 128 ? 8 : 4;  // 8 warps keep 2 per SMSP (255-reg budget)
+#ifndef RELAPACK_UPD64_BLOCKS
+#define RELAPACK_UPD64_BLOCKS 1
+#endif
+  // resident CTAs per SM the register budget is sized for (64-tiles with a
+  // 3-CTA budget measured slightly slower: compile-time knob, default 1)
+  static constexpr int MIN_BLOCKS = TBM == 128 ? 1 : RELAPACK_UPD64_BLOCKS;
   static constexpr int THREADS = NUM_WARPS * 32;
   static constexpr int WTM = TBM == 128 ? 64 : 32;      // warp tile rows
   static constexpr int WTN = 32;                        // warp tile cols
@@ -321,7 +327,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
 }
 
 template <int LAYOUT, bool USE_TMA, int TBM>
-__global__ void __launch_bounds__(Cfg<TBM>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
     k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args) {
   if (ld_info(args.d_info) != 0) return;  // dpotrf2 semantics: stop after a failed pivot
   extern __shared__ uint8_t smem_raw[];
