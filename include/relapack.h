@@ -210,6 +210,18 @@ RELAPACK_API void relapack_profile_reset(void);
  * recursion level, algorithmic flops, milliseconds.  Returns the count. */
 RELAPACK_API int relapack_profile_records(int max, double* out);
 
+/*
+ * Timeline of the last factorization run with RELAPACK_TRACE=1 in the
+ * environment (the captured graph itself, not a serialised replay): every
+ * kernel records the %globaltimer of its first CTA's start and its last CTA's
+ * end.  Writes up to `max` records of 7 doubles in plan order — op kind
+ * (0 potf2, 1 trsm, 2 gemm, 3 syrk, 20/21 copies: -1 times), m, n, k,
+ * algorithmic flops, start and end in microseconds from the earliest start
+ * (-1 if the op launched no kernel) — and returns the count, 0 when no traced
+ * run exists, -1 on a CUDA error.  Synchronises the device.
+ */
+RELAPACK_API int relapack_trace_read(int max, double* out);
+
 /* Library version string (build id). */
 RELAPACK_API const char* relapack_version(void);
 

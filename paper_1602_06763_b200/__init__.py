@@ -95,6 +95,8 @@ def lib():
         L.relapack_profile_reset.restype = None
         L.relapack_profile_records.argtypes = [c_int, ctypes.POINTER(c_double)]
         L.relapack_profile_records.restype = c_int
+        L.relapack_trace_read.argtypes = [c_int, ctypes.POINTER(c_double)]
+        L.relapack_trace_read.restype = c_int
         L.relapack_dpotrf_dist_loopback.argtypes = [ctypes.c_char_p, c_int, c_void_p, c_int, c_int, c_int, c_int, ip]
         L.relapack_dpotrf_dist_loopback.restype = c_int
         L.relapack_dist_schedule.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_int,
@@ -169,6 +171,22 @@ def profile_records(max_records: int = 100000):
         r = buf[7 * i: 7 * i + 7]
         out.append(dict(kind=kinds[int(r[0])], m=int(r[1]), n=int(r[2]), k=int(r[3]), level=int(r[4]),
                         flops=r[5], ms=r[6]))
+    return out
+
+
+def trace_records(max_records: int = 100000):
+    """Kernel timeline of the last RELAPACK_TRACE=1 factorization: list of dicts
+    (kind, m, n, k, flops, t0_us, t1_us) in plan order (see include/relapack.h)."""
+    buf = (ctypes.c_double * (7 * max_records))()
+    cnt = lib().relapack_trace_read(max_records, buf)
+    if cnt < 0:
+        raise RelapackError(f"relapack_trace_read failed: {last_error()}")
+    names = {0: "potf2", 1: "trsm", 2: "gemm", 3: "syrk", 20: "h2d", 21: "d2h"}
+    out = []
+    for i in range(cnt):
+        r = buf[7 * i: 7 * i + 7]
+        out.append(dict(kind=names.get(int(r[0]), str(int(r[0]))), m=int(r[1]), n=int(r[2]), k=int(r[3]),
+                        flops=r[4], t0_us=r[5], t1_us=r[6]))
     return out
 
 

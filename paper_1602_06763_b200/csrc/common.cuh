@@ -107,6 +107,30 @@ __device__ __forceinline__ double sqrt_from_rsqrt(double d, double y) {
   return fma(e, 0.5 * y, r);
 }
 
+// Per-launch timeline record (tools/trace_timeline.py): earliest CTA start and
+// latest CTA end in %globaltimer ns; null when tracing is off.
+struct TraceRec {
+  unsigned long long t0, t1;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void trace_begin(TraceRec* tr) {
+  if (tr && threadIdx.x == 0) atomicMin(&tr->t0, globaltimer_ns());
+}
+
+// Call at the end of a kernel by every thread (contains a barrier when on).
+__device__ __forceinline__ void trace_end(TraceRec* tr) {
+  if (tr) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&tr->t1, globaltimer_ns());
+  }
+}
+
 __device__ __forceinline__ int ld_info(const int* d_info) {
   return *reinterpret_cast<const volatile int*>(d_info);
 }

@@ -43,6 +43,8 @@ int cuda_fail(cudaError_t e, const char* what) {
   return -1000 - (int)e;
 }
 
+thread_local TraceRec* g_launch_trace = nullptr;
+
 // ------------------------------------------------------------------ knobs
 static std::atomic<int> g_crossover{-1}, g_split_tile{-1}, g_graphs{-1};
 static std::atomic<uintptr_t> g_stream{0};
@@ -90,8 +92,16 @@ static bool dag_enabled() { return env_int("RELAPACK_DAG", 1) != 0; }
 // CTA cap of the deferred (lookahead) trailing updates: leaves SMs to the
 // next panel's chain; 0 = uncapped
 static int bulk_ctas() { return env_int("RELAPACK_BULK_CTAS", 132); }
+// CTA cap of the non-deferred updates (0 = uncapped)
+static int upd_ctas() { return env_int("RELAPACK_UPD_CTAS", 0); }
 
 static bool splitk_enabled() { return env_int("RELAPACK_SPLITK", 1) != 0; }
+
+// RELAPACK_TRACE=1: every kernel of the plan records its first-CTA start and
+// last-CTA end (tools/trace_timeline.py reads them with relapack_trace_read).
+static bool trace_enabled() { return env_int("RELAPACK_TRACE", 0) != 0; }
+static std::mutex g_trace_mu;
+static const void* g_trace_plan = nullptr;  // the Plan whose trace relapack_trace_read returns
 
 static bool graphs_enabled() {
   int g = g_graphs.load();
@@ -106,11 +116,13 @@ struct Plan {
   int64_t hld = 0;
   std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
   cudaGraphExec_t exec = nullptr;
+  TraceRec* d_trace = nullptr;  // RELAPACK_TRACE=1: per-op kernel start/end (globaltimer)
   double* splitk_ws = nullptr;  // split-K partial tiles, one slot per concurrently runnable update
   int* splitk_cnt = nullptr;    // per-tile arrival counters (self-resetting; zeroed at every run start)
   size_t cnt_bytes = 0;
   ~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
+    if (d_trace) cudaFree(d_trace);
     if (splitk_ws) cudaFree(splitk_ws);
     if (splitk_cnt) cudaFree(splitk_cnt);
   }
@@ -326,8 +338,19 @@ static int debug_skip_mask() {
   return m;
 }
 
+static cudaError_t launch_op_impl(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
+                                  cudaStream_t st);
+
 static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
                              cudaStream_t st) {
+  g_launch_trace = pl.d_trace ? pl.d_trace + i : nullptr;
+  const cudaError_t e = launch_op_impl(pl, i, A, ld, layout, d_info, st);
+  g_launch_trace = nullptr;
+  return e;
+}
+
+static cudaError_t launch_op_impl(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
+                                  cudaStream_t st) {
   const PlanOp& op = pl.ops[i];
   if (debug_skip_mask() & (1 << (int)op.kind)) {
     k_noop<<<1, 32, 0, st>>>();
@@ -369,8 +392,21 @@ static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, in
 
 // Run-start nodes: reset info and (robustness after an early exit) the
 // split-K arrival counters.
+__global__ void k_trace_reset(TraceRec* tr, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    tr[i].t0 = ~0ull;
+    tr[i].t1 = 0;
+  }
+}
+
 static cudaError_t run_prologue(const Plan& pl, int* d_info, cudaStream_t st) {
   cudaError_t e = launch_set_int(d_info, 0, st);
+  if (e == cudaSuccess && pl.d_trace) {
+    const int n = (int)pl.ops.size();
+    k_trace_reset<<<(n + 255) / 256, 256, 0, st>>>(pl.d_trace, n);
+    e = cudaGetLastError();
+  }
   if (e == cudaSuccess && pl.splitk_cnt) e = cudaMemsetAsync(pl.splitk_cnt, 0, pl.cnt_bytes, st);
   return e;
 }
@@ -479,8 +515,10 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   if ((e = ensure_device(ds)) != cudaSuccess) return cuda_fail(e, "device setup");
   const bool use_dag = use_graph && dag_enabled();
   const int bulk = bulk_ctas();
+  const int upd_cap = upd_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24), bulk,
+              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24) |
+                  (trace_enabled() ? (1 << 30) : 0), bulk * 1024 + upd_cap,
               reinterpret_cast<uintptr_t>(host), hld};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
@@ -503,10 +541,16 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
       p->hld = hld;
     }
     p->upd.resize(p->ops.size());
+    if (trace_enabled() && (e = cudaMalloc(&p->d_trace, p->ops.size() * sizeof(TraceRec))) != cudaSuccess)
+      return cuda_fail(e, "trace buffer");
     for (size_t i = 0; i < p->ops.size(); ++i)
       if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) {
         fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
         if (use_dag && p->ops[i].deferred) p->upd[i].max_ctas = bulk;
+        // every other big update also leaves a few SMs free, so a base case
+        // or TRSM that becomes ready does not wait for a long tile to drain
+        // (tools/trace_timeline.py: otherwise the chain waits ~24 ms at n = 16384)
+        else if (use_dag && upd_cap > 0) p->upd[i].max_ctas = upd_cap;
       }
     std::vector<std::vector<int>> deps;
     std::vector<uint64_t> anc;
@@ -548,7 +592,36 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   else
     e = run_ops(*plan, A, ld, layout, d_info, st, profile);
   if (e != cudaSuccess) return cuda_fail(e, "launch");
+  if (plan->d_trace) {
+    std::lock_guard<std::mutex> tl(g_trace_mu);
+    g_trace_plan = plan;
+  }
   return 0;
+}
+
+// Copy the last traced plan's records: 7 doubles per op (kind, m, n, k, flops,
+// start_us, end_us; times relative to the earliest start).  Synchronizes.
+int trace_read(int max, double* out) {
+  std::lock_guard<std::mutex> tl(g_trace_mu);
+  const Plan* pl = static_cast<const Plan*>(g_trace_plan);
+  if (!pl || !pl->d_trace) return 0;
+  const size_t nops = pl->ops.size();
+  std::vector<TraceRec> h(nops);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(h.data(), pl->d_trace, nops * sizeof(TraceRec), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  unsigned long long t00 = ~0ull;
+  for (const TraceRec& r : h)
+    if (r.t1 && r.t0 < t00) t00 = r.t0;
+  int cnt = 0;
+  for (size_t i = 0; i < nops && cnt < max; ++i, ++cnt) {
+    const PlanOp& op = pl->ops[i];
+    double* o = out + 7 * cnt;
+    o[0] = op.kind; o[1] = op.m; o[2] = op.n; o[3] = op.k; o[4] = op.flops;
+    o[5] = h[i].t1 ? (double)(h[i].t0 - t00) * 1e-3 : -1.0;
+    o[6] = h[i].t1 ? (double)(h[i].t1 - t00) * 1e-3 : -1.0;
+  }
+  return cnt;
 }
 
 static int check_args(char uplo, int n, const void* A, int lda, int* layout) {
@@ -882,6 +955,8 @@ int relapack_profile_read(int kind, double* ms_total, double* flops_total, int* 
   if (launches) *launches = cnt;
   return 0;
 }
+
+int relapack_trace_read(int max, double* out) { return max < 0 || !out ? -1 : trace_read(max, out); }
 
 int relapack_profile_records(int max, double* out) {
   std::lock_guard<std::mutex> lk(g_prof_mu);

@@ -8,6 +8,11 @@
 namespace relapack {
 
 constexpr int kMaxDevices = 64;
+
+struct TraceRec;
+// Trace slot of the launch being issued (set by the driver around each op in
+// trace mode, read by the launch functions; null otherwise).
+extern thread_local TraceRec* g_launch_trace;
 constexpr int RELAPACK_BATCH_NMAX_ = 64;  // == RELAPACK_BATCH_NMAX in include/relapack.h
 
 // ---- K3/K4 update (update.cu) ----

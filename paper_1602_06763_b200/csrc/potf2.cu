@@ -294,9 +294,10 @@ __device__ __forceinline__ void copy_lower(double* s, double* __restrict__ A, in
 constexpr int kBaseMax = kPotf2Max;  // 128
 
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A, int64_t ld, int layout, int n,
-                                                                       int* d_info, int info_base) {
+                                                                       int* d_info, int info_base, TraceRec* tr) {
   PROBE(0);
   if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
   if (threadIdx.x == 0) fail_flag = 0;
@@ -307,13 +308,15 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   copy_lower<kBaseMax, false>(s, A, ld, layout, n);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
   PROBE(63);
+  trace_end(tr);
 }
 
 // Same kernel sized for n <= 64 (4 warps, 33 KB): used when the block is small.
 __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int64_t ld, int layout, int n,
-                                                                  int* d_info, int info_base) {
+                                                                  int* d_info, int info_base, TraceRec* tr) {
   PROBE(0);
   if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
   if (threadIdx.x == 0) fail_flag = 0;
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   copy_lower<64, false>(s, A, ld, layout, n);
   PROBE(63);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+  trace_end(tr);
 }
 
 // Copy the lower-triangle part (i >= j, i < n) of the L-view rectangle rows
@@ -475,10 +479,11 @@ __device__ __forceinline__ void syrk_in_smem(double* s, int n2) {
 }
 
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double* A, int64_t ld, int layout, int n,
-                                                                          int* d_info, int info_base) {
+                                                                          int* d_info, int info_base, TraceRec* tr) {
   constexpr int LDS = P2<kBaseMax>::LDS, NW = P2<kBaseMax>::NW;
   PROBE(50);
   if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
   __shared__ double rinv[kN1];
@@ -515,6 +520,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   }
   PROBE(56);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+  trace_end(tr);
 }
 
 // One warp, the whole block in registers (chol_regs.cuh): n <= 8 TN.  The
@@ -523,9 +529,10 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
 // same way.
 template <int TN>
 __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int layout, int n, int* d_info,
-                                                      int info_base) {
+                                                      int info_base, TraceRec* tr) {
   using T = RegTri<TN>;
   if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
   const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
   double v[T::NT][2];
 #pragma unroll
@@ -548,6 +555,7 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
         if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q];
       }
   if (fail && fail <= n && lane == 0) *d_info = info_base + fail;
+  trace_end(tr);
 }
 
 // Register kernel for n <= 32 (measured faster: 6.2 vs 10.3 us at n = 32),
@@ -589,21 +597,21 @@ cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, 
   if (n > kPotf2Max) return cudaErrorInvalidValue;
   if (potf2_use_regs(n)) {
     switch ((n + 7) / 8) {
-      case 1: k_potf2_reg<1><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      case 2: k_potf2_reg<2><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      case 3: k_potf2_reg<3><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      case 4: k_potf2_reg<4><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      case 5: k_potf2_reg<5><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      case 6: k_potf2_reg<6><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      case 7: k_potf2_reg<7><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
-      default: k_potf2_reg<8><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base); break;
+      case 1: k_potf2_reg<1><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      case 2: k_potf2_reg<2><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      case 3: k_potf2_reg<3><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      case 4: k_potf2_reg<4><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      case 5: k_potf2_reg<5><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      case 6: k_potf2_reg<6><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      case 7: k_potf2_reg<7><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
+      default: k_potf2_reg<8><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
     }
   } else if (n <= 64)
-    k_potf2_base64<<<1, P2<64>::THREADS, P2<64>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
+    k_potf2_base64<<<1, P2<64>::THREADS, P2<64>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
   else if (potf2_node128())
-    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
+    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
   else
-    k_potf2_base<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base);
+    k_potf2_base<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
   return cudaGetLastError();
 }
 

@@ -57,8 +57,9 @@ __device__ __forceinline__ void solve_steps(double (&x0)[R], double (&x1)[R], co
 template <int R>
 __global__ void __launch_bounds__(kTsThreads) k_trsm_base(const double* __restrict__ L, int64_t ldl,
                                                         double* __restrict__ B, int64_t ldb, int layout, int m, int t,
-                                                        const int* d_info) {
+                                                        const int* d_info, TraceRec* tr) {
   if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
   constexpr int kRows = kWarps * R;  // rows per CTA
   extern __shared__ double smem_d[];
   double* sL = smem_d;                // sL[k + j*kLd] = L(k, j) for k > j, else 0
@@ -144,13 +145,14 @@ __global__ void __launch_bounds__(kTsThreads) k_trsm_base(const double* __restri
     }
     if (r < rows && j < t) B[lv_off(layout, r0 + r, j, ldb)] = sB[r * kLd + j];
   }
+  trace_end(tr);
 }
 
 template <int R>
 cudaError_t launch_r(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t, const int* d_info,
                      cudaStream_t st) {
   const int grid = (m + kWarps * R - 1) / (kWarps * R);
-  k_trsm_base<R><<<grid, kTsThreads, smem_bytes<R>(), st>>>(L, ldl, B, ldb, layout, m, t, d_info);
+  k_trsm_base<R><<<grid, kTsThreads, smem_bytes<R>(), st>>>(L, ldl, B, ldb, layout, m, t, d_info, g_launch_trace);
   return cudaGetLastError();
 }
 

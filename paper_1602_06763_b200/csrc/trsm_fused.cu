@@ -122,10 +122,11 @@ __device__ __forceinline__ void stage_L_all(double* sL, double* rinv, const doub
 template <int NW>
 __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
     k_trsm_fused(const double* __restrict__ L, int64_t ldl, double* __restrict__ B, int64_t ldb, int layout, int m,
-                 int t, const int* d_info) {
+                 int t, const int* d_info, TraceRec* tr) {
   constexpr int kFRows = TF<NW>::ROWS, kFThreads = TF<NW>::THREADS;
   TPROBE(0);
   if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
   extern __shared__ double smem_t[];
   const int kFLdX = TF<NW>::ldx(t);
   double* sX = smem_t;                   // sX[r * kFLdX + c]
@@ -247,13 +248,15 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
     }
   }
   TPROBE(20);
+  trace_end(tr);
 }
 
 template <int NW>
 cudaError_t launch_nw(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                       const int* d_info, cudaStream_t st) {
   const int grid = (m + TF<NW>::ROWS - 1) / TF<NW>::ROWS;
-  k_trsm_fused<NW><<<grid, TF<NW>::THREADS, TF<NW>::smem(t), st>>>(L, ldl, B, ldb, layout, m, t, d_info);
+  k_trsm_fused<NW><<<grid, TF<NW>::THREADS, TF<NW>::smem(t), st>>>(L, ldl, B, ldb, layout, m, t, d_info,
+                                                                     g_launch_trace);
   return cudaGetLastError();
 }
 

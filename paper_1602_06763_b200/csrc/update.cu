@@ -328,8 +328,10 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
 
 template <int LAYOUT, bool USE_TMA, int TBM>
 __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
-    k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args) {
+    k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args,
+             TraceRec* tr) {
   if (ld_info(args.d_info) != 0) return;  // dpotrf2 semantics: stop after a failed pivot
+  trace_begin(tr);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nwork = args.ntiles * args.ksplit;
@@ -337,11 +339,12 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
     if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
     update_item<LAYOUT, USE_TMA, TBM>(tmA, tmB, args, smem, work);
   }
+  trace_end(tr);
 }
 
 template <int LAYOUT, bool USE_TMA, int TBM>
 cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const UpdateArgs& a, int grid, cudaStream_t st) {
-  k_update<LAYOUT, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a);
+  k_update<LAYOUT, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a, g_launch_trace);
   return cudaGetLastError();
 }
 

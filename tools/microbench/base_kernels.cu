@@ -6,6 +6,9 @@
 #include "../../paper_1602_06763_b200/csrc/potf2.cu"
 #include "../../paper_1602_06763_b200/csrc/trsm.cu"
 #include "../../paper_1602_06763_b200/csrc/trsm_fused.cu"
+namespace relapack {
+thread_local TraceRec* g_launch_trace = nullptr;  // defined by driver.cu in the library
+}
 using namespace relapack;
 int main() {
   const int n = 4096;
