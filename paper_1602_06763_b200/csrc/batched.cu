@@ -46,6 +46,19 @@ template <int NMAX, int LAYOUT>
 struct BC {
   static constexpr int TN = NMAX / 8;
   static constexpr int WPC = 4;  // warps (matrices in flight) per CTA
+  // CTAs per SM the register budget is sized for: more warps in flight hide
+  // the per-matrix column chain (compile-time knobs RELAPACK_BATCH_MINB<NMAX>)
+#ifndef RELAPACK_BATCH_MINB32
+#define RELAPACK_BATCH_MINB32 3
+#endif
+#ifndef RELAPACK_BATCH_MINB48
+#define RELAPACK_BATCH_MINB48 3
+#endif
+#ifndef RELAPACK_BATCH_MINB64
+#define RELAPACK_BATCH_MINB64 2
+#endif
+  static constexpr int MIN_BLOCKS =
+      NMAX == 64 ? RELAPACK_BATCH_MINB64 : NMAX == 48 ? RELAPACK_BATCH_MINB48 : NMAX == 32 ? RELAPACK_BATCH_MINB32 : 8;
   // even-packed lower triangle: NMAX (NMAX/2 + 1) doubles per prefetch slot
   static constexpr int SLOT = NMAX * (NMAX / 2 + 1);
   static constexpr size_t SMEM = sizeof(double) * SLOT * WPC;
@@ -154,7 +167,7 @@ __device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], 
 }
 
 template <int NMAX, int LAYOUT>
-__global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32)
+__global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::MIN_BLOCKS)
     k_batched_cls(int batch, const int* counts, const int* lists, double* const* d_A, const int* d_n,
                   const int* d_lda, int* d_info) {
   using C = BC<NMAX, LAYOUT>;
