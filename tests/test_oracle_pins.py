@@ -427,3 +427,15 @@ def test_oracle_thread_count_independent(tmp_path):
         env = dict(os.environ, OMP_NUM_THREADS=t)
         outs.append(json.loads(subprocess.check_output([sys.executable, "-c", code], env=env)))
     assert outs[0] == outs[1]
+
+
+def test_dpotrf_cols_panel_matches_full():
+    """The column-panel binding (used by the full-size GPU parity test) gives
+    bitwise the first J columns of the whole-matrix left-looking loop."""
+    n, J = 300, 64
+    A = gen.spd(n, 21)
+    full = np.array(A, order="F", copy=True)
+    assert oracle.dpotrf(full, "L") == 0
+    panel = np.asfortranarray(A[:, :J])
+    assert oracle.dpotrf_cols_panel(panel, J) == 0
+    assert np.array_equal(np.tril(panel), np.tril(full[:, :J]))
