@@ -39,13 +39,13 @@ constexpr bool kPrefetchC = RELAPACK_PREFETCH_C != 0;
 
 template <int TBM>
 struct Cfg {
-  static constexpr int NUM_WARPS = TBM == 128 ? 8 : 4;  // 8 warps keep 2 per SMSP (255-reg budget)
+  static constexpr int NUM_WARPS = TBM == 128 ? 8 : TBM == 64 ? 4 : 1;  // 8 warps keep 2 per SMSP (255-reg budget)
 #ifndef RELAPACK_UPD64_BLOCKS
 #define RELAPACK_UPD64_BLOCKS 1
 #endif
   // resident CTAs per SM the register budget is sized for (64-tiles with a
   // 3-CTA budget measured slightly slower: compile-time knob, default 1)
-  static constexpr int MIN_BLOCKS = TBM == 128 ? 1 : RELAPACK_UPD64_BLOCKS;
+  static constexpr int MIN_BLOCKS = TBM == 128 ? 1 : TBM == 64 ? RELAPACK_UPD64_BLOCKS : 4;
   static constexpr int THREADS = NUM_WARPS * 32;
   static constexpr int WTM = TBM == 128 ? 64 : 32;      // warp tile rows
   static constexpr int WTN = 32;                        // warp tile cols
@@ -373,12 +373,28 @@ cudaError_t configure_tbm() {
 
 }  // namespace
 
+// 64-tile count below which 32-tiles are used (RELAPACK_TILE32_BELOW, 0 = never)
+static long small_tile_threshold() {
+  static const long t = [] {
+    const char* v = getenv("RELAPACK_TILE32_BELOW");
+    return v ? atol(v) : 32L;
+  }();
+  return t;
+}
+
 // Tile size for an update: 128 x 128 CTA tiles when they fill the 148 SMs,
-// else 64 x 64 (4x the CTAs; latency of the small updates near the leaves).
+// else 64 x 64 (4x the CTAs; latency of the small updates near the leaves),
+// and 32 x 32 one-warp tiles when even the 64-tiles would leave most SMs
+// idle (the n <= 512 updates on the base-case chain: a 64 x 64 x 128 tile is
+// ~4 us of DMMA on one SM).
 int update_tile_for(int M, int N, int tri) {
-  const long tm = (M + 127) / 128, tn = (N + 127) / 128;
-  const long t128 = tri ? tm * (tm + 1) / 2 : tm * tn;
-  return t128 >= 148 ? 128 : 64;
+  auto tiles = [&](int t) -> long {
+    const long tm = (M + t - 1) / t, tn = (N + t - 1) / t;
+    return tri ? tm * (tm + 1) / 2 : tm * tn;
+  };
+  if (tiles(128) >= 148) return 128;
+  if (tiles(64) >= small_tile_threshold()) return 64;
+  return 32;
 }
 
 static long ntiles_of(int M, int N, int tri, int tile) {
@@ -439,13 +455,14 @@ int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit) {
 cudaError_t configure_update() {
   cudaError_t e = configure_tbm<128>();
   if (e != cudaSuccess) return e;
-  return configure_tbm<64>();
+  if ((e = configure_tbm<64>()) != cudaSuccess) return e;
+  return configure_tbm<32>();
 }
 
 cudaError_t launch_update(const UpdateOp& op, cudaStream_t st) {
   const UpdateArgs& a = op.args;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaSuccess;
-  return op.tile == 128 ? launch_tbm<128>(op, st) : launch_tbm<64>(op, st);
+  return op.tile == 128 ? launch_tbm<128>(op, st) : op.tile == 64 ? launch_tbm<64>(op, st) : launch_tbm<32>(op, st);
 }
 
 // Host: TMA descriptor for an operand block of the L-view (rows x K) with
