@@ -39,16 +39,19 @@ constexpr bool kPrefetchC = RELAPACK_PREFETCH_C != 0;
 
 template <int TBM>
 struct Cfg {
-  static constexpr int NUM_WARPS = TBM == 128 ? 8 : TBM == 64 ? 4 : 1;  // 8 warps keep 2 per SMSP (255-reg budget)
+  // 128: 8 warps of 64x32 (2 per SMSP, 255-reg budget); 64: 4 warps of
+  // 32x32; 32: 4 warps of 16x16 (tiny latency-bound updates: a warp's DMMA
+  // issue, K/4 x MT x NT x 16 cycles, is the floor, so small warp tiles)
+  static constexpr int NUM_WARPS = TBM == 128 ? 8 : 4;
 #ifndef RELAPACK_UPD64_BLOCKS
 #define RELAPACK_UPD64_BLOCKS 1
 #endif
   // resident CTAs per SM the register budget is sized for (64-tiles with a
   // 3-CTA budget measured slightly slower: compile-time knob, default 1)
-  static constexpr int MIN_BLOCKS = TBM == 128 ? 1 : TBM == 64 ? RELAPACK_UPD64_BLOCKS : 4;
+  static constexpr int MIN_BLOCKS = TBM == 128 ? 1 : TBM == 64 ? RELAPACK_UPD64_BLOCKS : 2;
   static constexpr int THREADS = NUM_WARPS * 32;
-  static constexpr int WTM = TBM == 128 ? 64 : 32;      // warp tile rows
-  static constexpr int WTN = 32;                        // warp tile cols
+  static constexpr int WTM = TBM == 128 ? 64 : TBM == 64 ? 32 : 16;  // warp tile rows
+  static constexpr int WTN = TBM == 32 ? 16 : 32;                    // warp tile cols
   static constexpr int MT = WTM / 8, NT = WTN / 8;      // DMMA tiles per warp
   static constexpr int WGM = TBM / WTM;                 // warps along M (2)
   static constexpr int TILE_BYTES = TBM * BK * 8;
@@ -307,16 +310,17 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
   if (fi < flim) {
     double* Cf = args.C + fi;  // + slow * ldc
 #pragma unroll 1
-    for (int q0 = 0; q0 < TBM / SLOW_STEP; q0 += 16) {
-      double v[16];
+    constexpr int kRows = TBM / SLOW_STEP, kQ = kRows < 16 ? kRows : 16;  // rows per thread, in flight
+    for (int q0 = 0; q0 < kRows; q0 += kQ) {
+      double v[kQ];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < kQ; ++q) {
         const int sg = sbase + s0 + SLOW_STEP * (q0 + q);
         const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
         v[q] = (sg < slim && (!args.tri || i >= j)) ? Cf[(int64_t)sg * args.ldc] : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < kQ; ++q) {
         const int sl = s0 + SLOW_STEP * (q0 + q);
         const int sg = sbase + sl;
         const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
