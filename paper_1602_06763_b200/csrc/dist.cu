@@ -268,7 +268,7 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
         a.tri = op.kind == OP_SYRK;
         a.M = op.kind == OP_SYRK ? op.n : op.m;
         a.N = op.n;
-        u.tile = update_tile_for(a.M, a.N, a.tri);
+        u.tile = update_tile_for(a.M, a.N, a.K, a.tri);
         a.tiles_m = (a.M + u.tile - 1) / u.tile;
         a.ntiles = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * ((a.N + u.tile - 1) / u.tile);
         a.ksplit = 1;

@@ -94,6 +94,8 @@ static bool dag_enabled() { return env_int("RELAPACK_DAG", 1) != 0; }
 static int bulk_ctas() { return env_int("RELAPACK_BULK_CTAS", 132); }
 // CTA cap of the non-deferred updates (0 = uncapped)
 static int upd_ctas() { return env_int("RELAPACK_UPD_CTAS", 0); }
+// deferred (lookahead) updates at low graph-node priority (RELAPACK_DEFER_LOW=0: equal)
+static bool defer_low_priority() { return env_int("RELAPACK_DEFER_LOW", 1) != 0; }
 
 static bool splitk_enabled() { return env_int("RELAPACK_SPLITK", 1) != 0; }
 
@@ -187,7 +189,7 @@ static void fill_update(UpdateOp& u, const PlanOp& op, double* A, int64_t ld, in
     a.N = op.n;
     a.tri = 0;
   }
-  u.tile = update_tile_for(a.M, a.N, a.tri);
+  u.tile = update_tile_for(a.M, a.N, a.K, a.tri);
   a.tiles_m = (a.M + u.tile - 1) / u.tile;
   const int tiles_n = (a.N + u.tile - 1) / u.tile;
   a.ntiles = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * tiles_n;
@@ -494,7 +496,7 @@ static cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes
     if ((e = cudaGraphNodeGetType(nodes[i], &t)) != cudaSuccess) return e;
     if (t != cudaGraphNodeTypeKernel) continue;
     cudaKernelNodeAttrValue v{};
-    v.priority = deferred[i] ? least : greatest;
+    v.priority = (deferred[i] && defer_low_priority()) ? least : greatest;
     if ((e = cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v)) != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -520,7 +522,7 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const int upd_cap = upd_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
               pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24) |
-                  (trace_enabled() ? (1 << 30) : 0), bulk * 1024 + upd_cap,
+                  (trace_enabled() ? (1 << 30) : 0) | (defer_low_priority() ? 0 : (1 << 29)), bulk * 1024 + upd_cap,
               reinterpret_cast<uintptr_t>(host), hld};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);

@@ -47,7 +47,7 @@ struct UpdateOp {
 
 cudaError_t launch_update(const UpdateOp& op, cudaStream_t st);
 bool make_operand_map(CUtensorMap* map, const double* base, int64_t ld, int layout, int rows, int K, int box_rows);
-int update_tile_for(int M, int N, int tri);
+int update_tile_for(int M, int N, int K, int tri);
 // Split-K factor for an update of (M, N, K) on `tile` x `tile` CTA tiles (1 = none)
 // and the workspace it needs (doubles) — see update.cu.
 int update_ksplit_for(int M, int N, int K, int tri, int tile);

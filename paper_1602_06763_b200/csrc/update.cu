@@ -377,6 +377,17 @@ cudaError_t configure_tbm() {
 
 }  // namespace
 
+// RELAPACK_SPLIT128=1: small-grid long-K updates split K over 128-tiles
+// instead of dropping to 64-tiles (measured slower: n = 4096 2.43 vs 2.30 ms,
+// n = 16384 49.1 vs 48.2 ms, tools/exp22.sh) — off by default
+static bool split128_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("RELAPACK_SPLIT128");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 // 64-tile count below which 32-tiles are used (RELAPACK_TILE32_BELOW, 0 = never)
 static long small_tile_threshold() {
   static const long t = [] {
@@ -391,12 +402,17 @@ static long small_tile_threshold() {
 // and 32 x 32 one-warp tiles when even the 64-tiles would leave most SMs
 // idle (the n <= 512 updates on the base-case chain: a 64 x 64 x 128 tile is
 // ~4 us of DMMA on one SM).
-int update_tile_for(int M, int N, int tri) {
+int update_tile_for(int M, int N, int K, int tri) {
   auto tiles = [&](int t) -> long {
     const long tm = (M + t - 1) / t, tn = (N + t - 1) / t;
     return tri ? tm * (tm + 1) / 2 : tm * tn;
   };
   if (tiles(128) >= 148) return 128;
+  // fewer than 148 big tiles but a long K: keep the 128-tiles (8 warps, ~95 %
+  // of an SM's DMMA rate) and fill the GPU with split-K rather than dropping
+  // to 64-tiles, whose 4 warps of 32 x 32 reach about half of it
+  const int KT = (K + BK - 1) / BK;
+  if (split128_enabled() && tiles(128) * (KT / 16) >= 148) return 128;
   if (tiles(64) >= small_tile_threshold()) return 64;
   return 32;
 }

@@ -23,7 +23,7 @@ static UpdateOp make(double* A, int64_t ld, int M, int N, int K, int tri, const 
   a.M = M;
   a.N = N;
   a.tri = tri;
-  u.tile = update_tile_for(M, N, tri);
+  u.tile = update_tile_for(M, N, K, tri);
   a.tiles_m = (M + u.tile - 1) / u.tile;
   const int tn = (N + u.tile - 1) / u.tile;
   a.ntiles = tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * tn;
