@@ -84,11 +84,10 @@ __device__ __forceinline__ void stage_L(double* sL, double* rinv, const double* 
 
 // t <= 128: stage L(0:64, 0:64), L(64:128, 64:128) (diagonal blocks) and
 // L(64:128, 0:64) in one pass of asynchronous 8-byte copies (cp.async: no
-// registers held, every copy of a thread in flight), then one fix-up pass
-// moves the diagonal into 1/L_jj and zeroes it.  Ends with a barrier.
+// registers held, every copy of a thread in flight); finish_L_all completes it.
 template <int NW>
-__device__ __forceinline__ void stage_L_all(double* sL, double* rinv, const double* __restrict__ L, int64_t ldl,
-                                            int layout, int t) {
+__device__ __forceinline__ void stage_L_all(double* sL, const double* __restrict__ L, int64_t ldl, int layout,
+                                            int t) {
   constexpr int kFThreads = TF<NW>::THREADS;
   constexpr int kPer = kFC * kFC / kFThreads;
 #pragma unroll
@@ -109,6 +108,12 @@ __device__ __forceinline__ void stage_L_all(double* sL, double* rinv, const doub
         *dst = 0.0;
     }
   }
+}
+
+// After stage_L_all: wait for the copies, then move the diagonal of the two
+// diagonal blocks into 1/L_jj and zero it.
+template <int NW>
+__device__ __forceinline__ void finish_L_all(double* sL, double* rinv, int t) {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   if (threadIdx.x < 2 * kFC) {
@@ -139,7 +144,9 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
   const int g = lane >> 2, tq = lane & 3;
   const int wrow = warp * 8;             // this warp's first slab row
 
-  // ---- stage the slab (coalesced along the contiguous index; 16 loads in flight)
+  // ---- stage L (t <= 128: every block at once by cp.async, in flight while
+  // the slab is loaded through registers, 16 loads in flight per thread)
+  if (pre) stage_L_all<NW>(sL, L, ldl, layout, t);
   {
     const int total = kFRows * t;
     for (int e0 = tid; e0 < total; e0 += kFThreads * 16) {
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
       }
     }
   }
-  if (pre) stage_L_all<NW>(sL, sRinv, L, ldl, layout, t);
+  if (pre) finish_L_all<NW>(sL, sRinv, t);
   __syncthreads();
   TPROBE(1);
 

@@ -57,7 +57,7 @@ int main() {
   cudaStreamCreate(&st);
   struct Shape { int M, N, K, tri; } shapes[] = {{128, 128, 128, 1}, {128, 128, 256, 1}, {256, 256, 512, 1},
                                                 {512, 512, 1024, 1}, {1024, 1024, 2048, 1}, {128, 128, 128, 0},
-                                                {2048, 128, 128, 0}, {512, 512, 512, 0}};
+                                                {2048, 128, 128, 0}, {512, 512, 512, 0}, {1024, 1024, 2048, 0}, {2048, 1024, 1024, 0}};
   for (auto sh : shapes) {
     for (int ksf : {0, 1, 2, 4, 8}) {
       UpdateOp u = make(A, n, sh.M, sh.N, sh.K, sh.tri, info, ws, cnt, ksf);
