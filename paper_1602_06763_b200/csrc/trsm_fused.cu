@@ -90,22 +90,46 @@ __device__ __forceinline__ void stage_L_all(double* sL, const double* __restrict
                                             int t) {
   constexpr int kFThreads = TF<NW>::THREADS;
   constexpr int kPer = kFC * kFC / kFThreads;
+  auto cp8 = [](double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  };
+  // layout T: the L-view column index is contiguous in memory and in the
+  // block's shared-memory rows, so whole pairs go as one 16-byte copy (half
+  // the copy instructions, which bound this prologue)
+  const bool pairs = layout == kLayoutT && (ldl & 1) == 0 && (reinterpret_cast<uintptr_t>(L) & 15) == 0;
 #pragma unroll
   for (int bk = 0; bk < 3; ++bk) {
     const int r0 = bk == 0 ? 0 : kFC, c0 = bk == 1 ? kFC : 0;
+    if (pairs) {
 #pragma unroll 4
-    for (int u = 0; u < kPer; ++u) {
-      const int e = threadIdx.x + u * kFThreads;
-      const int a = e & (kFC - 1), b = e >> 6;
-      const int j = layout == kLayoutN ? a : b, k = layout == kLayoutN ? b : a;
-      const int gi = r0 + j, gk = c0 + k;
-      double* dst = sL + bk * kFC * kFLdL + j * kFLdL + k;
-      if (gi < t && gk < t && (bk == 2 || gi >= gk))
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)),
-                     "l"(L + lv_off(layout, gi, gk, ldl))
-                     : "memory");
-      else
-        *dst = 0.0;
+      for (int u = 0; u < kPer / 2; ++u) {
+        const int e = threadIdx.x + u * kFThreads;
+        const int k = 2 * (e & (kFC / 2 - 1)), j = e >> 5;
+        const int gi = r0 + j, gk = c0 + k;
+        double* dst = sL + bk * kFC * kFLdL + j * kFLdL + k;
+        const bool ok0 = gi < t && gk < t && (bk == 2 || gi >= gk);
+        const bool ok1 = gi < t && gk + 1 < t && (bk == 2 || gi >= gk + 1);
+        const double* src = L + lv_off(kLayoutT, gi, gk, ldl);
+        if (ok0 && ok1) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+        } else {
+          if (ok0) cp8(dst, src); else dst[0] = 0.0;
+          if (ok1) cp8(dst + 1, src + 1); else dst[1] = 0.0;
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int u = 0; u < kPer; ++u) {
+        const int e = threadIdx.x + u * kFThreads;
+        const int a = e & (kFC - 1), b = e >> 6;
+        const int j = layout == kLayoutN ? a : b, k = layout == kLayoutN ? b : a;
+        const int gi = r0 + j, gk = c0 + k;
+        double* dst = sL + bk * kFC * kFLdL + j * kFLdL + k;
+        if (gi < t && gk < t && (bk == 2 || gi >= gk))
+          cp8(dst, L + lv_off(layout, gi, gk, ldl));
+        else
+          *dst = 0.0;
+      }
     }
   }
 }
