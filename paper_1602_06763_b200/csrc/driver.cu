@@ -116,6 +116,12 @@ struct Plan {
   std::vector<PlanOp> ops;
   const double* host = nullptr;  // host-matrix path: the caller's pinned matrix (OP_H2D / OP_D2H ops)
   int64_t hld = 0;
+  // split copies: the graph holds an external event wait (H2D) / record (D2H)
+  // node per copy block; the copies themselves run on two library streams, one
+  // per link direction (memcpy nodes inside one graph were serialised: 38 ms
+  // for n = 16384 against 21.6 ms for both directions on two streams)
+  bool split_copies = false;
+  std::vector<cudaEvent_t> ev;  // per op (copy ops only)
   std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
   cudaGraphExec_t exec = nullptr;
   TraceRec* d_trace = nullptr;  // RELAPACK_TRACE=1: per-op kernel start/end (globaltimer)
@@ -125,6 +131,8 @@ struct Plan {
   ~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (d_trace) cudaFree(d_trace);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
     if (splitk_ws) cudaFree(splitk_ws);
     if (splitk_cnt) cudaFree(splitk_cnt);
   }
@@ -141,6 +149,8 @@ struct DeviceState {
   int* h_info = nullptr;  // pinned
   double* stage = nullptr;  // staging buffer for host matrices
   size_t stage_elems = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // split-copy streams (one per link direction)
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
   std::list<std::pair<PlanKey, std::unique_ptr<Plan>>> lru;
   std::map<PlanKey, std::list<std::pair<PlanKey, std::unique_ptr<Plan>>>::iterator> index;
 };
@@ -161,6 +171,10 @@ static cudaError_t ensure_device(DeviceState* ds) {
   if ((e = cudaMalloc(&ds->d_info, sizeof(int))) != cudaSuccess) return e;
   if ((e = cudaHostAlloc(&ds->h_info, sizeof(int), cudaHostAllocDefault)) != cudaSuccess) return e;
   if ((e = configure_kernels()) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&ds->h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&ds->d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&ds->ev_start, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&ds->ev_done, cudaEventDisableTiming)) != cudaSuccess) return e;
   ds->configured = true;
   return cudaSuccess;
 }
@@ -324,6 +338,13 @@ static cudaError_t launch_copy2d(double* dst, int64_t dld, const double* src, in
   return cudaGetLastError();
 }
 
+// Host-matrix path: copies on two copy streams synchronised with the graph by
+// events (default) or as memcpy nodes inside the graph (RELAPACK_SPLIT_COPIES=0)
+static bool split_copies_enabled() {
+  static const bool on = env_int("RELAPACK_SPLIT_COPIES", 1) != 0;
+  return on;
+}
+
 // Host-matrix copies as cudaMemcpy2DAsync nodes (default) or SM kernels
 // (RELAPACK_COPY_KERNEL=1; measured slower: n = 16384 e2e 78.8 vs 65.4 ms,
 // tools/exp15.sh).
@@ -338,6 +359,25 @@ static bool copy_kernels() {
 static int debug_skip_mask() {
   static const int m = env_int("RELAPACK_DEBUG_SKIP", 0);
   return m;
+}
+
+// The copy of host-path op i (OP_H2D / OP_D2H): L-view block rows [c_i,
+// c_i+m) x cols [c_j, c_j+k) as one 2-D copy on stream st.
+static cudaError_t copy_block(const Plan& pl, size_t i, double* A, int64_t ld, int layout, cudaStream_t st) {
+  const PlanOp& op = pl.ops[i];
+  const size_t width = sizeof(double) * (layout == kLayoutN ? op.m : op.k);
+  const size_t height = layout == kLayoutN ? op.k : op.m;
+  double* dev = A + lv_off(layout, op.c_i, op.c_j, ld);
+  double* host = const_cast<double*>(pl.host) + lv_off(layout, op.c_i, op.c_j, pl.hld);
+  if (copy_kernels()) {
+    const int64_t w = (int64_t)(width / sizeof(double)), h = (int64_t)height;
+    return op.kind == OP_H2D ? launch_copy2d(dev, ld, host, pl.hld, w, h, st)
+                             : launch_copy2d(host, pl.hld, dev, ld, w, h, st);
+  }
+  return op.kind == OP_H2D ? cudaMemcpy2DAsync(dev, ld * sizeof(double), host, pl.hld * sizeof(double), width, height,
+                                               cudaMemcpyHostToDevice, st)
+                           : cudaMemcpy2DAsync(host, pl.hld * sizeof(double), dev, ld * sizeof(double), width, height,
+                                               cudaMemcpyDeviceToHost, st);
 }
 
 static cudaError_t launch_op_impl(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
@@ -361,23 +401,10 @@ static cudaError_t launch_op_impl(const Plan& pl, size_t i, double* A, int64_t l
   switch (op.kind) {
     case OP_H2D:
     case OP_D2H: {
-      // L-view block rows [c_i, c_i+m) x cols [c_j, c_j+k) as one 2-D copy
-      const size_t width = sizeof(double) * (layout == kLayoutN ? op.m : op.k);
-      const size_t height = layout == kLayoutN ? op.k : op.m;
-      double* dev = A + lv_off(layout, op.c_i, op.c_j, ld);
-      double* host = const_cast<double*>(pl.host) + lv_off(layout, op.c_i, op.c_j, pl.hld);
-      if (copy_kernels()) {
-        // SM-driven copy through the pinned mapping: H2D and D2H blocks run
-        // concurrently (both link directions) as ordinary DAG kernel nodes
-        const int64_t w = (int64_t)(width / sizeof(double)), h = (int64_t)height;
-        return op.kind == OP_H2D ? launch_copy2d(dev, ld, host, pl.hld, w, h, st)
-                                 : launch_copy2d(host, pl.hld, dev, ld, w, h, st);
-      }
-      return op.kind == OP_H2D
-                 ? cudaMemcpy2DAsync(dev, ld * sizeof(double), host, pl.hld * sizeof(double), width, height,
-                                     cudaMemcpyHostToDevice, st)
-                 : cudaMemcpy2DAsync(host, pl.hld * sizeof(double), dev, ld * sizeof(double), width, height,
-                                     cudaMemcpyDeviceToHost, st);
+      if (pl.split_copies)  // graph-side half of a split copy (the copy runs on a copy stream)
+        return op.kind == OP_H2D ? cudaStreamWaitEvent(st, pl.ev[i], cudaEventWaitExternal)
+                                 : cudaEventRecordWithFlags(pl.ev[i], st, cudaEventRecordExternal);
+      return copy_block(pl, i, A, ld, layout, st);
     }
     case OP_POTF2:
       return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
@@ -522,7 +549,8 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const int upd_cap = upd_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
               pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24) |
-                  (trace_enabled() ? (1 << 30) : 0) | (defer_low_priority() ? 0 : (1 << 29)), bulk * 1024 + upd_cap,
+                  (trace_enabled() ? (1 << 30) : 0) | (defer_low_priority() ? 0 : (1 << 29)) |
+                  (split_copies_enabled() ? (1 << 28) : 0), bulk * 1024 + upd_cap,
               reinterpret_cast<uintptr_t>(host), hld};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
@@ -543,6 +571,14 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
       p->ops.swap(all);
       p->host = host;
       p->hld = hld;
+      p->split_copies = use_graph && split_copies_enabled();
+      if (p->split_copies) {
+        p->ev.assign(p->ops.size(), nullptr);
+        for (size_t i = 0; i < p->ops.size(); ++i)
+          if (p->ops[i].kind == OP_H2D || p->ops[i].kind == OP_D2H)
+            if ((e = cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming)) != cudaSuccess)
+              return cuda_fail(e, "copy event");
+      }
     }
     p->upd.resize(p->ops.size());
     if (trace_enabled() && (e = cudaMalloc(&p->d_trace, p->ops.size() * sizeof(TraceRec))) != cudaSuccess)
@@ -591,10 +627,31 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
       ds->lru.pop_back();
     }
   }
-  if (use_graph)
+  if (use_graph && plan->split_copies) {
+    // H2D blocks on one copy stream (each followed by its event), the graph
+    // (waiting on those events per block), the D2H blocks on the other copy
+    // stream (each after the graph's record of its event); `st` ends after all
+    const Plan& pl = *plan;
+    e = cudaEventRecord(ds->ev_start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->h2d, ds->ev_start, 0);
+    for (size_t i = 0; i < pl.ops.size() && e == cudaSuccess; ++i)
+      if (pl.ops[i].kind == OP_H2D) {
+        e = copy_block(pl, i, A, ld, layout, ds->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(pl.ev[i], ds->h2d);
+      }
+    if (e == cudaSuccess) e = cudaGraphLaunch(pl.exec, st);
+    for (size_t i = 0; i < pl.ops.size() && e == cudaSuccess; ++i)
+      if (pl.ops[i].kind == OP_D2H) {
+        e = cudaStreamWaitEvent(ds->d2h, pl.ev[i], 0);
+        if (e == cudaSuccess) e = copy_block(pl, i, A, ld, layout, ds->d2h);
+      }
+    if (e == cudaSuccess) e = cudaEventRecord(ds->ev_done, ds->d2h);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ds->ev_done, 0);
+  } else if (use_graph) {
     e = cudaGraphLaunch(plan->exec, st);
-  else
+  } else {
     e = run_ops(*plan, A, ld, layout, d_info, st, profile);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "launch");
   if (plan->d_trace) {
     std::lock_guard<std::mutex> tl(g_trace_mu);
@@ -848,6 +905,10 @@ void relapack_finalize(void) {
       if (ds->d_info) cudaFree(ds->d_info);
       if (ds->h_info) cudaFreeHost(ds->h_info);
       if (ds->capture) cudaStreamDestroy(ds->capture);
+      if (ds->h2d) cudaStreamDestroy(ds->h2d);
+      if (ds->d2h) cudaStreamDestroy(ds->d2h);
+      if (ds->ev_start) cudaEventDestroy(ds->ev_start);
+      if (ds->ev_done) cudaEventDestroy(ds->ev_done);
     }
     delete ds;
     g_dev[d] = nullptr;
