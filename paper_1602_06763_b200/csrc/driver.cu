@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -122,6 +123,9 @@ struct Plan {
   // for n = 16384 against 21.6 ms for both directions on two streams)
   bool split_copies = false;
   std::vector<cudaEvent_t> ev;  // per op (copy ops only)
+  // copy ops in issue order: H2D by first use, D2H by last write (no block
+  // waits behind one that is needed later / ready later on its stream)
+  std::vector<int> h2d_order, d2h_order;
   std::vector<UpdateOp> upd;  // parallel to ops (only GEMM/SYRK entries used)
   cudaGraphExec_t exec = nullptr;
   TraceRec* d_trace = nullptr;  // RELAPACK_TRACE=1: per-op kernel start/end (globaltimer)
@@ -573,6 +577,33 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
       p->hld = hld;
       p->split_copies = use_graph && split_copies_enabled();
       if (p->split_copies) {
+        // first use / last write of every copy block (footprint overlap)
+        std::vector<Rect> W(p->ops.size()), R1(p->ops.size()), R2(p->ops.size());
+        for (size_t i = 0; i < p->ops.size(); ++i) op_regions(p->ops[i], &W[i], &R1[i], &R2[i]);
+        auto hit = [](const Rect& a, const Rect& b) {
+          return a.buf >= 0 && a.buf == b.buf && a.r0 < b.r1 && b.r0 < a.r1 && a.c0 < b.c1 && b.c0 < a.c1;
+        };
+        std::vector<std::pair<size_t, int>> hk, dk;
+        for (size_t i = 0; i < p->ops.size(); ++i) {
+          const OpKind kd = p->ops[i].kind;
+          if (kd != OP_H2D && kd != OP_D2H) continue;
+          const Rect blk = kd == OP_H2D ? W[i] : R1[i];
+          size_t key = kd == OP_H2D ? p->ops.size() : 0;
+          for (size_t j = 0; j < p->ops.size(); ++j) {
+            const OpKind kj = p->ops[j].kind;
+            if (kj == OP_H2D || kj == OP_D2H) continue;
+            if (kd == OP_H2D && (hit(blk, W[j]) || hit(blk, R1[j]) || hit(blk, R2[j]))) {
+              key = j;
+              break;
+            }
+            if (kd == OP_D2H && hit(blk, W[j])) key = j;
+          }
+          (kd == OP_H2D ? hk : dk).push_back({key, (int)i});
+        }
+        std::stable_sort(hk.begin(), hk.end());
+        std::stable_sort(dk.begin(), dk.end());
+        for (auto& q : hk) p->h2d_order.push_back(q.second);
+        for (auto& q : dk) p->d2h_order.push_back(q.second);
         p->ev.assign(p->ops.size(), nullptr);
         for (size_t i = 0; i < p->ops.size(); ++i)
           if (p->ops[i].kind == OP_H2D || p->ops[i].kind == OP_D2H)
@@ -634,17 +665,17 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
     const Plan& pl = *plan;
     e = cudaEventRecord(ds->ev_start, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->h2d, ds->ev_start, 0);
-    for (size_t i = 0; i < pl.ops.size() && e == cudaSuccess; ++i)
-      if (pl.ops[i].kind == OP_H2D) {
-        e = copy_block(pl, i, A, ld, layout, ds->h2d);
-        if (e == cudaSuccess) e = cudaEventRecord(pl.ev[i], ds->h2d);
-      }
+    for (size_t q = 0; q < pl.h2d_order.size() && e == cudaSuccess; ++q) {
+      const int i = pl.h2d_order[q];
+      e = copy_block(pl, i, A, ld, layout, ds->h2d);
+      if (e == cudaSuccess) e = cudaEventRecord(pl.ev[i], ds->h2d);
+    }
     if (e == cudaSuccess) e = cudaGraphLaunch(pl.exec, st);
-    for (size_t i = 0; i < pl.ops.size() && e == cudaSuccess; ++i)
-      if (pl.ops[i].kind == OP_D2H) {
-        e = cudaStreamWaitEvent(ds->d2h, pl.ev[i], 0);
-        if (e == cudaSuccess) e = copy_block(pl, i, A, ld, layout, ds->d2h);
-      }
+    for (size_t q = 0; q < pl.d2h_order.size() && e == cudaSuccess; ++q) {
+      const int i = pl.d2h_order[q];
+      e = cudaStreamWaitEvent(ds->d2h, pl.ev[i], 0);
+      if (e == cudaSuccess) e = copy_block(pl, i, A, ld, layout, ds->d2h);
+    }
     if (e == cudaSuccess) e = cudaEventRecord(ds->ev_done, ds->d2h);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ds->ev_done, 0);
   } else if (use_graph) {
