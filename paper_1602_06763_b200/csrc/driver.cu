@@ -84,6 +84,8 @@ PlanParams current_params() {
   p.lookahead = env_int("RELAPACK_LOOKAHEAD", 1) != 0;
   p.trsm_rows = env_int("RELAPACK_TRSM_ROWS", 0);
   p.lookahead_depth = env_int("RELAPACK_LOOKAHEAD_DEPTH", 1);
+  p.defer_b21 = env_int("RELAPACK_DEFER_B21", 1) != 0;
+  p.b21_chunks = env_int("RELAPACK_B21_CHUNKS", 1);
   return p;
 }
 
@@ -552,7 +554,7 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const int bulk = bulk_ctas();
   const int upd_cap = upd_ctas();
   PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24) |
+              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24) | (pp.defer_b21 ? 0 : (1 << 27)) | (pp.b21_chunks << 20) |
                   (trace_enabled() ? (1 << 30) : 0) | (defer_low_priority() ? 0 : (1 << 29)) |
                   (split_copies_enabled() ? (1 << 28) : 0), bulk * 1024 + upd_cap,
               reinterpret_cast<uintptr_t>(host), hld};
@@ -1000,6 +1002,8 @@ int relapack_plan_schedule(int n, int c, int T, int lookahead, int64_t* out, int
   p.lookahead = lookahead != 0;
   p.trsm_rows = current_params().trsm_rows;
   p.lookahead_depth = current_params().lookahead_depth;
+  p.defer_b21 = current_params().defer_b21;
+  p.b21_chunks = current_params().b21_chunks;
   std::vector<PlanOp> ops;
   build_potrf_plan(n, p, ops);
   const int cnt = (int)ops.size();

@@ -101,16 +101,25 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
       const int n1c = split_point(nn, p.split_tile), n2c = nn - n1c;
       const int r1 = r0 + n1c;
       trailing(r0, n1c, depth - 1);
-      PlanOp g{};
-      g.kind = OP_GEMM;
-      g.level = level + 1;
-      g.c_i = r1; g.c_j = r0;   // rows of B2 x cols of B1
-      g.a_i = r1; g.a_j = off;  // A21 rows of B2
-      g.b_i = r0; g.b_j = off;  // A21 rows of B1
-      g.m = n2c; g.n = n1c; g.k = n1;
-      g.flops = 2.0 * n2c * n1c * n1;
-      g.deferred = 1;
-      ops.push_back(g);
+      // GEMM(B21) in column chunks (b21_chunks, each a multiple of the split
+      // tile): the TRSM of B21 starts on its first columns as soon as their
+      // chunk is done
+      const int nch = p.b21_chunks < 1 ? 1 : p.b21_chunks;
+      int cw = (n1c + nch - 1) / nch;
+      cw = (cw + p.split_tile - 1) / p.split_tile * p.split_tile;
+      for (int c0 = 0; c0 < n1c; c0 += cw) {
+        const int w = n1c - c0 < cw ? n1c - c0 : cw;
+        PlanOp g{};
+        g.kind = OP_GEMM;
+        g.level = level + 1;
+        g.c_i = r1; g.c_j = r0 + c0;   // rows of B2 x cols of B1
+        g.a_i = r1; g.a_j = off;       // A21 rows of B2
+        g.b_i = r0 + c0; g.b_j = off;  // A21 rows of B1
+        g.m = n2c; g.n = w; g.k = n1;
+        g.flops = 2.0 * n2c * w * n1;
+        g.deferred = p.defer_b21 ? 1 : 0;  // the TRSM of B21 needs it: on the critical path
+        ops.push_back(g);
+      }
       syrk(r1, n2c);
       ops.back().deferred = 1;
     };

@@ -64,6 +64,10 @@ struct PlanParams {
   // same way this many times (1 = one split), so the first leaf of potrf(A22)
   // waits only for the update of its own corner
   int lookahead_depth = 1;
+  // lookahead GEMM(B21) as a deferred (low-priority, CTA-capped) update too
+  bool defer_b21 = true;
+  // GEMM(B21) issued as this many column chunks
+  int b21_chunks = 1;
   // > 0: the TRSM of a node's A21 is issued as independent row panels of this
   // many rows (rows of B are independent), so the DAG can overlap the panels'
   // chains with each other and start the trailing updates of finished rows
