@@ -307,7 +307,7 @@ cudaError_t configure_trsm_fused() {
   return cudaFuncSetAttribute(k_trsm_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem<4>());
 }
 
-// 64-row CTAs (8 warps) for tall panels (m >= 4096), 32-row CTAs (4 warps, two
+// 64-row CTAs (8 warps) for tall panels (m >= 2048), 32-row CTAs (4 warps, two
 // CTAs per SM, twice the CTAs) for shorter ones — measured, profiles/
 // (RELAPACK_TRSM_NW=4|8 forces one).
 static int trsm_nw(int m) {
@@ -316,7 +316,11 @@ static int trsm_nw(int m) {
     return v ? atoi(v) : 0;
   }();
   if (forced == 4 || forced == 8) return forced;
-  return m >= 4096 ? 8 : 4;
+  static const int m8 = [] {  // RELAPACK_TRSM_NW8_FROM: panel height from which 64-row CTAs are used
+    const char* v = getenv("RELAPACK_TRSM_NW8_FROM");
+    return v ? atoi(v) : 2048;
+  }();
+  return m >= m8 ? 8 : 4;
 }
 
 cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
