@@ -22,6 +22,7 @@
 // each bank pair exactly twice.
 #include <cstdlib>
 
+#include "chol_regs.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -282,6 +283,134 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
   trace_end(tr);
 }
 
+// ---- t <= 128 with the row slab in REGISTERS: each warp owns RG groups of 8
+// rows and all t columns (16 accumulator tiles per group), so shared memory
+// holds only the three L blocks (104 KB) and a CTA covers 8 * RG * NW rows —
+// twice the rows per SM of the shared-memory slab at the same per-warp chain
+// (the RG groups' substitution chains interleave in one instruction stream).
+template <int NW, int RG>
+struct TRG {
+  static constexpr int ROWS = 8 * RG * NW, THREADS = 32 * NW;
+  static constexpr size_t SMEM = sizeof(double) * (3 * (size_t)kFC * kFLdL + 2 * kFC);
+};
+
+// Solve the 64 columns of chunk cb (tiles 8cb .. 8cb+7) against its diagonal
+// block sLd (1/L_jj in sRd), sub-block by sub-block, for every row group.
+template <int RG, int CB>
+__device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][16][2], const double* sLd, const double* sRd,
+                                                int lane, int g, int tq) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    double l0[8], l1[8], rc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      l0[c] = sLd[(8 * s + 2 * tq) * kFLdL + 8 * s + c];      // L(8s+2t,   8s+c), 0 unless 2t > c
+      l1[c] = sLd[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c];  // L(8s+2t+1, 8s+c)
+      rc[c] = sRd[8 * s + c];
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        double& x0 = xs[r][8 * CB + s][0];
+        double& x1 = xs[r][8 * CB + s][1];
+        const double xj = __shfl_sync(0xffffffffu, (c & 1) ? x1 : x0, (lane & ~3) | (c >> 1)) * rc[c];
+        x0 -= xj * l0[c];
+        x1 -= xj * l1[c];
+        if (tq == (c >> 1)) {
+          if (c & 1)
+            x1 = xj;
+          else
+            x0 = xj;
+        }
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        const double a = -tile_frag(xs[r][8 * CB + s][0], xs[r][8 * CB + s][1], ks, g, tq);  // -X_s[g][4ks + tq]
+#pragma unroll
+        for (int s2 = s + 1; s2 < 8; ++s2)
+          dmma_884(xs[r][8 * CB + s2][0], xs[r][8 * CB + s2][1], a, sLd[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
+      }
+    }
+  }
+}
+
+template <int NW, int RG>
+__global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
+    k_trsm_reg(const double* __restrict__ L, int64_t ldl, double* __restrict__ B, int64_t ldb, int layout, int m,
+               int t, const int* d_info, TraceRec* tr) {
+  if (ld_info(d_info) != 0) return;
+  trace_begin(tr);
+  extern __shared__ double smem_r[];
+  double* sL = smem_r;                    // the three 64x64 L blocks
+  double* sRinv = sL + 3 * kFC * kFLdL;   // 1 / L_jj of both diagonal blocks
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int row_base = blockIdx.x * TRG<NW, RG>::ROWS + warp * 8 * RG;
+  stage_L_all<NW>(sL, L, ldl, layout, t);  // async, overlaps the slab loads
+  double xs[RG][16][2];
+  const bool pairs = layout == kLayoutT && (ldb & 1) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int sb = 0; sb < 16; ++sb) {
+      const int row = row_base + 8 * r + g, col = 8 * sb + 2 * tq;
+      if (pairs && row < m && col + 1 < t) {
+        const double2 v = *reinterpret_cast<const double2*>(B + lv_off(kLayoutT, row, col, ldb));
+        xs[r][sb][0] = v.x;
+        xs[r][sb][1] = v.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          xs[r][sb][q] = (row < m && col + q < t) ? B[lv_off(layout, row, col + q, ldb)] : 0.0;
+      }
+    }
+  finish_L_all<NW>(sL, sRinv, t);
+  __syncthreads();
+  solve_chunk_reg<RG, 0>(xs, sL, sRinv, lane, g, tq);
+  if (t > kFC) {
+    // X_1 -= X_0 L_{1,0}^T (A fragments of X_0 from the quads, B from block 2)
+    const double* sLb = sL + 2 * kFC * kFLdL;
+#pragma unroll
+    for (int k0 = 0; k0 < kFC; k0 += 4) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        const double a = -tile_frag(xs[r][k0 >> 3][0], xs[r][k0 >> 3][1], (k0 >> 2) & 1, g, tq);
+#pragma unroll
+        for (int sb = 0; sb < 8; ++sb)
+          dmma_884(xs[r][8 + sb][0], xs[r][8 + sb][1], a, sLb[(8 * sb + g) * kFLdL + k0 + tq]);
+      }
+    }
+    solve_chunk_reg<RG, 1>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
+  }
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int sb = 0; sb < 16; ++sb) {
+      const int row = row_base + 8 * r + g, col = 8 * sb + 2 * tq;
+      if (pairs && row < m && col + 1 < t) {
+        *reinterpret_cast<double2*>(B + lv_off(kLayoutT, row, col, ldb)) = make_double2(xs[r][sb][0], xs[r][sb][1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (row < m && col + q < t) B[lv_off(layout, row, col + q, ldb)] = xs[r][sb][q];
+      }
+    }
+  trace_end(tr);
+}
+
+template <int NW, int RG>
+cudaError_t launch_reg(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
+                       const int* d_info, cudaStream_t st) {
+  const int grid = (m + TRG<NW, RG>::ROWS - 1) / TRG<NW, RG>::ROWS;
+  k_trsm_reg<NW, RG><<<grid, TRG<NW, RG>::THREADS, TRG<NW, RG>::SMEM, st>>>(L, ldl, B, ldb, layout, m, t, d_info,
+                                                                           g_launch_trace);
+  return cudaGetLastError();
+}
+
 template <int NW>
 cudaError_t launch_nw(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                       const int* d_info, cudaStream_t st) {
@@ -304,7 +433,13 @@ cudaError_t configure_trsm_fused() {
   cudaError_t e =
       cudaFuncSetAttribute(k_trsm_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem<8>());
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_trsm_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem<4>());
+  if ((e = cudaFuncSetAttribute(k_trsm_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem<4>())) !=
+      cudaSuccess)
+    return e;
+  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 2>, attr, (int)TRG<8, 2>::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 1>, attr, (int)TRG<8, 1>::SMEM)) != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_trsm_reg<4, 1>, attr, (int)TRG<4, 1>::SMEM);
 }
 
 // 64-row CTAs (8 warps) for tall panels (m >= 2048), 32-row CTAs (4 warps, two
@@ -323,10 +458,43 @@ static int trsm_nw(int m) {
   return m >= m8 ? 8 : 4;
 }
 
+// RELAPACK_TRSM_REG: 0 = shared-memory slab kernel only, 1 = register-slab
+// kernel for t <= 128 (default), 2 = always 128-row register CTAs;
+// RELAPACK_TRSM_RG2_FROM = panel height from which the 128-row CTAs are used,
+// RELAPACK_TRSM_REG8_FROM = from which the 64-row (8-warp) CTAs are used
+static int trsm_reg_mode() {
+  static const int v = [] {
+    const char* e = getenv("RELAPACK_TRSM_REG");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+static int trsm_rg2_from() {
+  static const int v = [] {
+    const char* e = getenv("RELAPACK_TRSM_RG2_FROM");
+    return e ? atoi(e) : (1 << 30);  // the 2-group variant spills: off unless asked for
+  }();
+  return v;
+}
+static int trsm_reg8_from() {
+  static const int v = [] {
+    const char* e = getenv("RELAPACK_TRSM_REG8_FROM");
+    return e ? atoi(e) : 2048;
+  }();
+  return v;
+}
+
 cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                               const int* d_info, cudaStream_t st) {
   if (m <= 0 || t <= 0) return cudaSuccess;
   if (t > kFTmax) return cudaErrorInvalidValue;
+  if (t <= 2 * kFC && trsm_reg_mode() > 0) {
+    // register-slab kernel: 128-row CTAs for tall panels, 64 / 32 rows below
+    const int mode = trsm_reg_mode();
+    if (mode == 2 || (mode == 1 && m >= trsm_rg2_from())) return launch_reg<8, 2>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    if (m >= trsm_reg8_from()) return launch_reg<8, 1>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    return launch_reg<4, 1>(L, ldl, B, ldb, layout, m, t, d_info, st);
+  }
   return trsm_nw(m) == 8 ? launch_nw<8>(L, ldl, B, ldb, layout, m, t, d_info, st)
                         : launch_nw<4>(L, ldl, B, ldb, layout, m, t, d_info, st);
 }
