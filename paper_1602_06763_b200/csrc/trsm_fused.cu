@@ -296,8 +296,8 @@ struct TRG {
 
 // Solve the 64 columns of chunk cb (tiles 8cb .. 8cb+7) against its diagonal
 // block sLd (1/L_jj in sRd), sub-block by sub-block, for every row group.
-template <int RG, int CB>
-__device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][16][2], const double* sLd, const double* sRd,
+template <int RG, int CB, int NT>
+__device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][NT][2], const double* sLd, const double* sRd,
                                                 int lane, int g, int tq) {
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
@@ -338,7 +338,7 @@ __device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][16][2], const d
   }
 }
 
-template <int NW, int RG>
+template <int NW, int RG, int NC>
 __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
     k_trsm_reg(const double* __restrict__ L, int64_t ldl, double* __restrict__ B, int64_t ldb, int layout, int m,
                int t, const int* d_info, TraceRec* tr) {
@@ -351,12 +351,13 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
   const int g = lane >> 2, tq = lane & 3;
   const int row_base = blockIdx.x * TRG<NW, RG>::ROWS + warp * 8 * RG;
   stage_L_all<NW>(sL, L, ldl, layout, t);  // async, overlaps the slab loads
-  double xs[RG][16][2];
+  constexpr int NT = 8 * NC;  // 8-column tiles held (t <= 64 NC)
+  double xs[RG][NT][2];
   const bool pairs = layout == kLayoutT && (ldb & 1) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
 #pragma unroll
   for (int r = 0; r < RG; ++r)
 #pragma unroll
-    for (int sb = 0; sb < 16; ++sb) {
+    for (int sb = 0; sb < NT; ++sb) {
       const int row = row_base + 8 * r + g, col = 8 * sb + 2 * tq;
       if (pairs && row < m && col + 1 < t) {
         const double2 v = *reinterpret_cast<const double2*>(B + lv_off(kLayoutT, row, col, ldb));
@@ -370,8 +371,8 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
     }
   finish_L_all<NW>(sL, sRinv, t);
   __syncthreads();
-  solve_chunk_reg<RG, 0>(xs, sL, sRinv, lane, g, tq);
-  if (t > kFC) {
+  solve_chunk_reg<RG, 0, NT>(xs, sL, sRinv, lane, g, tq);
+  if (NC == 2 && t > kFC) {  // (NC == 1 instances never get here: t <= 64)
     // X_1 -= X_0 L_{1,0}^T (A fragments of X_0 from the quads, B from block 2)
     const double* sLb = sL + 2 * kFC * kFLdL;
 #pragma unroll
@@ -381,15 +382,15 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
         const double a = -tile_frag(xs[r][k0 >> 3][0], xs[r][k0 >> 3][1], (k0 >> 2) & 1, g, tq);
 #pragma unroll
         for (int sb = 0; sb < 8; ++sb)
-          dmma_884(xs[r][8 + sb][0], xs[r][8 + sb][1], a, sLb[(8 * sb + g) * kFLdL + k0 + tq]);
+          dmma_884(xs[r][(8 + sb) % NT][0], xs[r][(8 + sb) % NT][1], a, sLb[(8 * sb + g) * kFLdL + k0 + tq]);
       }
     }
-    solve_chunk_reg<RG, 1>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
+    if constexpr (NC == 2) solve_chunk_reg<RG, 1, NT>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
   }
 #pragma unroll
   for (int r = 0; r < RG; ++r)
 #pragma unroll
-    for (int sb = 0; sb < 16; ++sb) {
+    for (int sb = 0; sb < NT; ++sb) {
       const int row = row_base + 8 * r + g, col = 8 * sb + 2 * tq;
       if (pairs && row < m && col + 1 < t) {
         *reinterpret_cast<double2*>(B + lv_off(kLayoutT, row, col, ldb)) = make_double2(xs[r][sb][0], xs[r][sb][1]);
@@ -406,8 +407,12 @@ template <int NW, int RG>
 cudaError_t launch_reg(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                        const int* d_info, cudaStream_t st) {
   const int grid = (m + TRG<NW, RG>::ROWS - 1) / TRG<NW, RG>::ROWS;
-  k_trsm_reg<NW, RG><<<grid, TRG<NW, RG>::THREADS, TRG<NW, RG>::SMEM, st>>>(L, ldl, B, ldb, layout, m, t, d_info,
-                                                                           g_launch_trace);
+  if (t <= kFC)
+    k_trsm_reg<NW, RG, 1><<<grid, TRG<NW, RG>::THREADS, TRG<NW, RG>::SMEM, st>>>(L, ldl, B, ldb, layout, m, t, d_info,
+                                                                                g_launch_trace);
+  else
+    k_trsm_reg<NW, RG, 2><<<grid, TRG<NW, RG>::THREADS, TRG<NW, RG>::SMEM, st>>>(L, ldl, B, ldb, layout, m, t, d_info,
+                                                                                g_launch_trace);
   return cudaGetLastError();
 }
 
@@ -437,9 +442,12 @@ cudaError_t configure_trsm_fused() {
       cudaSuccess)
     return e;
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 2>, attr, (int)TRG<8, 2>::SMEM)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 1>, attr, (int)TRG<8, 1>::SMEM)) != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_trsm_reg<4, 1>, attr, (int)TRG<4, 1>::SMEM);
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 2, 2>, attr, (int)TRG<8, 2>::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 1, 2>, attr, (int)TRG<8, 1>::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<4, 1, 2>, attr, (int)TRG<4, 1>::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 2, 1>, attr, (int)TRG<8, 2>::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_trsm_reg<8, 1, 1>, attr, (int)TRG<8, 1>::SMEM)) != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_trsm_reg<4, 1, 1>, attr, (int)TRG<4, 1>::SMEM);
 }
 
 // 64-row CTAs (8 warps) for tall panels (m >= 2048), 32-row CTAs (4 warps, two
