@@ -118,6 +118,23 @@ __device__ __forceinline__ void stage_L_all(double* sL, const double* __restrict
           if (ok1) cp8(dst + 1, src + 1); else dst[1] = 0.0;
         }
       }
+    } else if (layout == kLayoutN) {
+      // transposing copy: a warp moves an 8 (rows j, contiguous in global)
+      // x 4 (columns k) patch, so its eight 64-byte global segments are whole
+      // and its shared-memory stores (row stride kFLdL = 4 mod 16 doubles) hit
+      // every bank pair exactly twice (a 32-row column would be 8-way)
+      const int lane = threadIdx.x & 31;
+#pragma unroll 4
+      for (int u = 0; u < kPer; ++u) {
+        const int blk = (threadIdx.x >> 5) + u * (kFThreads / 32);  // 0 .. 127: 8 row patches x 16 column patches
+        const int j = 8 * (blk & 7) + (lane & 7), k = 4 * (blk >> 3) + (lane >> 3);
+        const int gi = r0 + j, gk = c0 + k;
+        double* dst = sL + bk * kFC * kFLdL + j * kFLdL + k;
+        if (gi < t && gk < t && (bk == 2 || gi >= gk))
+          cp8(dst, L + lv_off(kLayoutN, gi, gk, ldl));
+        else
+          *dst = 0.0;
+      }
     } else {
 #pragma unroll 4
       for (int u = 0; u < kPer; ++u) {
@@ -288,6 +305,10 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
 // holds only the three L blocks (104 KB) and a CTA covers 8 * RG * NW rows —
 // twice the rows per SM of the shared-memory slab at the same per-warp chain
 // (the RG groups' substitution chains interleave in one instruction stream).
+#ifndef RELAPACK_TRSM_SPLITACC
+#define RELAPACK_TRSM_SPLITACC 1
+#endif
+
 template <int NW, int RG>
 struct TRG {
   static constexpr int ROWS = 8 * RG * NW, THREADS = 32 * NW;
@@ -325,6 +346,30 @@ __device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][NT][2], const d
         }
       }
     }
+#if RELAPACK_TRSM_SPLITACC
+    // the next sub-block's tile first, its two k-halves into separate
+    // accumulators (two independent DMMAs instead of a dependent pair: the
+    // next substitution waits ~one DMMA latency less)
+    if (s + 1 < 8) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        double a[2];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) a[ks] = -tile_frag(xs[r][8 * CB + s][0], xs[r][8 * CB + s][1], ks, g, tq);
+        double h0 = 0.0, h1 = 0.0;
+        dmma_884(xs[r][8 * CB + s + 1][0], xs[r][8 * CB + s + 1][1], a[0], sLd[(8 * (s + 1) + g) * kFLdL + 8 * s + tq]);
+        dmma_884(h0, h1, a[1], sLd[(8 * (s + 1) + g) * kFLdL + 8 * s + 4 + tq]);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int s2 = s + 2; s2 < 8; ++s2)
+            dmma_884(xs[r][8 * CB + s2][0], xs[r][8 * CB + s2][1], a[ks],
+                     sLd[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
+        xs[r][8 * CB + s + 1][0] += h0;
+        xs[r][8 * CB + s + 1][1] += h1;
+      }
+    }
+#else
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
 #pragma unroll
@@ -335,6 +380,7 @@ __device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][NT][2], const d
           dmma_884(xs[r][8 * CB + s2][0], xs[r][8 * CB + s2][1], a, sLd[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
       }
     }
+#endif
   }
 }
 
@@ -344,6 +390,7 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
                int t, const int* d_info, TraceRec* tr) {
   if (ld_info(d_info) != 0) return;
   trace_begin(tr);
+  TPROBE(0);
   extern __shared__ double smem_r[];
   double* sL = smem_r;                    // the three 64x64 L blocks
   double* sRinv = sL + 3 * kFC * kFLdL;   // 1 / L_jj of both diagonal blocks
@@ -371,7 +418,9 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
     }
   finish_L_all<NW>(sL, sRinv, t);
   __syncthreads();
+  TPROBE(1);
   solve_chunk_reg<RG, 0, NT>(xs, sL, sRinv, lane, g, tq);
+  TPROBE(2);
   if (NC == 2 && t > kFC) {  // (NC == 1 instances never get here: t <= 64)
     // X_1 -= X_0 L_{1,0}^T (A fragments of X_0 from the quads, B from block 2)
     const double* sLb = sL + 2 * kFC * kFLdL;
@@ -385,7 +434,9 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
           dmma_884(xs[r][(8 + sb) % NT][0], xs[r][(8 + sb) % NT][1], a, sLb[(8 * sb + g) * kFLdL + k0 + tq]);
       }
     }
+    TPROBE(3);
     if constexpr (NC == 2) solve_chunk_reg<RG, 1, NT>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
+    TPROBE(4);
   }
 #pragma unroll
   for (int r = 0; r < RG; ++r)
@@ -400,6 +451,7 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
           if (row < m && col + q < t) B[lv_off(layout, row, col + q, ldb)] = xs[r][sb][q];
       }
     }
+  TPROBE(5);
   trace_end(tr);
 }
 

@@ -65,13 +65,18 @@ int main() {
     char nm[64]; snprintf(nm, 64, "trsm_fused m=%d t=%d layout N", m, t);
     time(nm, [&] { launch_trsm_fused(d, n, d + 256, n, kLayoutN, m, t, info, 0); });
   }
+  for (int lay : {kLayoutN, kLayoutT})
   for (int m : {128, 8192}) {
-    launch_trsm_fused(d, n, d + 256, n, kLayoutN, m, 128, info, 0);
+    launch_trsm_fused(d, n, d + 256 * (lay == kLayoutN ? 1 : n), n, lay, m, 128, info, 0);
     cudaDeviceSynchronize();
     long long pr[64];
     cudaMemcpyFromSymbol(pr, g_tprobe, sizeof(pr));
-    printf("trsm_fused m=%d t=128 phases (cycles): slab+L %lld | cb0 solve %lld | cb1 update %lld | cb1 solve %lld | store %lld\n",
-           m, pr[1] - pr[0], pr[3] - pr[2], pr[4] - pr[3], pr[5] - pr[4], pr[20] - pr[5]);
+    printf("trsm_reg layout %c m=%d t=128 phases (cycles, CTA 0 thread 0): slab+L %lld | cb0 solve %lld | cb1 update %lld | cb1 solve %lld | store %lld | total %lld\n",
+           lay == kLayoutN ? 'N' : 'T', m, pr[1] - pr[0], pr[2] - pr[1], pr[3] - pr[2], pr[4] - pr[3], pr[5] - pr[4], pr[5] - pr[0]);
+  }
+  for (int m : {2048, 8192}) {
+    char nm[64]; snprintf(nm, 64, "trsm_fused m=%d t=128 layout T", m);
+    time(nm, [&] { launch_trsm_fused(d, n, d + 256 * n, n, kLayoutT, m, 128, info, 0); });
   }
   time("trsm m=2048 t=64 layout T", [&] { launch_trsm_base(d, n, d + 64 * n, n, kLayoutT, 2048, 64, info, 0); });
   return 0;
