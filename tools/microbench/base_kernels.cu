@@ -57,6 +57,7 @@ int main() {
     printf(" end %lld\n", pr[63] - pr[0]);
   }
   time("potf2 n=64 layout T", [&] { launch_potf2(d, n, kLayoutT, 64, info, 0, 0); });
+  time("potf2 n=128 layout T", [&] { launch_potf2(d, n, kLayoutT, 128, info, 0, 0); });
   for (int m : {64, 512, 2048, 8192}) for (int t : {16, 64}) {
     char nm[64]; snprintf(nm, 64, "trsm m=%d t=%d layout N", m, t);
     time(nm, [&] { launch_trsm_base(d, n, d + 64, n, kLayoutN, m, t, info, 0); });
