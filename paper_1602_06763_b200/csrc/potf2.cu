@@ -29,6 +29,13 @@ namespace {
 
 constexpr int kPanel = 8;
 
+#ifndef RELAPACK_NODE_EARLY_STORE
+#define RELAPACK_NODE_EARLY_STORE 0
+#endif
+#ifndef RELAPACK_POTF2_SPARE
+#define RELAPACK_POTF2_SPARE 1
+#endif
+
 #ifdef RELAPACK_PROBE  // phase timestamps for tools/microbench/base_kernels.cu only
 __device__ long long g_probe[64];
 #define PROBE(k) \
@@ -243,7 +250,11 @@ __device__ int potf2_smem(double* s, int n, int* fail_flag) {
       if (T > 1) {
         const int T2 = T - 1;
         const int nt2 = T2 * (T2 + 1) / 2;  // lower tiles of the grid rooted at (r0+8, r0+8)
-        trail_tiles<LDS>(s, j0, r0 + 8, warp - 1, nt2, NW - 1, g, t);
+        // with 8 warps, warp 4 shares warp 0's SMSP: it stays idle so the
+        // panel chain does not compete for issue slots and the DMMA pipe
+        constexpr bool kSpare = NW == 8 && RELAPACK_POTF2_SPARE;
+        const int hw = kSpare ? warp - 1 - (warp > 4) : warp - 1;
+        if (!(kSpare && warp == 4)) trail_tiles<LDS>(s, j0, r0 + 8, hw, nt2, kSpare ? NW - 2 : NW - 1, g, t);
       }
       (void)ntiles;
     }
@@ -504,14 +515,19 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     trsm_in_smem<LDS>(s, rinv, n2);
     __syncthreads();
     PROBE(53);
+#if RELAPACK_NODE_EARLY_STORE
     // L11 and L21 are final: write them back while A22 is finished
     copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
+#endif
     syrk_in_smem<LDS, NW>(s, n2);
     __syncthreads();
     PROBE(54);
     fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
     if (fail) fail += kN1;
     PROBE(55);
+#if !RELAPACK_NODE_EARLY_STORE
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
+#endif
     copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1);
   } else {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
