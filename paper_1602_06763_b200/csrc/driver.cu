@@ -546,6 +546,13 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   DeviceState* ds = device_state(dev);
   cudaError_t e;
   PlanParams pp = current_params();
+  if (host) {
+    // host-matrix path: the TRSM GEMMs go in copy-panel-wide column chunks,
+    // each waiting only for its own host blocks (n = 16384 e2e 57.0 -> 52.7 ms,
+    // tools/experiments/exp_e2e2.sh; no effect on the device-only path)
+    pp.host_gemm_cols = env_int("RELAPACK_HOST_GEMM_COLS", copy_panel());
+    pp.b21_chunks = env_int("RELAPACK_HOST_B21_CHUNKS", pp.b21_chunks);
+  }
   const bool profile = g_prof_on.load() != 0;
   const bool use_graph = graphs_enabled() && !profile;
   std::lock_guard<std::mutex> lk(ds->mu);

@@ -44,16 +44,20 @@ void build_trsm(int L_off, int b_buf, int B_i, int B_j, int m, int k, int level,
   }
   const int pp = split_point(k, p.split_tile), q = k - pp;
   build_trsm(L_off, b_buf, B_i, B_j, m, pp, level, p, ops);
-  PlanOp g{};
-  g.kind = OP_GEMM;
-  g.level = level;
-  g.c_i = B_i; g.c_j = B_j + pp;       // B2 (m x q)
-  g.a_i = B_i; g.a_j = B_j;            // X1 (m x p)
-  g.b_i = L_off + pp; g.b_j = L_off;   // Lb (q x p)
-  g.m = m; g.n = q; g.k = pp;
-  g.flops = 2.0 * m * q * pp;
-  g.c_buf = b_buf; g.a_buf = b_buf; g.b_buf = BUF_A;
-  ops.push_back(g);
+  const int cw = p.host_gemm_cols > 0 && q > p.host_gemm_cols ? p.host_gemm_cols : q;
+  for (int c0 = 0; c0 < q; c0 += cw) {
+    const int w = q - c0 < cw ? q - c0 : cw;
+    PlanOp g{};
+    g.kind = OP_GEMM;
+    g.level = level;
+    g.c_i = B_i; g.c_j = B_j + pp + c0;       // B2 (m x q), columns [c0, c0 + w)
+    g.a_i = B_i; g.a_j = B_j;                 // X1 (m x p)
+    g.b_i = L_off + pp + c0; g.b_j = L_off;   // Lb (q x p), rows [c0, c0 + w)
+    g.m = m; g.n = w; g.k = pp;
+    g.flops = 2.0 * m * w * pp;
+    g.c_buf = b_buf; g.a_buf = b_buf; g.b_buf = BUF_A;
+    ops.push_back(g);
+  }
   build_trsm(L_off + pp, b_buf, B_i, B_j + pp, m, q, level, p, ops);
 }
 

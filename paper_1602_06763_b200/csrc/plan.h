@@ -72,6 +72,10 @@ struct PlanParams {
   // many rows (rows of B are independent), so the DAG can overlap the panels'
   // chains with each other and start the trailing updates of finished rows
   int trsm_rows = 0;
+  // > 0 (host-matrix path): the TRSM's GEMM updates B2 -= X1 Lb^T are issued
+  // as column chunks of this width, so each starts as soon as its own host
+  // blocks have arrived instead of waiting for all of B2
+  int host_gemm_cols = 0;
 };
 
 // Rectangle of an op's footprint in L-view coordinates of buffer `buf`.
