@@ -131,8 +131,17 @@ __device__ __forceinline__ void trace_end(TraceRec* tr) {
   }
 }
 
+// Every plan kernel starts here: wait for the grids it depends on
+// (programmatic dependent launch: a no-op unless the graph edge into this
+// node is programmatic, driver.cu capture_dag), then read the info word.
 __device__ __forceinline__ int ld_info(const int* d_info) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   return *reinterpret_cast<const volatile int*>(d_info);
 }
+
+// Let the dependent grids launch (they still wait for this grid's completion
+// in ld_info): issued when a CTA's main work is done, so their launch
+// latency overlaps this grid's stores.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 }  // namespace relapack

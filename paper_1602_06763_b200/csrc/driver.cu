@@ -101,6 +101,11 @@ static int upd_ctas() { return env_int("RELAPACK_UPD_CTAS", 0); }
 static bool defer_low_priority() { return env_int("RELAPACK_DEFER_LOW", 1) != 0; }
 
 static bool splitk_enabled() { return env_int("RELAPACK_SPLITK", 1) != 0; }
+// programmatic dependent launch on the plan DAG's kernel-to-kernel edges
+// (1: every edge between plan kernels, 2: edges into base cases and TRSMs,
+// 3 (default): 2 + edges into the non-deferred SYRKs of the chain; 0: off;
+// n = 4096 2.186 -> 2.130 ms, n = 16384 47.26 -> 47.01 ms, exp_pdl.sh)
+static int pdl_mode() { return env_int("RELAPACK_PDL", 3); }
 
 // RELAPACK_TRACE=1: every kernel of the plan records its first-CTA start and
 // last-CTA end (tools/trace_timeline.py reads them with relapack_trace_read).
@@ -495,12 +500,34 @@ static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int
   const cudaGraphNode_t root = cur[0];
   nodes.assign(pl.ops.size(), nullptr);
   std::vector<cudaGraphNode_t> want;
+  std::vector<cudaGraphEdgeData> edge;
+  auto kernel_op = [&](int j) { return pl.ops[j].kind <= OP_SYRK && !(debug_skip_mask() >> pl.ops[j].kind & 1); };
   for (size_t i = 0; i < pl.ops.size(); ++i) {
     want.clear();
-    for (int d : deps[i]) want.push_back(nodes[d]);
-    if (want.empty()) want.push_back(root);
-    if ((e = cudaStreamUpdateCaptureDependencies(st, want.data(), want.size(), cudaStreamSetCaptureDependencies)) !=
-        cudaSuccess)
+    edge.clear();
+    for (int d : deps[i]) {
+      want.push_back(nodes[d]);
+      // programmatic edge between two plan kernels (the downstream grid may
+      // launch once every CTA of the upstream one passed pdl_trigger; it
+      // still waits for its completion in ld_info) — not out of the
+      // deferred, SM-capped updates, whose early trigger would park the
+      // dependents' CTAs on the SMs the chain needs
+      cudaGraphEdgeData x{};
+      const int pm = pdl_mode();
+      const OpKind dk = pl.ops[i].kind;
+      const bool into = pm == 1 || dk == OP_POTF2 || dk == OP_TRSM || (pm == 3 && dk == OP_SYRK && !pl.ops[i].deferred);
+      if (pm > 0 && into && kernel_op((int)i) && kernel_op(d) && !pl.ops[d].deferred) {
+        x.from_port = cudaGraphKernelNodePortProgrammatic;
+        x.type = cudaGraphDependencyTypeProgrammatic;
+      }
+      edge.push_back(x);
+    }
+    if (want.empty()) {
+      want.push_back(root);
+      edge.push_back(cudaGraphEdgeData{});
+    }
+    if ((e = cudaStreamUpdateCaptureDependencies_v2(st, want.data(), edge.data(), want.size(),
+                                                    cudaStreamSetCaptureDependencies)) != cudaSuccess)
       return e;
     if ((e = launch_op(pl, i, A, ld, layout, d_info, st)) != cudaSuccess) return e;
     if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;

@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   __syncthreads();
   PROBE(1);
   const int fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
+  pdl_trigger();
   copy_lower<kBaseMax, false>(s, A, ld, layout, n);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
   PROBE(63);
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   PROBE(1);
   const int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
   PROBE(62);
+  pdl_trigger();
   copy_lower<64, false>(s, A, ld, layout, n);
   PROBE(63);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
     if (fail) fail += kN1;
     PROBE(55);
+    pdl_trigger();
 #if !RELAPACK_NODE_EARLY_STORE
     copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
 #endif
@@ -561,6 +564,7 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
         v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(layout, r, c, ld)] : (r == c ? 1.0 : 0.0);
       }
   const int fail = reg_potrf<TN>(v, lane);
+  pdl_trigger();
 #pragma unroll
   for (int i = 0; i < TN; ++i)
 #pragma unroll

@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
     TPROBE(3 + 2 * cb);
   }
   __syncthreads();
+  pdl_trigger();
   // ---- write the slab back
   {
     const int total = kFRows * t;
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
     if constexpr (NC == 2) solve_chunk_reg<RG, 1, NT>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
     TPROBE(4);
   }
+  pdl_trigger();
 #pragma unroll
   for (int r = 0; r < RG; ++r)
 #pragma unroll

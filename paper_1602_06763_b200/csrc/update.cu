@@ -153,7 +153,7 @@ __device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::
 // (persistent launch with a capped grid, see launch_tbm).
 template <int LAYOUT, bool USE_TMA, int TBM>
 __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtensorMap& tmB, const UpdateArgs& args,
-                                            uint8_t* smem, int work) {
+                                            uint8_t* smem, int work, bool last) {
   using C = Cfg<TBM>;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
@@ -248,6 +248,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
   // buffers are free now), then C -= tile with coalesced accesses along the
   // contiguous global dimension, 16 independent loads in flight per thread.
   // SYRK tiles write only i >= j.
+  if (last) pdl_trigger();  // this CTA's last tile: dependents may launch
   __syncthreads();
   double* sC = reinterpret_cast<double*>(smem);
 #pragma unroll
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
   const int nwork = args.ntiles * args.ksplit;
   for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
     if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
-    update_item<LAYOUT, USE_TMA, TBM>(tmA, tmB, args, smem, work);
+    update_item<LAYOUT, USE_TMA, TBM>(tmA, tmB, args, smem, work, work + (int)gridDim.x >= nwork);
   }
   trace_end(tr);
 }

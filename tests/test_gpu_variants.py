@@ -55,6 +55,8 @@ VARIANTS = {
     "no_tile32": {"RELAPACK_TILE32_BELOW": "0"},
     "crossover64": {"RELAPACK_CROSSOVER": "64", "RELAPACK_TRSM_BASE": "64"},
     "trsm_base256": {"RELAPACK_TRSM_BASE": "256"},
+    "pdl_all_edges": {"RELAPACK_PDL": "1"},
+    "pdl_off": {"RELAPACK_PDL": "0"},
 }
 
 
