@@ -42,16 +42,21 @@ struct Cfg {
   // 128: 8 warps of 64x32 (2 per SMSP, 255-reg budget); 64: 4 warps of
   // 32x32; 32: 4 warps of 16x16 (tiny latency-bound updates: a warp's DMMA
   // issue, K/4 x MT x NT x 16 cycles, is the floor, so small warp tiles)
-  static constexpr int NUM_WARPS = TBM == 128 ? 8 : 4;
+// 64-tiles: 4 warps of 32x32 (default) or 8 of 32x16 (compile-time knob;
+// measured n = 16384 47.06-47.53 vs 47.04 ms, n = 4096 2.25 vs 2.14 ms)
+#ifndef RELAPACK_UPD64_WARPS
+#define RELAPACK_UPD64_WARPS 4
+#endif
+  static constexpr int NUM_WARPS = TBM == 128 ? 8 : TBM == 64 ? RELAPACK_UPD64_WARPS : 4;
 #ifndef RELAPACK_UPD64_BLOCKS
-#define RELAPACK_UPD64_BLOCKS 1
+#define RELAPACK_UPD64_BLOCKS (RELAPACK_UPD64_WARPS == 8 ? 2 : 1)
 #endif
   // resident CTAs per SM the register budget is sized for (64-tiles with a
   // 3-CTA budget measured slightly slower: compile-time knob, default 1)
   static constexpr int MIN_BLOCKS = TBM == 128 ? 1 : TBM == 64 ? RELAPACK_UPD64_BLOCKS : 2;
   static constexpr int THREADS = NUM_WARPS * 32;
   static constexpr int WTM = TBM == 128 ? 64 : TBM == 64 ? 32 : 16;  // warp tile rows
-  static constexpr int WTN = TBM == 32 ? 16 : 32;                    // warp tile cols
+  static constexpr int WTN = TBM == 32 || (TBM == 64 && NUM_WARPS == 8) ? 16 : 32;  // warp tile cols
   static constexpr int MT = WTM / 8, NT = WTN / 8;      // DMMA tiles per warp
   static constexpr int WGM = TBM / WTM;                 // warps along M (2)
   static constexpr int TILE_BYTES = TBM * BK * 8;
