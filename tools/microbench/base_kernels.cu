@@ -72,6 +72,8 @@ int main() {
     cudaDeviceSynchronize();
     long long pr[64];
     cudaMemcpyFromSymbol(pr, g_tprobe, sizeof(pr));
+    printf("trsm_reg layout %c m=%d load: L issue %lld, slab loads issued %lld, L landed + rinv %lld\n",
+           lay == kLayoutN ? 'N' : 'T', m, pr[6] - pr[0], pr[7] - pr[6], pr[1] - pr[7]);
     printf("trsm_reg layout %c m=%d t=128 phases (cycles, CTA 0 thread 0): slab+L %lld | cb0 solve %lld | cb1 update %lld | cb1 solve %lld | store %lld | total %lld\n",
            lay == kLayoutN ? 'N' : 'T', m, pr[1] - pr[0], pr[2] - pr[1], pr[3] - pr[2], pr[4] - pr[3], pr[5] - pr[4], pr[5] - pr[0]);
   }
