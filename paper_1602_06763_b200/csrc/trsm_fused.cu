@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
   const int g = lane >> 2, tq = lane & 3;
   const int row_base = blockIdx.x * TRG<NW, RG>::ROWS + warp * 8 * RG;
   stage_L_all<NW>(sL, L, ldl, layout, t);  // async, overlaps the slab loads
+  TPROBE(6);
   constexpr int NT = 8 * NC;  // 8-column tiles held (t <= 64 NC)
   double xs[RG][NT][2];
   const bool pairs = layout == kLayoutT && (ldb & 1) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
           xs[r][sb][q] = (row < m && col + q < t) ? B[lv_off(layout, row, col + q, ldb)] : 0.0;
       }
     }
+  TPROBE(7);
   finish_L_all<NW>(sL, sRinv, t);
   __syncthreads();
   TPROBE(1);
