@@ -95,6 +95,7 @@ static bool dag_enabled() { return env_int("RELAPACK_DAG", 1) != 0; }
 // CTA cap of the deferred (lookahead) trailing updates: leaves SMs to the
 // next panel's chain; 0 = uncapped
 static int bulk_ctas() { return env_int("RELAPACK_BULK_CTAS", 132); }
+static double bulk_min_flops() { return 1e9 * env_int("RELAPACK_BULK_MIN_GF", 16); }
 // CTA cap of the non-deferred updates (0 = uncapped)
 static int upd_ctas() { return env_int("RELAPACK_UPD_CTAS", 0); }
 // deferred (lookahead) updates at low graph-node priority (RELAPACK_DEFER_LOW=0: equal)
@@ -653,7 +654,12 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
     for (size_t i = 0; i < p->ops.size(); ++i)
       if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) {
         fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
-        if (use_dag && p->ops[i].deferred) p->upd[i].max_ctas = bulk;
+        // deferred (lookahead) updates big enough to hold SMs for long run
+        // persistent on `bulk` CTAs, leaving SMs to the chain; small ones
+        // (below RELAPACK_BULK_MIN_GF GFLOP) run uncapped at low priority —
+        // capped, a small 64-tile GEMM runs one 4-warp CTA per SM at half the
+        // SM's rate and ends up on the critical path (n = 4096 trace)
+        if (use_dag && p->ops[i].deferred && p->ops[i].flops >= bulk_min_flops()) p->upd[i].max_ctas = bulk;
         // every other big update also leaves a few SMs free, so a base case
         // or TRSM that becomes ready does not wait for a long tile to drain
         // (tools/trace_timeline.py: otherwise the chain waits ~24 ms at n = 16384)

@@ -74,5 +74,12 @@ tot_wait = sum(a[2] for a in on_path.values())
 print(f"critical path: {len(path)} ops, running {tot_run / 1e3:.3f} ms + waiting {tot_wait / 1e3:.3f} ms")
 for k, (c, run, wait) in sorted(on_path.items(), key=lambda kv: -kv[1][1]):
     print(f"  {k:6s} x{c:4d} running {run / 1e3:8.3f} ms  waiting before start {wait / 1e3:8.3f} ms")
+if os.environ.get("CP_DETAIL") == "1":
+    prev_end = 0.0
+    for i in path:
+        r, o = recs[i], ops[i]
+        print(f"    {r['kind']:5s} m={o['m']:5d} n={o['n']:5d} k={o['k']:5d} lvl={o['level']} defer={o['deferred']} "
+              f"wait {max(0.0, r['t0_us'] - prev_end):7.1f} run {r['t1_us'] - r['t0_us']:7.1f} us")
+        prev_end = r["t1_us"]
 if len(sys.argv) > 3:
     json.dump({"recs": recs, "path": path}, open(sys.argv[3], "w"))
