@@ -349,9 +349,70 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
 // coalesced along the contiguous index.  MODE 0: synchronous load (zero
 // outside), 1: asynchronous load (cp.async; wait with cp.async.wait_all),
 // 2: store.
+// copy_rect for layout N with ld even and A 16-byte aligned: rows i, i+1 of
+// a column are adjacent in global and in shared memory (LDS even, r0 even),
+// so each thread moves 16-byte pairs (half the load/store instructions; the
+// copies of the 128-node are bound by LSU issue, not bandwidth).
+template <int R, int C, int LDS, int THREADS, int MODE>
+__device__ __forceinline__ void copy_rect_pairs(double* s, double* __restrict__ A, int64_t ld, int n, int r0,
+                                                int c0) {
+  constexpr int R2 = R / 2, kTot = R2 * C, kPer = (kTot + THREADS - 1) / THREADS, kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kPer; u0 += kBatch) {
+    double2 v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int e = threadIdx.x + (u0 + u) * THREADS;
+      const int i = r0 + 2 * (e % R2), j = c0 + e / R2;
+      const bool in = u0 + u < kPer && e < kTot;
+      const bool lo0 = in && i < n && i >= j, lo1 = in && i + 1 < n && i + 1 >= j;
+      double* g = A + i + (int64_t)j * ld;
+      double* sp = s + i + j * LDS;
+      if (MODE == 0)
+        v[u] = (lo0 && lo1) ? *reinterpret_cast<const double2*>(g) : make_double2(lo0 ? g[0] : 0.0, lo1 ? g[1] : 0.0);
+      if (MODE == 1 && in) {
+        if (lo0 && lo1) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sp)), "l"(g) : "memory");
+        } else {
+          if (lo0)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sp)), "l"(g) : "memory");
+          else
+            sp[0] = 0.0;
+          if (lo1)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sp + 1)), "l"(g + 1) : "memory");
+          else
+            sp[1] = 0.0;
+        }
+      }
+      if (MODE == 2 && (lo0 || lo1)) v[u] = *reinterpret_cast<const double2*>(sp);
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int e = threadIdx.x + (u0 + u) * THREADS;
+      const int i = r0 + 2 * (e % R2), j = c0 + e / R2;
+      const bool in = u0 + u < kPer && e < kTot;
+      const bool lo0 = in && i < n && i >= j, lo1 = in && i + 1 < n && i + 1 >= j;
+      double* g = A + i + (int64_t)j * ld;
+      if (MODE == 0 && in) *reinterpret_cast<double2*>(s + i + j * LDS) = v[u];
+      if (MODE == 2) {
+        if (lo0 && lo1) {
+          *reinterpret_cast<double2*>(g) = v[u];
+        } else {
+          if (lo0) g[0] = v[u].x;
+          if (lo1) g[1] = v[u].y;
+        }
+      }
+    }
+  }
+}
+
 template <int R, int C, int LDS, int THREADS, int MODE>
 __device__ __forceinline__ void copy_rect(double* s, double* __restrict__ A, int64_t ld, int layout, int n, int r0,
-                                          int c0) {
+                                          int c0, bool pairs) {
+  if (pairs && layout == kLayoutN && (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    copy_rect_pairs<R, C, LDS, THREADS, MODE>(s, A, ld, n, r0, c0);
+    return;
+  }
   constexpr int kTot = R * C, kPer = (kTot + THREADS - 1) / THREADS, kBatch = 16;
 #pragma unroll 1
   for (int u0 = 0; u0 < kPer; u0 += kBatch) {
@@ -493,6 +554,8 @@ __device__ __forceinline__ void syrk_in_smem(double* s, int n2) {
 
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double* A, int64_t ld, int layout, int n,
                                                                           int* d_info, int info_base, TraceRec* tr) {
+  const bool pairs = (layout & 0x100) != 0;  // 16-byte copies (host knob RELAPACK_COPY_PAIRS)
+  layout &= 0xff;
   constexpr int LDS = P2<kBaseMax>::LDS, NW = P2<kBaseMax>::NW;
   PROBE(50);
   if (ld_info(d_info) != 0) return;
@@ -503,8 +566,8 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   if (threadIdx.x == 0) fail_flag = 0;
   constexpr int TH = P2<kBaseMax>::THREADS;
   // A11 now; A21 and A22 stream in (cp.async) while A11 is factored
-  copy_rect<kN1, kN1, LDS, TH, 0>(s, A, ld, layout, n, 0, 0);
-  copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, n, kN1, 0);
+  copy_rect<kN1, kN1, LDS, TH, 0>(s, A, ld, layout, n, 0, 0, pairs);
+  copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, n, kN1, 0, pairs);
   __syncthreads();
   PROBE(51);
   int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
@@ -519,7 +582,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     PROBE(53);
 #if RELAPACK_NODE_EARLY_STORE
     // L11 and L21 are final: write them back while A22 is finished
-    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
 #endif
     syrk_in_smem<LDS, NW>(s, n2);
     __syncthreads();
@@ -529,13 +592,13 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     PROBE(55);
     pdl_trigger();
 #if !RELAPACK_NODE_EARLY_STORE
-    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
 #endif
-    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1);
+    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
   } else {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     PROBE(55);
-    copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0);
+    copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
   }
   PROBE(56);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
@@ -594,6 +657,15 @@ static bool potf2_use_regs(int n) { return n <= potf2_regs_max(); }
 
 // 64 < n <= 128: the in-CTA recursion node (default) or the flat right-looking
 // kernel (RELAPACK_NODE128=0).
+// 128-node copies as 16-byte pairs for uplo L (RELAPACK_COPY_PAIRS=0: 8-byte)
+static bool copy_pairs() {
+  static const bool r = [] {
+    const char* v = getenv("RELAPACK_COPY_PAIRS");
+    return !(v && v[0] == '0');
+  }();
+  return r;
+}
+
 static bool potf2_node128() {
   static const bool r = [] {
     const char* v = getenv("RELAPACK_NODE128");
@@ -629,7 +701,8 @@ cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, 
   } else if (n <= 64)
     k_potf2_base64<<<1, P2<64>::THREADS, P2<64>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
   else if (potf2_node128())
-    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
+    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout | (copy_pairs() ? 0x100 : 0), n,
+                                                                          d_info, info_base, g_launch_trace);
   else
     k_potf2_base<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
   return cudaGetLastError();
