@@ -403,6 +403,23 @@ static long small_tile_threshold() {
   return t;
 }
 
+// (RELAPACK_TILE32_MAX_TILES / RELAPACK_TILE32_MAX_K: 32-tiles for any update
+// with at most that many 32-tiles and K at most that long)
+static long tile32_max_tiles() {
+  static const long t = [] {
+    const char* v = getenv("RELAPACK_TILE32_MAX_TILES");
+    return v ? atol(v) : 0L;
+  }();
+  return t;
+}
+static int tile32_max_k() {
+  static const int t = [] {
+    const char* v = getenv("RELAPACK_TILE32_MAX_K");
+    return v ? atoi(v) : 1024;
+  }();
+  return t;
+}
+
 // Tile size for an update: 128 x 128 CTA tiles when they fill the 148 SMs,
 // else 64 x 64 (4x the CTAs; latency of the small updates near the leaves),
 // and 32 x 32 one-warp tiles when even the 64-tiles would leave most SMs
@@ -419,6 +436,10 @@ int update_tile_for(int M, int N, int K, int tri) {
   // to 64-tiles, whose 4 warps of 32 x 32 reach about half of it
   const int KT = (K + BK - 1) / BK;
   if (split128_enabled() && tiles(128) * (KT / 16) >= 148) return 128;
+  // short-K updates whose 32-tiles still fit ~4 CTAs per SM: the 4-warp
+  // 16x16 tiles finish sooner than 64-tiles (tools/microbench/update_small:
+  // gemm 2048x128x128 11.9 -> 7.1 us, gemm 512^2 x 512 24.2 -> 18.8 us)
+  if (K <= tile32_max_k() && tiles(32) <= tile32_max_tiles()) return 32;
   if (tiles(64) >= small_tile_threshold()) return 64;
   return 32;
 }

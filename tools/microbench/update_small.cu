@@ -10,7 +10,7 @@ thread_local TraceRec* g_launch_trace = nullptr;
 using namespace relapack;
 
 static UpdateOp make(double* A, int64_t ld, int M, int N, int K, int tri, const int* info, double* ws, int* cnt,
-                     int ks_force) {
+                     int ks_force, int tile_force = 0) {
   UpdateOp u{};
   UpdateArgs& a = u.args;
   memset(&a, 0, sizeof(a));
@@ -23,7 +23,7 @@ static UpdateOp make(double* A, int64_t ld, int M, int N, int K, int tri, const 
   a.M = M;
   a.N = N;
   a.tri = tri;
-  u.tile = update_tile_for(M, N, K, tri);
+  u.tile = tile_force ? tile_force : update_tile_for(M, N, K, tri);
   a.tiles_m = (M + u.tile - 1) / u.tile;
   const int tn = (N + u.tile - 1) / u.tile;
   a.ntiles = tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * tn;
@@ -58,9 +58,13 @@ int main() {
   struct Shape { int M, N, K, tri; } shapes[] = {{128, 128, 128, 1}, {128, 128, 256, 1}, {256, 256, 512, 1},
                                                 {512, 512, 1024, 1}, {1024, 1024, 2048, 1}, {128, 128, 128, 0},
                                                 {2048, 128, 128, 0}, {512, 512, 512, 0}, {1024, 1024, 2048, 0}, {2048, 1024, 1024, 0}};
-  for (auto sh : shapes) {
-    for (int ksf : {0, 1, 2, 4, 8}) {
-      UpdateOp u = make(A, n, sh.M, sh.N, sh.K, sh.tri, info, ws, cnt, ksf);
+  for (auto sh : shapes)
+  for (int tf : {0, 32, 64, 128}) {
+    if (tf && sh.M < 2 * tf) continue;
+    for (int ksf : {0, 1, 2, 4, 8, 16}) {
+      UpdateOp u = make(A, n, sh.M, sh.N, sh.K, sh.tri, info, ws, cnt, ksf, tf);
+      if (tf && ksf == 0) continue;
+      if ((sh.K + 15) / 16 < 2 * u.args.ksplit) continue;
       if (u.args.ksplit > 1 && (int64_t)u.args.ksplit * u.args.ntiles * u.tile * u.tile * 8 > (64ll << 20)) continue;
       cudaGraph_t g;
       cudaGraphExec_t ge;
@@ -80,8 +84,8 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       const double fl = sh.tri ? (double)sh.N * sh.N * sh.K : 2.0 * sh.M * sh.N * sh.K;
-      printf("%s M=%4d N=%4d K=%4d tile=%3d ksplit=%d%s: %7.2f us/launch  %6.2f TF/s (%s)\n", sh.tri ? "syrk" : "gemm",
-             sh.M, sh.N, sh.K, u.tile, u.args.ksplit, ksf == 0 ? " (auto)" : "", ms * 1e3 / 200,
+      printf("%s M=%4d N=%4d K=%4d tile=%3d%s ksplit=%2d%s: %7.2f us/launch  %6.2f TF/s (%s)\n", sh.tri ? "syrk" : "gemm",
+             sh.M, sh.N, sh.K, u.tile, tf ? "f" : " ", u.args.ksplit, ksf == 0 ? " (auto)" : "", ms * 1e3 / 200,
              fl / (ms * 1e-3 / 200) / 1e12, cudaGetErrorString(cudaGetLastError()));
       cudaGraphExecDestroy(ge);
       cudaGraphDestroy(g);
