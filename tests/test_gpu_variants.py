@@ -57,6 +57,9 @@ VARIANTS = {
     "trsm_base256": {"RELAPACK_TRSM_BASE": "256"},
     "pdl_all_edges": {"RELAPACK_PDL": "1"},
     "pdl_off": {"RELAPACK_PDL": "0"},
+    "copy_8byte": {"RELAPACK_COPY_PAIRS": "0"},
+    "defer_cap_all": {"RELAPACK_BULK_MIN_GF": "0"},
+    "no_defer_cap": {"RELAPACK_BULK_CTAS": "0"},
 }
 
 
