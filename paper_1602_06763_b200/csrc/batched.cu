@@ -37,6 +37,10 @@
 
 namespace relapack {
 
+#ifndef RELAPACK_BATCH_SQUARE
+#define RELAPACK_BATCH_SQUARE 1
+#endif
+
 namespace {
 
 constexpr int kPanel = 8;
@@ -59,8 +63,12 @@ struct BC {
 #endif
   static constexpr int MIN_BLOCKS =
       NMAX == 64 ? RELAPACK_BATCH_MINB64 : NMAX == 48 ? RELAPACK_BATCH_MINB48 : NMAX == 32 ? RELAPACK_BATCH_MINB32 : 8;
-  // even-packed lower triangle: NMAX (NMAX/2 + 1) doubles per prefetch slot
-  static constexpr int SLOT = NMAX * (NMAX / 2 + 1);
+  // even-packed lower triangle: NMAX (NMAX/2 + 1) doubles per prefetch slot;
+  // n <= 32, uplo L: room for the whole column-major square at stride SQ_LD
+  // instead (the square path below)
+  static constexpr bool SQ = NMAX <= 32 && LAYOUT == kLayoutN && RELAPACK_BATCH_SQUARE;
+  static constexpr int SQ_LD = NMAX + 2;  // 16-byte aligned columns; DMMA-layout reads 2-way (the minimum)
+  static constexpr int SLOT = SQ && NMAX * SQ_LD > NMAX * (NMAX / 2 + 1) ? NMAX * SQ_LD : NMAX * (NMAX / 2 + 1);
   static constexpr size_t SMEM = sizeof(double) * SLOT * WPC;
   // layout N: column j of L from row (j & ~1), columns back to back;
   // layout T: row i of L, columns 0 .. (i | 1), rows back to back.
@@ -107,9 +115,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Small full-class matrices stored densely (n == lda == NMAX <= 32, uplo L):
+// the per-column bulk copies would be 8..256 bytes each, so the lanes instead
+// move the columns' lower parts as 16-byte cp.async chunks (a few per lane).
+template <int NMAX, int LAYOUT>
+__device__ __forceinline__ bool square_ok(const double* A, int n, int64_t lda) {
+  return BC<NMAX, LAYOUT>::SQ && n == NMAX && lda == NMAX && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+}
+
 template <int NMAX, int LAYOUT>
 __device__ __forceinline__ bool bulk_ok(const double* A, int n, int64_t lda) {
-  return ((n & 1) == 0) && ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  return !square_ok<NMAX, LAYOUT>(A, n, lda) && ((n & 1) == 0) && ((lda & 1) == 0) &&
+         ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
 }
 
 // Start the load of matrix (A, n, lda) into slot s: one bulk copy per column
@@ -118,6 +135,20 @@ __device__ __forceinline__ bool bulk_ok(const double* A, int n, int64_t lda) {
 template <int NMAX, int LAYOUT>
 __device__ __forceinline__ void issue_load(double* s, uint64_t* bar, const double* A, int n, int64_t lda, int lane) {
   using C = BC<NMAX, LAYOUT>;
+  if (square_ok<NMAX, LAYOUT>(A, n, lda)) {
+    constexpr int CH = NMAX / 2;  // 16-byte chunks per column
+    __syncwarp();                 // every lane has read the previous matrix out of the slot
+#pragma unroll
+    for (int k = lane; k < NMAX * CH; k += 32) {
+      const int col = k / CH, r2 = 2 * (k % CH);
+      if (r2 + 1 < col) continue;  // wholly above the diagonal
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s + col * C::SQ_LD + r2)),
+                   "l"(A + col * NMAX + r2)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    return;
+  }
   if (!bulk_ok<NMAX, LAYOUT>(A, n, lda)) return;
   fence_proxy_async_smem();  // this warp's earlier generic accesses of the slot precede the async writes
   if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(8 * n * (n / 2 + 1)));
@@ -137,13 +168,23 @@ __device__ __forceinline__ void issue_load(double* s, uint64_t* bar, const doubl
 // else straight from global memory); identity beyond n, 0 above the diagonal.
 template <int NMAX, int LAYOUT>
 __device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], const double* s, bool from_slot,
-                                          const double* A, int n, int64_t lda, int lane) {
+                                          bool square, const double* A, int n, int64_t lda, int lane) {
   using C = BC<NMAX, LAYOUT>;
   using T = RegTri<NMAX / 8>;
   const int g = lane >> 2, t = lane & 3;
-  // two separate loops (warp-uniform branch): a select between the shared and
+  // separate loops (warp-uniform branches): a select between the shared and
   // the global load would issue both
-  if (from_slot) {
+  if (C::SQ && square) {
+#pragma unroll
+    for (int i = 0; i < C::TN; ++i)
+#pragma unroll
+      for (int k = 0; k <= i; ++k)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+          v[T::id(i, k)][q] = r >= c ? s[r + c * C::SQ_LD] : (r == c ? 1.0 : 0.0);
+        }
+  } else if (from_slot) {
 #pragma unroll
     for (int i = 0; i < C::TN; ++i)
 #pragma unroll
@@ -198,12 +239,16 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
   uint32_t parity = 0;
   while (pos < count) {
     double v[T::NT][2];
+    const bool sq = square_ok<NMAX, LAYOUT>(A, n, lda);
     const bool bulk = bulk_ok<NMAX, LAYOUT>(A, n, lda);
-    if (bulk) {
+    if (sq) {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();
+    } else if (bulk) {
       mbar_wait(bar, parity);
       parity ^= 1u;
     }
-    load_regs<NMAX, LAYOUT>(v, slot, bulk, A, n, lda, lane);
+    load_regs<NMAX, LAYOUT>(v, slot, bulk, sq, A, n, lda, lane);
     // prefetch this warp's next matrix into the (now consumed) slot
     const int npos = pos + stride;
     int nb = 0, nn = 0;
