@@ -26,6 +26,7 @@
 //  * odd n, odd lda or a base not 16-byte aligned take a plain-load path into
 //    the same slot layout.
 #include <mutex>
+#include <type_traits>
 
 #include "chol_regs.cuh"
 #include "common.cuh"
@@ -342,7 +343,19 @@ struct BatchWs {
   int* buf = nullptr;
   size_t cap = 0;  // batch entries
   int sms = 0;
+  // one stream per size class, forked from / joined back into the caller's
+  // stream: a class's CTAs start on the SMs the previous class's tail frees
+  cudaStream_t cs[kClasses] = {};
+  cudaEvent_t fork = nullptr, join[kClasses] = {};
 };
+
+static bool batch_streams() {
+  static const bool v = [] {
+    const char* e = getenv("RELAPACK_BATCH_STREAMS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 BatchWs g_bws[kMaxDevices];
 
 }  // namespace
@@ -373,21 +386,61 @@ cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* 
   if ((e = cudaMemsetAsync(counts, 0, kClasses * sizeof(int), st)) != cudaSuccess) return e;
   k_bucket<<<(batch + 255) / 256, 256, 0, st>>>(batch, d_n, d_lda, d_info, counts, lists);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  return layout == kLayoutN ? launch_classes<kLayoutN>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st)
-                            : launch_classes<kLayoutT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st);
+  if (!batch_streams())
+    return layout == kLayoutN ? launch_classes<kLayoutN>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st)
+                              : launch_classes<kLayoutT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st);
+  if (!w.fork) {
+    if ((e = cudaEventCreateWithFlags(&w.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int c = 0; c < kClasses; ++c) {
+      if ((e = cudaStreamCreateWithFlags(&w.cs[c], cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&w.join[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+  }
+  if ((e = cudaEventRecord(w.fork, st)) != cudaSuccess) return e;
+  for (int c = kClasses - 1; c >= 0; --c) {  // the 64-class (longest) first
+    if ((e = cudaStreamWaitEvent(w.cs[c], w.fork, 0)) != cudaSuccess) return e;
+    const int nmax = 16 * (c + 1);
+    auto go = [&](auto lay) -> cudaError_t {
+      constexpr int L = decltype(lay)::value;
+      switch (nmax) {
+        case 64: return launch_cls<64, L>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, w.cs[c]);
+        case 48: return launch_cls<48, L>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, w.cs[c]);
+        case 32: return launch_cls<32, L>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, w.cs[c]);
+        default: return launch_cls<16, L>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, w.cs[c]);
+      }
+    };
+    e = layout == kLayoutN ? go(std::integral_constant<int, kLayoutN>{}) : go(std::integral_constant<int, kLayoutT>{});
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(w.join[c], w.cs[c])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, w.join[c], 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 void release_batched_workspace() {
   for (int d = 0; d < kMaxDevices; ++d) {
     std::lock_guard<std::mutex> lk(g_bws[d].mu);
-    if (g_bws[d].buf) {
+    BatchWs& w = g_bws[d];
+    if (w.buf || w.fork) {
       int cur = 0;
       cudaGetDevice(&cur);
       cudaSetDevice(d);
-      cudaFree(g_bws[d].buf);
+      if (w.buf) cudaFree(w.buf);
+      if (w.fork) {
+        cudaEventDestroy(w.fork);
+        for (int c = 0; c < kClasses; ++c) {
+          cudaStreamDestroy(w.cs[c]);
+          cudaEventDestroy(w.join[c]);
+        }
+      }
       cudaSetDevice(cur);
     }
-    g_bws[d].buf = nullptr;
+    w.buf = nullptr;
+    w.fork = nullptr;
+    for (int c = 0; c < kClasses; ++c) {
+      w.cs[c] = nullptr;
+      w.join[c] = nullptr;
+    }
     g_bws[d].cap = 0;
   }
 }

@@ -2,8 +2,9 @@
 
 The knobs are read once per process, so every variant runs in a subprocess
 that factors a few seeded matrices (both uplo, several recursion depths, panel
-heights on both sides of the kernels' CTA-size thresholds) and compares them
-with the oracle under the same tolerances as test_gpu_parity.py.
+heights on both sides of the kernels' CTA-size thresholds) and a batch (CFG[4]
+shape and ragged layouts), and compares them with the oracle under the same
+tolerances as test_gpu_parity.py.
 """
 import os
 import subprocess
@@ -38,6 +39,10 @@ for seed in (1, 2):
     for uplo in "LU":
         dA = to_dev(A); info = rl.dpotrf(dA, uplo); torch.cuda.synchronize()
         assert info == 0 and np.array_equal(lower_of(dev_full(dA, 256), uplo), L), (seed, uplo)
+from tests.test_gpu_parity import test_batched_parity, test_batched_ragged_layouts
+for uplo in "LU":
+    test_batched_parity(uplo)
+    test_batched_ragged_layouts(uplo)
 print("variant ok")
 """
 
@@ -59,6 +64,7 @@ VARIANTS = {
     "pdl_off": {"RELAPACK_PDL": "0"},
     "copy_8byte": {"RELAPACK_COPY_PAIRS": "0"},
     "defer_cap_all": {"RELAPACK_BULK_MIN_GF": "0"},
+    "batch_one_stream": {"RELAPACK_BATCH_STREAMS": "0"},
     "no_defer_cap": {"RELAPACK_BULK_CTAS": "0"},
 }
 
