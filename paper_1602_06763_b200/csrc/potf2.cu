@@ -406,11 +406,77 @@ __device__ __forceinline__ void copy_rect_pairs(double* s, double* __restrict__ 
   }
 }
 
+// copy_rect for layout T (uplo U) with ld even and A 16-byte aligned: the L
+// view's (i, j) and (i, j + 1) are adjacent in global memory, so a warp moves
+// an 8-row x 8-column patch as 16-byte global accesses (4 column pairs x 8
+// rows) and 8-byte shared-memory accesses at i + j*LDS, which with LDS = 4
+// mod 16 hit every bank pair exactly twice (the element-wise copy runs 32
+// consecutive columns per warp: 8-way conflicted).
+template <int R, int C, int LDS, int THREADS, int MODE>
+__device__ __forceinline__ void copy_rect_pairsT(double* s, double* __restrict__ A, int64_t ld, int n, int r0,
+                                                 int c0) {
+  static_assert(R % 8 == 0 && C % 8 == 0, "8x8 patches");
+  constexpr int NW = THREADS / 32, PATCHES = (R / 8) * (C / 8), kPer = (PATCHES + NW - 1) / NW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jp = lane & 3, il = lane >> 2;
+  constexpr int kBatch = 4;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kPer; u0 += kBatch) {
+    double2 v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int p = warp + (u0 + u) * NW;
+      const bool in = u0 + u < kPer && p < PATCHES;
+      const int i = r0 + 8 * (p / (C / 8)) + il, j = c0 + 8 * (p % (C / 8)) + 2 * jp;
+      const bool lo0 = in && i < n && i >= j, lo1 = in && i < n && i >= j + 1;
+      double* g = A + j + (int64_t)i * ld;
+      if (MODE == 0)
+        v[u] = (lo0 && lo1) ? *reinterpret_cast<const double2*>(g) : make_double2(lo0 ? g[0] : 0.0, lo1 ? g[1] : 0.0);
+      if (MODE == 1 && in) {
+        double* sp = s + i + j * LDS;
+        if (lo0)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sp)), "l"(g) : "memory");
+        else
+          sp[0] = 0.0;
+        if (lo1)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sp + LDS)), "l"(g + 1) : "memory");
+        else
+          sp[LDS] = 0.0;
+      }
+      if (MODE == 2 && (lo0 || lo1)) v[u] = make_double2(s[i + j * LDS], s[i + (j + 1) * LDS]);
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int p = warp + (u0 + u) * NW;
+      const bool in = u0 + u < kPer && p < PATCHES;
+      const int i = r0 + 8 * (p / (C / 8)) + il, j = c0 + 8 * (p % (C / 8)) + 2 * jp;
+      const bool lo0 = in && i < n && i >= j, lo1 = in && i < n && i >= j + 1;
+      double* g = A + j + (int64_t)i * ld;
+      if (MODE == 0 && in) {
+        s[i + j * LDS] = v[u].x;
+        s[i + (j + 1) * LDS] = v[u].y;
+      }
+      if (MODE == 2) {
+        if (lo0 && lo1) {
+          *reinterpret_cast<double2*>(g) = v[u];
+        } else {
+          if (lo0) g[0] = v[u].x;
+          if (lo1) g[1] = v[u].y;
+        }
+      }
+    }
+  }
+}
+
 template <int R, int C, int LDS, int THREADS, int MODE>
 __device__ __forceinline__ void copy_rect(double* s, double* __restrict__ A, int64_t ld, int layout, int n, int r0,
                                           int c0, bool pairs) {
   if (pairs && layout == kLayoutN && (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
     copy_rect_pairs<R, C, LDS, THREADS, MODE>(s, A, ld, n, r0, c0);
+    return;
+  }
+  if (pairs && layout == kLayoutT && (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    copy_rect_pairsT<R, C, LDS, THREADS, MODE>(s, A, ld, n, r0, c0);
     return;
   }
   constexpr int kTot = R * C, kPer = (kTot + THREADS - 1) / THREADS, kBatch = 16;
