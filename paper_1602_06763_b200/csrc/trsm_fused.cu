@@ -306,6 +306,9 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
 // holds only the three L blocks (104 KB) and a CTA covers 8 * RG * NW rows —
 // twice the rows per SM of the shared-memory slab at the same per-warp chain
 // (the RG groups' substitution chains interleave in one instruction stream).
+#ifndef RELAPACK_TRSM_MASKL
+#define RELAPACK_TRSM_MASKL 1
+#endif
 #ifndef RELAPACK_TRSM_SPLITACC
 #define RELAPACK_TRSM_SPLITACC 1
 #endif
@@ -326,8 +329,14 @@ __device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][NT][2], const d
     double l0[8], l1[8], rc[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
+#if RELAPACK_TRSM_MASKL
+      // L(8s+2t, 8s+c), L(8s+2t+1, 8s+c): zero above the diagonal, not loaded
+      l0[c] = 2 * tq > c ? sLd[(8 * s + 2 * tq) * kFLdL + 8 * s + c] : 0.0;
+      l1[c] = 2 * tq + 1 > c ? sLd[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c] : 0.0;
+#else
       l0[c] = sLd[(8 * s + 2 * tq) * kFLdL + 8 * s + c];      // L(8s+2t,   8s+c), 0 unless 2t > c
       l1[c] = sLd[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c];  // L(8s+2t+1, 8s+c)
+#endif
       rc[c] = sRd[8 * s + c];
     }
 #pragma unroll
