@@ -534,7 +534,10 @@ static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int
     if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;
     if (ncur != 1) return cudaErrorStreamCaptureInvalidated;
     nodes[i] = cur[0];
-    deferred_node.push_back((char)pl.ops[i].deferred);
+    // priority class: 2 deferred update, 1 other GEMM (the TRSM's updates),
+    // 0 the chain (base cases, TRSM bases, the non-deferred SYRKs)
+    const PlanOp& o = pl.ops[i];
+    deferred_node.push_back((char)(o.deferred ? (o.flops >= bulk_min_flops() ? 3 : 2) : o.kind == OP_GEMM ? 1 : 0));
   }
   // join every sink so the capture ends on one node
   std::vector<char> has_succ(pl.ops.size(), 0);
@@ -557,7 +560,22 @@ static cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes
     if ((e = cudaGraphNodeGetType(nodes[i], &t)) != cudaSuccess) return e;
     if (t != cudaGraphNodeTypeKernel) continue;
     cudaKernelNodeAttrValue v{};
-    v.priority = (deferred[i] && defer_low_priority()) ? least : greatest;
+    const int cls = deferred[i];
+    const int mode = env_int("RELAPACK_PRIO_MODE", 1);
+    // mode 0: deferred lowest, the rest highest; 1: chain > TRSM GEMMs >
+    // deferred; 2: TRSM GEMMs > chain > deferred; 3: as 1 with the small
+    // (uncapped) deferred updates one level above the large ones
+    const int step = greatest < least ? 1 : -1;  // towards lower priority
+    if (cls >= 2)
+      v.priority = !defer_low_priority() ? greatest
+                   : (mode == 3 && cls == 2 && least != greatest + 2 * step) ? least - step
+                                                                             : least;
+    else if (mode == 1 || mode == 3)
+      v.priority = cls == 0 ? greatest : greatest + step;
+    else if (mode == 2)
+      v.priority = cls == 1 ? greatest : greatest + step;
+    else
+      v.priority = greatest;
     if ((e = cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v)) != cudaSuccess) return e;
   }
   return cudaSuccess;

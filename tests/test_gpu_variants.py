@@ -65,6 +65,7 @@ VARIANTS = {
     "copy_8byte": {"RELAPACK_COPY_PAIRS": "0"},
     "defer_cap_all": {"RELAPACK_BULK_MIN_GF": "0"},
     "batch_one_stream": {"RELAPACK_BATCH_STREAMS": "0"},
+    "prio_two_levels": {"RELAPACK_PRIO_MODE": "0"},
     "no_defer_cap": {"RELAPACK_BULK_CTAS": "0"},
 }
 
