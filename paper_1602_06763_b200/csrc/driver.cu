@@ -241,7 +241,8 @@ static cudaError_t setup_splitk(Plan& p, const std::vector<uint64_t>* anc) {
   for (size_t i = 0; i < nops; ++i) {
     if (p.ops[i].kind != OP_GEMM && p.ops[i].kind != OP_SYRK) continue;
     UpdateArgs& a = p.upd[i].args;
-    const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, p.upd[i].tile);
+    const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, p.upd[i].tile,
+                                     p.ops[i].kind == OP_SYRK && !p.ops[i].deferred);
     if (ks <= 1) continue;
     a.ksplit = ks;
     const int64_t e = update_ws_elems(a.M, a.N, a.tri, p.upd[i].tile, ks);

@@ -50,7 +50,9 @@ bool make_operand_map(CUtensorMap* map, const double* base, int64_t ld, int layo
 int update_tile_for(int M, int N, int K, int tri);
 // Split-K factor for an update of (M, N, K) on `tile` x `tile` CTA tiles (1 = none)
 // and the workspace it needs (doubles) — see update.cu.
-int update_ksplit_for(int M, int N, int K, int tri, int tile);
+// chain: the update sits on the base-case chain (non-deferred SYRK): latency
+// over efficiency, down to 2 k-tiles per split
+int update_ksplit_for(int M, int N, int K, int tri, int tile, bool chain = false);
 int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit);
 
 // ---- K1 base-case potf2 (potf2.cu) ----

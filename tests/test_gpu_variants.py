@@ -66,6 +66,7 @@ VARIANTS = {
     "defer_cap_all": {"RELAPACK_BULK_MIN_GF": "0"},
     "batch_one_stream": {"RELAPACK_BATCH_STREAMS": "0"},
     "prio_two_levels": {"RELAPACK_PRIO_MODE": "0"},
+    "chain_split_as_others": {"RELAPACK_SPLITK_CHAIN_KT": "0"},
     "no_defer_cap": {"RELAPACK_BULK_CTAS": "0"},
 }
 
