@@ -347,6 +347,9 @@ struct BatchWs {
   // stream: a class's CTAs start on the SMs the previous class's tail frees
   cudaStream_t cs[kClasses] = {};
   cudaEvent_t fork = nullptr, join[kClasses] = {};
+  // end of the last call that used the workspace: a call on another stream
+  // waits for it before overwriting the counts / lists
+  cudaEvent_t done = nullptr;
 };
 
 static bool batch_streams() {
@@ -383,12 +386,20 @@ cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* 
   // the lists are indexed with stride `batch` of this call
   int* counts = w.buf;
   int* lists = w.buf + kClasses;
+  if (!w.done && (e = cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  if ((e = cudaStreamIsCapturing(st, &capturing)) != cudaSuccess) return e;
+  // the previous call (any stream) has finished with the workspace; inside a
+  // graph capture the graph's own edges order the calls instead
+  if (capturing == cudaStreamCaptureStatusNone && (e = cudaStreamWaitEvent(st, w.done, 0)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(counts, 0, kClasses * sizeof(int), st)) != cudaSuccess) return e;
   k_bucket<<<(batch + 255) / 256, 256, 0, st>>>(batch, d_n, d_lda, d_info, counts, lists);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (!batch_streams())
-    return layout == kLayoutN ? launch_classes<kLayoutN>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st)
-                              : launch_classes<kLayoutT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st);
+  if (!batch_streams()) {
+    e = layout == kLayoutN ? launch_classes<kLayoutN>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st)
+                           : launch_classes<kLayoutT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st);
+    return e != cudaSuccess || capturing != cudaStreamCaptureStatusNone ? e : cudaEventRecord(w.done, st);
+  }
   if (!w.fork) {
     if ((e = cudaEventCreateWithFlags(&w.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
     for (int c = 0; c < kClasses; ++c) {
@@ -414,7 +425,8 @@ cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* 
     if ((e = cudaEventRecord(w.join[c], w.cs[c])) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(st, w.join[c], 0)) != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  // (not inside a capture: an event recorded there cannot be waited on later)
+  return capturing != cudaStreamCaptureStatusNone ? cudaSuccess : cudaEventRecord(w.done, st);
 }
 
 void release_batched_workspace() {
@@ -426,6 +438,7 @@ void release_batched_workspace() {
       cudaGetDevice(&cur);
       cudaSetDevice(d);
       if (w.buf) cudaFree(w.buf);
+      if (w.done) cudaEventDestroy(w.done);
       if (w.fork) {
         cudaEventDestroy(w.fork);
         for (int c = 0; c < kClasses; ++c) {
@@ -437,6 +450,7 @@ void release_batched_workspace() {
     }
     w.buf = nullptr;
     w.fork = nullptr;
+    w.done = nullptr;
     for (int c = 0; c < kClasses; ++c) {
       w.cs[c] = nullptr;
       w.join[c] = nullptr;

@@ -270,6 +270,61 @@ def test_batched_parity(uplo):
     assert worst <= TOL
 
 
+def _batched_case(count, seed):
+    b = gen.batched_spd(count, seed)
+    buf = torch.from_numpy(b["buf"]).cuda()
+    ptrs = (buf.data_ptr() + 8 * torch.from_numpy(b["offsets"])).cuda()
+    ns = torch.from_numpy(b["ns"]).cuda()
+    ldas = torch.from_numpy(b["ldas"]).cuda()
+    infos = torch.full((len(b["ns"]),), -99, dtype=torch.int32, device="cuda")
+    return b, buf, ptrs, ns, ldas, infos
+
+
+def _batched_check(b, buf, infos):
+    ref = b["buf"].copy()
+    rinfo = oracle.dpotrf_batched("L", b["ns"], ref, b["offsets"], b["ldas"])
+    assert np.array_equal(infos.cpu().numpy(), rinfo)
+    G = buf.cpu().numpy()
+    for i in np.nonzero(rinfo == 0)[0]:
+        nb, off = int(b["ns"][i]), int(b["offsets"][i])
+        A = b["buf"][off: off + nb * nb].reshape(nb, nb).T
+        g = G[off: off + nb * nb].reshape(nb, nb).T
+        r = ref[off: off + nb * nb].reshape(nb, nb).T
+        assert floored_rel_err(lower_of(g, "L"), lower_of(r, "L"), A) <= TOL
+
+
+def test_batched_two_streams():
+    """Back-to-back batched calls on two streams share the library's bucketing
+    workspace: the second must not overwrite it while the first still runs."""
+    cases = [_batched_case(4000, 21), _batched_case(3000, 22)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for (b, buf, ptrs, ns, ldas, infos), s in zip(cases, (s1, s2)):
+        with torch.cuda.stream(s):
+            assert rl.dpotrf_batched(ns, ptrs, ldas, infos, "L") == 0
+    torch.cuda.synchronize()
+    for b, buf, ptrs, ns, ldas, infos in cases:
+        _batched_check(b, buf, infos)
+
+
+def test_batched_graph_capture():
+    """The batched call (bucketing + size classes on forked streams) captured
+    into a CUDA graph and replayed gives the same factors."""
+    b, buf, ptrs, ns, ldas, infos = _batched_case(2000, 23)
+    pristine = buf.clone()
+    assert rl.dpotrf_batched(ns, ptrs, ldas, infos, "L") == 0  # sizes the workspace outside capture
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rl.dpotrf_batched(ns, ptrs, ldas, infos, "L", stream=s)
+    for _ in range(2):
+        buf.copy_(pristine)
+        infos.fill_(-99)
+        g.replay()
+        torch.cuda.synchronize()
+        _batched_check(b, buf, infos)
+
+
 def test_batched_bad_sizes():
     n_ok = 16
     buf = torch.from_numpy(np.asfortranarray(gen.spd(n_ok, 1)).T.copy().reshape(-1)).cuda()
