@@ -92,11 +92,16 @@ RELAPACK_API void relapack_dpotrf(const char* uplo, const int* n, double* A, con
 RELAPACK_API int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int* d_info, relapack_stream_t stream);
 
 /*
- * relapack_dpotrf_batched — independent small factorizations (CFG[4]), one
- * kernel launch.  Matrix b is d_A[b] (DEVICE pointer, d_lda[b] x d_n[b]).
+ * relapack_dpotrf_batched — independent small factorizations (CFG[4]).
+ * Matrix b is d_A[b] (DEVICE pointer, d_lda[b] x d_n[b]).
  *   d_n, d_A, d_lda, d_info  DEVICE arrays of length `batch`
  * Per matrix: info as relapack_dpotrf; n outside [0, RELAPACK_BATCH_NMAX] sets
  * that matrix's info to -2, lda < max(1, n) sets -4; such matrices are skipped.
+ * Work on `stream`: a bucketing kernel, then one kernel per size class
+ * (16/32/48/64) on library streams forked from and joined back into `stream`
+ * (capturable into a CUDA graph).  The bucketing workspace is library-owned
+ * per device (released by relapack_finalize); calls on different streams are
+ * ordered by the library so they never share it concurrently.
  * Returns 0, -1 (bad uplo), -2 (batch < 0) or <= -1000 (CUDA error).
  */
 #define RELAPACK_BATCH_NMAX 64
