@@ -29,6 +29,9 @@ namespace {
 
 constexpr int kPanel = 8;
 
+#ifndef RELAPACK_PANEL_RB
+#define RELAPACK_PANEL_RB 1
+#endif
 #ifndef RELAPACK_NODE_EARLY_STORE
 #define RELAPACK_NODE_EARLY_STORE 0
 #endif
@@ -136,14 +139,15 @@ __device__ __forceinline__ void strip_update(double* s, int n, int j0, int r0, i
 
 // Factor panel [j0, j0 + 8) (rows j0..n-1, already fully updated) in warp 0's
 // registers and store it.  Returns the 1-based failing column or 0.
-template <int NMAX, int LDS>
+template <int NMAX, int LDS, int RB = 0>
 __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) {
-  constexpr int R = P2<NMAX>::RPL;
+  // RB: row blocks of 32 above j0 skipped (rows < 32 RB hold nothing of this panel)
+  constexpr int R = P2<NMAX>::RPL - RB;
   const int w = min(kPanel, n - j0);
   double x[R][kPanel];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int i = lane + 32 * r;
+    const int i = lane + 32 * (r + RB);
 #pragma unroll
     for (int c = 0; c < kPanel; ++c) x[r][c] = (i < n && c < w && i >= j0 + c) ? s[i + (j0 + c) * LDS] : 0.0;
   }
@@ -159,7 +163,7 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
     double own = x[0][0];
 #pragma unroll
     for (int r = 1; r < R; ++r)
-      if ((j0 >> 5) == r) own = x[r][0];
+      if ((j0 >> 5) - RB == r) own = x[r][0];
     dsh = __shfl_sync(0xffffffffu, own, j0 & 31);  // lane (j0 & 31) holds a_{j0,j0}
   }
   // Column c's update of column c+1 is done at once (it feeds the next
@@ -170,7 +174,7 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
     double v = x[0][c];
 #pragma unroll
     for (int r = 1; r < R; ++r)
-      if ((row >> 5) == r) v = x[r][c];
+      if ((row >> 5) - RB == r) v = x[r][c];
     return v;
   };
 #pragma unroll
@@ -208,7 +212,7 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
   // diagonal entries l_jj = sqrt(d), off the critical path
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int i = lane + 32 * r;
+    const int i = lane + 32 * (r + RB);
 #pragma unroll
     for (int c = 0; c < kPanel; ++c) {
       if (i == j0 + c) x[r][c] = sqrt_from_rsqrt(dpiv[c], rpiv[c]);
@@ -240,7 +244,8 @@ __device__ int potf2_smem(double* s, int n, int* fail_flag) {
     if (warp == 0) {
       strip_update<NMAX, LDS>(s, n, j0, r0, g, t);
       __syncwarp();
-      const int f = factor_panel<NMAX, LDS>(s, n, r0, lane);
+      const int f = (RELAPACK_PANEL_RB && NMAX == 64 && r0 >= 32) ? factor_panel<NMAX, LDS, NMAX == 64 ? 1 : 0>(s, n, r0, lane)
+                                                                   : factor_panel<NMAX, LDS>(s, n, r0, lane);
       if (lane == 0 && f) *fail_flag = f;
     } else {
       // tiles of the trailing grid with tk >= 1 (columns >= r0 + 8)
