@@ -1,6 +1,6 @@
 # Round-end style refresh: GPU tests, smoke, every bench config, the reference
 # arm and the ncu launch list of the default step.  Outputs in gpurun_out/$TAG_*.
-TAG=${TAG:-r01l}
+TAG=${TAG:-r01n}
 O=gpurun_out
 python -m pytest tests -m gpu -q > $O/${TAG}_pytest_gpu.txt 2>&1; tail -1 $O/${TAG}_pytest_gpu.txt
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/${TAG}_smoke.txt 2>&1; tail -1 $O/${TAG}_smoke.txt
