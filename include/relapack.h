@@ -227,6 +227,37 @@ RELAPACK_API int relapack_profile_records(int max, double* out);
  */
 RELAPACK_API int relapack_trace_read(int max, double* out);
 
+/*
+ * Kernel test hooks (synchronous; test infrastructure, not a production API).
+ * Each launches ONE kernel of the hot path on caller-provided DEVICE blocks with
+ * the size-rule choices forced, so every instantiation the factorization runs
+ * can be compared with the oracle's BLAS-3 definitions.
+ *
+ * relapack_update_test — K3/K4: C(M x N) += alpha A B^T on
+ *   the tri part of C (0 all, 1 lower i >= j, 2 upper i <= j; M == N if tri).
+ *   Operand X (rows x cols) has element (r, c) at X[r + c*ld] (layout 0) or
+ *   X[c + r*ld] (layout 1); A is M x K, B is N x K, C is M x N.  The
+ *   factorization uses la = lb = lc and alpha = -1 (C -= A B^T).
+ *   tile 0 = size rule, else 32/64/128; ksplit 0 = size rule, 1 = none,
+ *   2..16 = forced deterministic split-K; allow_tma 0 forces the plain-load
+ *   operand path (it is also taken when a base is not 16-byte aligned or an ld
+ *   is odd).  chosen (host, 3 ints, may be NULL) receives (tile, used TMA,
+ *   ksplit).  Returns 0, -1 (bad argument) or <= -1000 (CUDA error).
+ * relapack_trsm_test — K5 (§8a a3 base): B(m x t) := B L^{-T} (L the t x t lower
+ *   L-view block at L, both in `layout`).  variant 0 = the plan's dispatch,
+ *   1 register-slab 32-row CTAs, 2 register-slab 64-row, 3 register-slab 128-row
+ *   (t <= 128), 4 / 5 shared-memory-slab 4 / 8 warps (t <= 256), 6 the
+ *   row-parallel kernel (t <= 64).
+ * relapack_potf2_test — K1 (§8a a2): base-case factorization of the n x n
+ *   (n <= 128) L-view block; *info (host) = the kernel's info.
+ */
+RELAPACK_API int relapack_update_test(int la, int lb, int lc, int tri, int M, int N, int K, double alpha, double* C,
+                                      int64_t ldc, const double* A, int64_t lda, const double* B, int64_t ldb, int tile,
+                                      int ksplit, int allow_tma, relapack_stream_t stream, int* chosen);
+RELAPACK_API int relapack_trsm_test(int layout, int m, int t, const double* L, int64_t ldl, double* B, int64_t ldb,
+                                    int variant, relapack_stream_t stream);
+RELAPACK_API int relapack_potf2_test(int layout, int n, double* A, int64_t lda, int* info, relapack_stream_t stream);
+
 /* Library version string (build id). */
 RELAPACK_API const char* relapack_version(void);
 

@@ -105,6 +105,14 @@ def lib():
         L.relapack_plan_schedule.argtypes = [c_int, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_int64), c_int,
                                              ctypes.POINTER(c_int), ctypes.POINTER(c_int), c_int]
         L.relapack_plan_schedule.restype = c_int
+        i64 = ctypes.c_int64
+        L.relapack_update_test.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_double, c_void_p, i64,
+                                           c_void_p, i64, c_void_p, i64, c_int, c_int, c_int, c_void_p, ip]
+        L.relapack_update_test.restype = c_int
+        L.relapack_trsm_test.argtypes = [c_int, c_int, c_int, c_void_p, i64, c_void_p, i64, c_int, c_void_p]
+        L.relapack_trsm_test.restype = c_int
+        L.relapack_potf2_test.argtypes = [c_int, c_int, c_void_p, i64, ip, c_void_p]
+        L.relapack_potf2_test.restype = c_int
         _lib = L
     return _lib
 
@@ -302,6 +310,76 @@ def dpotrf_dist_loopback(As, uplo: str = "L", nb: int = 512, dist_min: int = 409
     if r != 0:
         raise RelapackError(f"relapack_dpotrf_dist_loopback failed ({r}): {last_error()}")
     return list(infos)
+
+
+def _block_args(X):
+    """(pointer, ld, layout) of a 2-D float64 CUDA tensor with a unit stride:
+    layout 0 when X[r, c] is at ptr + r + c*ld (column-major), 1 when at ptr + c + r*ld."""
+    import torch
+
+    if X.dtype != torch.float64 or X.dim() != 2:
+        raise TypeError("expected a 2-D float64 tensor")
+    rows, cols = X.shape
+    if X.stride(0) == 1 and (cols <= 1 or X.stride(1) >= max(1, rows)):
+        return X.data_ptr(), max(1, X.stride(1) if cols > 1 else rows), 0
+    if X.stride(1) == 1 and (rows <= 1 or X.stride(0) >= max(1, cols)):
+        return X.data_ptr(), max(1, X.stride(0) if rows > 1 else cols), 1
+    raise ValueError("operand needs a unit stride in one dimension")
+
+
+def update_test(C, A, B, alpha: float = -1.0, tri: int = 0, tile: int = 0, ksplit: int = 0, tma: bool = True,
+                stream=None):
+    """Kernel test hook (K3/K4): C += alpha A B^T on the tri part of C (0 all, 1 lower, 2 upper).
+    C: (M, N), A: (M, K), B: (N, K) float64 CUDA tensors, each column- or row-major (its layout).
+    Returns (tile, used_tma, ksplit) the launch used."""
+    import torch
+
+    pc, ldc, lc = _block_args(C)
+    pa, lda, la = _block_args(A)
+    pb, ldb, lb = _block_args(B)
+    M, N = C.shape
+    K = A.shape[1]
+    if A.shape[0] != M or B.shape != (N, K):
+        raise ValueError("shape mismatch")
+    st = stream if stream is not None else torch.cuda.current_stream(C.device)
+    chosen = (ctypes.c_int * 3)()
+    r = lib().relapack_update_test(la, lb, lc, tri, M, N, K, float(alpha), ctypes.c_void_p(pc), ldc,
+                                   ctypes.c_void_p(pa), lda, ctypes.c_void_p(pb), ldb, tile, ksplit, int(tma),
+                                   ctypes.c_void_p(st.cuda_stream), chosen)
+    if r != 0:
+        raise RelapackError(f"relapack_update_test failed ({r}): {last_error()}")
+    return tuple(chosen)
+
+
+def trsm_test(Lblk, B, variant: int = 0, stream=None):
+    """Kernel test hook (K5): B := B L^{-T} with L the lower triangle of the (t, t) block Lblk.
+    Lblk and B must share one layout (column-major: uplo L; row-major: the uplo U L-view)."""
+    import torch
+
+    pl, ldl, ll = _block_args(Lblk)
+    pb, ldb, lb = _block_args(B)
+    if ll != lb:
+        raise ValueError("L and B must have the same layout")
+    m, t = B.shape
+    st = stream if stream is not None else torch.cuda.current_stream(B.device)
+    r = lib().relapack_trsm_test(ll, m, t, ctypes.c_void_p(pl), ldl, ctypes.c_void_p(pb), ldb, variant,
+                                 ctypes.c_void_p(st.cuda_stream))
+    if r != 0:
+        raise RelapackError(f"relapack_trsm_test failed ({r}): {last_error()}")
+
+
+def potf2_test(A, stream=None) -> int:
+    """Kernel test hook (K1): base-case factorization of the (n, n) block (n <= 128); returns info."""
+    import torch
+
+    pa, lda, la = _block_args(A)
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    info = ctypes.c_int(0)
+    r = lib().relapack_potf2_test(la, A.shape[0], ctypes.c_void_p(pa), lda, ctypes.byref(info),
+                                  ctypes.c_void_p(st.cuda_stream))
+    if r != 0:
+        raise RelapackError(f"relapack_potf2_test failed ({r}): {last_error()}")
+    return info.value
 
 
 def split_point(n: int, align: int) -> int:

@@ -21,7 +21,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["update.cu", "potf2.cu", "trsm.cu", "trsm_fused.cu", "batched.cu", "driver.cu", "dist.cu", "plan.cpp"]
+SOURCES = ["update.cu", "potf2.cu", "trsm.cu", "trsm_fused.cu", "batched.cu", "driver.cu", "dist.cu", "hooks.cu", "plan.cpp"]
 
 
 def _digest() -> str:

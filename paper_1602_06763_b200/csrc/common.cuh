@@ -90,9 +90,21 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // (truncation ~ 5e^3/16 < 2^-66; ~1 ulp after rounding): four dependent FP64
 // operations after the MUFU instead of six for two Newton steps — this is on
 // the per-column critical path of every base-case factorization.
+// The MUFU flushes subnormal inputs to zero (.ftz): a positive pivot below
+// 2^-1000 takes the approximation of d * 2^128 scaled back by 2^64 (exact
+// power-of-two scalings) in an out-of-line call behind a branch, so the usual
+// chain only gains a compare that runs beside the MUFU (ptxas if-converts an
+// inline version into predicated ops whose latency the chain would pay).
+static __device__ __noinline__ double rsqrt_approx_tiny(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d * 0x1p+128));
+  return y * 0x1p+64;
+}
+
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  if (d < 0x1p-1000) y = rsqrt_approx_tiny(d);
   const double p = d * y;
   const double e = fma(-p, y, 1.0);
   const double t = fma(0.375, e, 0.5);

@@ -258,26 +258,13 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
       case OP_GEMM:
       case OP_SYRK: {
         UpdateOp& u = dp.upd[i];
-        UpdateArgs& a = u.args;
-        memset(&a, 0, sizeof(a));
-        a.C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
-        a.ldc = ldc;
-        a.layout = layout;
-        a.d_info = d_info;
-        a.K = op.k;
-        a.tri = op.kind == OP_SYRK;
-        a.M = op.kind == OP_SYRK ? op.n : op.m;
-        a.N = op.n;
-        u.tile = update_tile_for(a.M, a.N, a.K, a.tri);
-        a.tiles_m = (a.M + u.tile - 1) / u.tile;
-        a.ntiles = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * ((a.N + u.tile - 1) / u.tile);
-        a.ksplit = 1;
-        a.A = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, dp.send, pad, nc, &lda_);
-        a.lda = lda_;
-        a.B = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, dp.send, pad, nc, &ldb);
-        a.ldb = ldb;
-        u.use_tma = make_operand_map(&u.tmA, a.A, a.lda, layout, a.M, a.K, u.tile) &&
-                    make_operand_map(&u.tmB, a.B, a.ldb, layout, a.N, a.K, u.tile);
+        const bool syrk = op.kind == OP_SYRK;
+        double* C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
+        const double* Ap = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, dp.send, pad, nc, &lda_);
+        const double* Bp = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, dp.send, pad, nc, &ldb);
+        init_update(u, C, ldc, layout, Ap, lda_, layout, Bp, ldb, layout, syrk ? op.n : op.m, op.n, op.k, -1.0,
+                    syrk ? 1 : 0);
+        u.args.d_info = d_info;
         e = launch_update(u, st);
         break;
       }

@@ -200,32 +200,10 @@ cudaError_t launch_set_int(int* p, int v, cudaStream_t st) {
 }
 
 static void fill_update(UpdateOp& u, const PlanOp& op, double* A, int64_t ld, int layout, const int* d_info) {
-  UpdateArgs& a = u.args;
-  memset(&a, 0, sizeof(a));
-  a.C = A + lv_off(layout, op.c_i, op.c_j, ld);
-  a.ldc = ld;
-  a.layout = layout;
-  a.d_info = d_info;
-  a.K = op.k;
-  if (op.kind == OP_SYRK) {
-    a.M = a.N = op.n;
-    a.tri = 1;
-  } else {
-    a.M = op.m;
-    a.N = op.n;
-    a.tri = 0;
-  }
-  u.tile = update_tile_for(a.M, a.N, a.K, a.tri);
-  a.tiles_m = (a.M + u.tile - 1) / u.tile;
-  const int tiles_n = (a.N + u.tile - 1) / u.tile;
-  a.ntiles = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * tiles_n;
-  a.ksplit = 1;
-  a.A = A + lv_off(layout, op.a_i, op.a_j, ld);
-  a.lda = ld;
-  a.B = A + lv_off(layout, op.b_i, op.b_j, ld);
-  a.ldb = ld;
-  u.use_tma = make_operand_map(&u.tmA, a.A, ld, layout, a.M, a.K, u.tile) &&
-              make_operand_map(&u.tmB, a.B, ld, layout, a.N, a.K, u.tile);
+  const bool syrk = op.kind == OP_SYRK;
+  init_update(u, A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, A + lv_off(layout, op.a_i, op.a_j, ld), ld, layout,
+              A + lv_off(layout, op.b_i, op.b_j, ld), ld, layout, syrk ? op.n : op.m, op.n, op.k, -1.0, syrk ? 1 : 0);
+  u.args.d_info = d_info;
 }
 
 // Enable split-K on the plan's small-grid / long-K updates and give each a

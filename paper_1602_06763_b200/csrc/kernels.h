@@ -17,11 +17,13 @@ constexpr int RELAPACK_BATCH_NMAX_ = 64;  // == RELAPACK_BATCH_NMAX in include/r
 
 // ---- K3/K4 update (update.cu) ----
 struct UpdateArgs {
-  double* C;          // L-view block (M x N) to update
+  double* C;          // block (M x N) to update: C += alpha * A B^T
   int64_t ldc;
   int M, N, K;
-  int layout;         // kLayoutN / kLayoutT
-  int tri;            // 1: SYRK, lower-triangular tiles only (M == N, A == B)
+  int layout;         // layout of C: kLayoutN / kLayoutT (element (i,j) at lv_off(layout, i, j, ld))
+  int la, lb;         // layouts of A (M x K) and B (N x K); the factorization uses la = lb = layout
+  double alpha;       // -1 for the factorization's C -= A B^T
+  int tri;            // 1: SYRK, lower-triangular tiles only (M == N); 2: upper triangle
   int tiles_m;
   const int* d_info;  // device info flag: kernels return immediately if != 0
   const double* A;    // fallback (non-TMA) operand pointers, L-view blocks
@@ -47,6 +49,14 @@ struct UpdateOp {
 
 cudaError_t launch_update(const UpdateOp& op, cudaStream_t st);
 bool make_operand_map(CUtensorMap* map, const double* base, int64_t ld, int layout, int rows, int K, int box_rows);
+// Fill an UpdateOp for C(M x N) += alpha * A(M x K) * B(N x K)^T with per-operand
+// layouts (tri 0 full, 1 lower, 2 upper triangle of C).  A C of layout T with
+// mixed operand layouts is rewritten as C^T += alpha * B A^T (layout N, triangle
+// flipped), the form the kernels are instantiated for.  tile <= 0: the size
+// rule update_tile_for; allow_tma = false forces the plain-load operand path.
+// ksplit stays 1 (setup by the caller).
+void init_update(UpdateOp& u, double* C, int64_t ldc, int lc, const double* A, int64_t lda, int la, const double* B,
+                 int64_t ldb, int lb, int M, int N, int K, double alpha, int tri, int tile = 0, bool allow_tma = true);
 int update_tile_for(int M, int N, int K, int tri);
 // Split-K factor for an update of (M, N, K) on `tile` x `tile` CTA tiles (1 = none)
 // and the workspace it needs (doubles) — see update.cu.
@@ -71,6 +81,8 @@ constexpr int kTrsmFusedMax = 256;
 cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,
                               const int* d_info, cudaStream_t st);
 cudaError_t configure_trsm_fused();
+cudaError_t launch_trsm_fused_variant(int v, const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m,
+                                      int t, const int* d_info, cudaStream_t st);
 // TRSM base dispatch (measured, profiles/): the row-parallel K5 for t <= 64 on
 // short panels, the chunked DMMA K5' otherwise.
 inline cudaError_t launch_trsm_any(const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m, int t,

@@ -572,4 +572,19 @@ cudaError_t launch_trsm_fused(const double* L, int64_t ldl, double* B, int64_t l
                         : launch_nw<4>(L, ldl, B, ldb, layout, m, t, d_info, st);
 }
 
+// Test hook dispatch (hooks.cu): 1 reg<4,1>, 2 reg<8,1>, 3 reg<8,2>, 4 smem-slab<4>, 5 smem-slab<8>.
+cudaError_t launch_trsm_fused_variant(int v, const double* L, int64_t ldl, double* B, int64_t ldb, int layout, int m,
+                                      int t, const int* d_info, cudaStream_t st) {
+  if (m <= 0 || t <= 0) return cudaSuccess;
+  if (t > kFTmax || (v <= 3 && t > 2 * kFC)) return cudaErrorInvalidValue;
+  switch (v) {
+    case 1: return launch_reg<4, 1>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    case 2: return launch_reg<8, 1>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    case 3: return launch_reg<8, 2>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    case 4: return launch_nw<4>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    case 5: return launch_nw<8>(L, ldl, B, ldb, layout, m, t, d_info, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace relapack

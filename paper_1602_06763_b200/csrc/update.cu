@@ -23,6 +23,7 @@
 //    same swizzled layout with plain loads, one stage at a time.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -85,6 +86,10 @@ __device__ __forceinline__ int kmap(int s, int t) {
   return LAYOUT == kLayoutN ? 4 * t + s : 4 * s + t;
 }
 
+// Element (i, j) of C belongs to the updated part: every element (tri 0), the
+// lower triangle i >= j (tri 1, SYRK) or the upper triangle i <= j (tri 2).
+__device__ __forceinline__ bool tri_keep(int tri, int i, int j) { return tri == 0 || (tri == 1 ? i >= j : i <= j); }
+
 __device__ __forceinline__ void tri_index(int x, int& ti, int& tj) {
   int r = (int)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
   while ((r + 1) * (r + 2) / 2 <= x) ++r;
@@ -94,10 +99,10 @@ __device__ __forceinline__ void tri_index(int x, int& ti, int& tj) {
 }
 
 // Fallback loader: the whole CTA fills one stage with plain loads (zero outside).
-template <int LAYOUT, int TBM>
+template <int LAYOUT, int TBM, int NTHREADS>
 __device__ __forceinline__ void fill_tile_ldg(uint8_t* tile, const double* X, int64_t ldx, int rows, int r0, int K,
                                               int k0) {
-  for (int e = threadIdx.x; e < TBM * BK; e += Cfg<TBM>::THREADS) {
+  for (int e = threadIdx.x; e < TBM * BK; e += NTHREADS) {
     int r, k;
     if (LAYOUT == kLayoutN) {
       r = e % TBM;
@@ -112,7 +117,7 @@ __device__ __forceinline__ void fill_tile_ldg(uint8_t* tile, const double* X, in
   }
 }
 
-template <int LAYOUT, int TBM>
+template <int LA, int LB, int TBM>
 __device__ __forceinline__ void issue_stage(uint8_t* smem, uint64_t* full, const CUtensorMap* tmA,
                                             const CUtensorMap* tmB, int it, int kt, int m0, int n0) {
   using C = Cfg<TBM>;
@@ -120,33 +125,38 @@ __device__ __forceinline__ void issue_stage(uint8_t* smem, uint64_t* full, const
   uint8_t* sa = smem + s * C::STAGE_BYTES;
   uint8_t* sb = sa + C::TILE_BYTES;
   mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-  if (LAYOUT == kLayoutN) {
+  if (LA == kLayoutN) {
 #pragma unroll
-    for (int b = 0; b < TBM / 16; ++b) {
-      tma_load_2d(sa + b * 2048, tmA, m0 + 16 * b, kt * BK, &full[s]);
-      tma_load_2d(sb + b * 2048, tmB, n0 + 16 * b, kt * BK, &full[s]);
-    }
+    for (int b = 0; b < TBM / 16; ++b) tma_load_2d(sa + b * 2048, tmA, m0 + 16 * b, kt * BK, &full[s]);
   } else {
     tma_load_2d(sa, tmA, kt * BK, m0, &full[s]);
+  }
+  if (LB == kLayoutN) {
+#pragma unroll
+    for (int b = 0; b < TBM / 16; ++b) tma_load_2d(sb + b * 2048, tmB, n0 + 16 * b, kt * BK, &full[s]);
+  } else {
     tma_load_2d(sb, tmB, kt * BK, n0, &full[s]);
   }
 }
 
 // One BK-deep step of the warp tile: 4 MMA k-steps x (MT x NT) DMMA.8x8x4.
-template <int LAYOUT, int TBM>
+// Both fragments use the k-map of A's layout (the k permutation must agree
+// between the two operands); for mixed layouts B's reads are 4-way instead of
+// 2-way bank-conflicted, which DMMA's issue rate hides.
+template <int LA, int LB, int TBM>
 __device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::NT][2], const uint8_t* sa,
                                           const uint8_t* sb, int wm, int wn, int g, int t) {
   using C = Cfg<TBM>;
 #pragma unroll
   for (int ks = 0; ks < BK / 4; ++ks) {
-    const int k = kmap<LAYOUT>(ks, t);
+    const int k = kmap<LA>(ks, t);
     double a[C::MT], b[C::NT];
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
-      a[mt] = *reinterpret_cast<const double*>(sa + tile_off<LAYOUT>(wm * C::WTM + mt * 8 + g, k));
+      a[mt] = *reinterpret_cast<const double*>(sa + tile_off<LA>(wm * C::WTM + mt * 8 + g, k));
 #pragma unroll
     for (int nt = 0; nt < C::NT; ++nt)
-      b[nt] = *reinterpret_cast<const double*>(sb + tile_off<LAYOUT>(wn * C::WTN + nt * 8 + g, k));
+      b[nt] = *reinterpret_cast<const double*>(sb + tile_off<LB>(wn * C::WTN + nt * 8 + g, k));
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
@@ -156,7 +166,7 @@ __device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::
 
 // One work item (tile, split) of the update; the CTA may process several
 // (persistent launch with a capped grid, see launch_tbm).
-template <int LAYOUT, bool USE_TMA, int TBM>
+template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM>
 __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtensorMap& tmB, const UpdateArgs& args,
                                             uint8_t* smem, int work, bool last) {
   using C = Cfg<TBM>;
@@ -166,7 +176,12 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
   const int tile = work % args.ntiles, split = work / args.ntiles;
   int tm, tn;
   if (args.tri) {
-    tri_index(tile, tm, tn);
+    tri_index(tile, tm, tn);  // tm >= tn: lower tile
+    if (args.tri == 2) {      // upper triangle: the transposed tile
+      const int x = tm;
+      tm = tn;
+      tn = x;
+    }
   } else {
     // grouped raster: kGroupM tile rows at a time, so the CTAs resident at
     // once share ~12 A panels and ~12 B panels in L2 instead of streaming all
@@ -226,26 +241,26 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
     __syncthreads();
     if (threadIdx.x == 0)
       for (int it = 0; it < STAGES - 1 && it < KT; ++it)
-        issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, it, kt0 + it, m0, n0);
+        issue_stage<LA, LB, TBM>(smem, full, &tmA, &tmB, it, kt0 + it, m0, n0);
     for (int kt = 0; kt < KT; ++kt) {
       if (threadIdx.x == 0 && kt + STAGES - 1 < KT) {
         if (kt >= 1) mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
-        issue_stage<LAYOUT, TBM>(smem, full, &tmA, &tmB, kt + STAGES - 1, kt0 + kt + STAGES - 1, m0, n0);
+        issue_stage<LA, LB, TBM>(smem, full, &tmA, &tmB, kt + STAGES - 1, kt0 + kt + STAGES - 1, m0, n0);
       }
       const int s = kt % STAGES;
       mbar_wait(&full[s], (kt / STAGES) & 1);
       const uint8_t* sa = smem + s * C::STAGE_BYTES;
-      mma_stage<LAYOUT, TBM>(acc, sa, sa + C::TILE_BYTES, wm, wn, g, t);
+      mma_stage<LA, LB, TBM>(acc, sa, sa + C::TILE_BYTES, wm, wn, g, t);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   } else {
     for (int kt = 0; kt < KT; ++kt) {
       __syncthreads();
-      fill_tile_ldg<LAYOUT, TBM>(smem, args.A, args.lda, args.M, m0, args.K, (kt0 + kt) * BK);
-      fill_tile_ldg<LAYOUT, TBM>(smem + C::TILE_BYTES, args.B, args.ldb, args.N, n0, args.K, (kt0 + kt) * BK);
+      fill_tile_ldg<LA, TBM, C::THREADS>(smem, args.A, args.lda, args.M, m0, args.K, (kt0 + kt) * BK);
+      fill_tile_ldg<LB, TBM, C::THREADS>(smem + C::TILE_BYTES, args.B, args.ldb, args.N, n0, args.K, (kt0 + kt) * BK);
       __syncthreads();
-      mma_stage<LAYOUT, TBM>(acc, smem, smem + C::TILE_BYTES, wm, wn, g, t);
+      mma_stage<LA, LB, TBM>(acc, smem, smem + C::TILE_BYTES, wm, wn, g, t);
     }
   }
 
@@ -323,20 +338,21 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
       for (int q = 0; q < kQ; ++q) {
         const int sg = sbase + s0 + SLOW_STEP * (q0 + q);
         const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
-        v[q] = (sg < slim && (!args.tri || i >= j)) ? Cf[(int64_t)sg * args.ldc] : 0.0;
+        v[q] = (sg < slim && tri_keep(args.tri, i, j)) ? Cf[(int64_t)sg * args.ldc] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         const int sl = s0 + SLOW_STEP * (q0 + q);
         const int sg = sbase + sl;
         const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
-        if (sg < slim && (!args.tri || i >= j)) Cf[(int64_t)sg * args.ldc] = v[q] - sC[sl * C::CPAD + f];
+        // alpha = -1 (the factorization's C -= A B^T) rounds exactly like v - s
+        if (sg < slim && tri_keep(args.tri, i, j)) Cf[(int64_t)sg * args.ldc] = fma(args.alpha, sC[sl * C::CPAD + f], v[q]);
       }
     }
   }
 }
 
-template <int LAYOUT, bool USE_TMA, int TBM>
+template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM>
 __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
     k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args,
              TraceRec* tr) {
@@ -347,38 +363,59 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
   const int nwork = args.ntiles * args.ksplit;
   for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
     if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
-    update_item<LAYOUT, USE_TMA, TBM>(tmA, tmB, args, smem, work, work + (int)gridDim.x >= nwork);
+    update_item<LA, LB, LAYOUT, USE_TMA, TBM>(tmA, tmB, args, smem, work, work + (int)gridDim.x >= nwork);
   }
   trace_end(tr);
 }
 
-template <int LAYOUT, bool USE_TMA, int TBM>
+template <int LA, int LB, int LC, bool USE_TMA, int TBM>
 cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const UpdateArgs& a, int grid, cudaStream_t st) {
-  k_update<LAYOUT, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a, g_launch_trace);
+  k_update<LA, LB, LC, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a, g_launch_trace);
   return cudaGetLastError();
 }
 
+template <int LA, int LB, int LC, int TBM>
+cudaError_t launch_combo(const UpdateOp& op, int grid, cudaStream_t st) {
+  return op.use_tma ? launch_one<LA, LB, LC, true, TBM>(op.tmA, op.tmB, op.args, grid, st)
+                    : launch_one<LA, LB, LC, false, TBM>(op.tmA, op.tmB, op.args, grid, st);
+}
+
+// Operand-layout combinations (la, lb, lc): the factorization's (N,N,N) and
+// (T,T,T), plus the mixed ones of the other recursive operations (trtri,
+// lauum, potrs, getrf), all normalised to lc = N by update_normalize.
 template <int TBM>
 cudaError_t launch_tbm(const UpdateOp& op, cudaStream_t st) {
   const UpdateArgs& a = op.args;
   int grid = a.ntiles * a.ksplit;
   if (op.max_ctas > 0 && grid > op.max_ctas) grid = op.max_ctas;  // persistent, leaves SMs to other streams
-  if (a.layout == kLayoutN)
-    return op.use_tma ? launch_one<kLayoutN, true, TBM>(op.tmA, op.tmB, a, grid, st)
-                      : launch_one<kLayoutN, false, TBM>(op.tmA, op.tmB, a, grid, st);
-  return op.use_tma ? launch_one<kLayoutT, true, TBM>(op.tmA, op.tmB, a, grid, st)
-                    : launch_one<kLayoutT, false, TBM>(op.tmA, op.tmB, a, grid, st);
+  const int combo = a.la * 4 + a.lb * 2 + a.layout;
+  switch (combo) {
+    case 0: return launch_combo<kLayoutN, kLayoutN, kLayoutN, TBM>(op, grid, st);
+    case 7: return launch_combo<kLayoutT, kLayoutT, kLayoutT, TBM>(op, grid, st);
+    case 2: return launch_combo<kLayoutN, kLayoutT, kLayoutN, TBM>(op, grid, st);
+    case 4: return launch_combo<kLayoutT, kLayoutN, kLayoutN, TBM>(op, grid, st);
+    case 6: return launch_combo<kLayoutT, kLayoutT, kLayoutN, TBM>(op, grid, st);
+    default: return cudaErrorInvalidValue;  // lc = T with mixed operands: normalise first
+  }
+}
+
+template <int LA, int LB, int LC, int TBM>
+cudaError_t configure_combo() {
+  cudaError_t e;
+  const int sm = Cfg<TBM>::SMEM_BYTES;
+  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if ((e = cudaFuncSetAttribute(k_update<LA, LB, LC, true, TBM>, attr, sm)) != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_update<LA, LB, LC, false, TBM>, attr, sm);
 }
 
 template <int TBM>
 cudaError_t configure_tbm() {
   cudaError_t e;
-  const int sm = Cfg<TBM>::SMEM_BYTES;
-  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_update<kLayoutN, true, TBM>, attr, sm)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_update<kLayoutN, false, TBM>, attr, sm)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_update<kLayoutT, true, TBM>, attr, sm)) != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_update<kLayoutT, false, TBM>, attr, sm);
+  if ((e = configure_combo<kLayoutN, kLayoutN, kLayoutN, TBM>()) != cudaSuccess) return e;
+  if ((e = configure_combo<kLayoutT, kLayoutT, kLayoutT, TBM>()) != cudaSuccess) return e;
+  if ((e = configure_combo<kLayoutN, kLayoutT, kLayoutN, TBM>()) != cudaSuccess) return e;
+  if ((e = configure_combo<kLayoutT, kLayoutN, kLayoutN, TBM>()) != cudaSuccess) return e;
+  return configure_combo<kLayoutT, kLayoutT, kLayoutN, TBM>();
 }
 
 }  // namespace
@@ -509,6 +546,51 @@ int update_ksplit_for(int M, int N, int K, int tri, int tile, bool chain) {
 
 int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit) {
   return ksplit > 1 ? (int64_t)ksplit * ntiles_of(M, N, tri, tile) * tile * tile : 0;
+}
+
+void init_update(UpdateOp& u, double* C, int64_t ldc, int lc, const double* A, int64_t lda, int la, const double* B,
+                 int64_t ldb, int lb, int M, int N, int K, double alpha, int tri, int tile, bool allow_tma) {
+  if (lc == kLayoutT && !(la == kLayoutT && lb == kLayoutT)) {
+    // C^T (layout N) += alpha * B A^T
+    const double* X = A;
+    A = B;
+    B = X;
+    const int64_t lx = lda;
+    lda = ldb;
+    ldb = lx;
+    const int l = la;
+    la = lb;
+    lb = l;
+    const int m = M;
+    M = N;
+    N = m;
+    tri = tri == 1 ? 2 : tri == 2 ? 1 : 0;
+    lc = kLayoutN;
+  }
+  UpdateArgs& a = u.args;
+  memset(&a, 0, sizeof(a));
+  a.C = C;
+  a.ldc = ldc;
+  a.layout = lc;
+  a.la = la;
+  a.lb = lb;
+  a.alpha = alpha;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.tri = tri;
+  a.A = A;
+  a.lda = lda;
+  a.B = B;
+  a.ldb = ldb;
+  a.ksplit = 1;
+  u.tile = tile > 0 ? tile : update_tile_for(M, N, K, tri != 0);
+  a.tiles_m = (M + u.tile - 1) / u.tile;
+  const int tiles_n = (N + u.tile - 1) / u.tile;
+  a.ntiles = tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * tiles_n;
+  u.max_ctas = 0;
+  u.use_tma = allow_tma && make_operand_map(&u.tmA, A, lda, la, M, K, u.tile) &&
+              make_operand_map(&u.tmB, B, ldb, lb, N, K, u.tile);
 }
 
 cudaError_t configure_update() {

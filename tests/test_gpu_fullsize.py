@@ -2,6 +2,8 @@
 times (captured graph, default knobs, the same seeded generator).
 
 * CFG[1] n = 4096 L: the whole factor against the oracle, element by element.
+* n = 8192 L and U, CFG[2] n = 16384 U: the whole factor against the oracle
+  (the launches on 128-tiles, the bulk of the bench's time, included).
 * CFG[2] n = 16384 U and CFG[3] n = 65536 L: the oracle computes a bounded
   sample one column at a time — its first J columns (the same left-looking
   loop; exact for those columns, it never reads later ones) — and properties
@@ -76,6 +78,53 @@ def test_cfg1_n4096_full():
     print(f"\nCFG[1] n=4096 L: full floored rel err {e:.3e} (tol {TOL}), backward error {be:.4f} (<= 10)")
     assert e <= TOL
     assert be <= 10.0
+
+
+def _full_compare(n, uplo, dist, seed=1):
+    """Whole factor against the oracle, element by element (the oracle runs the
+    full left-looking loop on the host cores: ~12 s at n = 8192, ~100 s at
+    n = 16384 on 16 cores)."""
+    P = gen.spd_torch(n, seed, dist=dist)
+    W, info = _factor(P, uplo)
+    assert info == 0
+    A = np.asfortranarray(P.cpu().numpy().T)  # symmetric: same bits either way
+    diag = np.diag(A).copy()
+    rinfo = oracle.dpotrf(A, uplo)  # in place: A becomes the oracle's factor
+    assert rinfo == 0
+    G = W.cpu().numpy()
+    # floored relative error (R8) over the uplo triangle, in row panels
+    worst = 0.0
+    for r0 in range(0, n, 2048):
+        r1 = min(n, r0 + 2048)
+        if uplo == "L":
+            g, o = G[r0:r1, :r1], A[r0:r1, :r1]
+        else:  # L-view rows r0..r1 = memory columns r0..r1
+            g, o = G[:r1, r0:r1].T, A[:r1, r0:r1].T
+        mask = np.tril(np.ones((r1 - r0, r1), bool), r0)
+        floor = 1e-4 * np.sqrt(diag[r0:r1])[:, None]
+        err = np.abs(g - o) / np.maximum(np.abs(o), floor)
+        worst = max(worst, float(np.max(err[mask])))
+    del A, G
+    L = _lview(W, uplo)
+    be = _backward_error(P, L)
+    print(f"\nn={n} {uplo} ({dist}): whole factor vs oracle floored rel err {worst:.3e} (tol {TOL}), "
+          f"backward error {be:.4f}")
+    assert worst <= TOL
+    assert be <= 10.0
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_n8192_full(uplo):
+    """n = 8192: the plan's top SYRK/GEMMs run on 128-tiles (k_update<*,TMA,128>), split-K 64-tiles below."""
+    _full_compare(8192, uplo, "uniform", seed=2)
+
+
+def test_cfg2_n16384_U_full():
+    """CFG[2] (the bench workload, same seed and generator) against the whole oracle factor."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3 * 16384 * 16384 * 8:
+        pytest.skip("needs 6 GiB of device memory")
+    _full_compare(16384, "U", "normal", seed=1)
 
 
 @pytest.mark.parametrize("n,uplo,dist,J", [(16384, "U", "normal", 256), (65536, "L", "uniform", 128)])

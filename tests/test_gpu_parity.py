@@ -449,3 +449,43 @@ def test_node128_info(k):
     finally:
         rl.set_crossover(old)
     assert info == rinfo == k + 1
+
+
+# ---------------------------------------------------------------- extreme exponents
+@pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("n", [100, 300, 1031])
+@pytest.mark.parametrize("e2", [1000, -1000])
+def test_scaled_inputs(n, uplo, e2):
+    """A * 2^e2 (exact scaling): entries near 2^1010 / 2^-990, pivots and factors
+    far from 1.  Compared after scaling back by 2^(-e2/2) (exact), so the norms
+    of the metric stay finite."""
+    A0 = gen.spd(n, 11)
+    A = np.asfortranarray(A0 * 2.0 ** e2)
+    G, info, R, rinfo = run_both(A, uplo)
+    assert info == rinfo == 0
+    s = 2.0 ** (-e2 // 2)
+    Lg, Lo = lower_of(G[:n], uplo) * s, lower_of(R[:n], uplo) * s
+    assert np.isfinite(Lg).all()
+    err = floored_rel_err(Lg, Lo, A0)
+    assert err <= TOL, f"scaled 2^{e2} n={n} {uplo}: {err:.3e}"
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("n,k", [(1, 0), (2, 1), (64, 40), (128, 127), (300, 200), (1031, 700)])
+def test_subnormal_pivot(n, k, uplo):
+    """A positive subnormal pivot (d = 2^-1060 > 0: only !(d > 0)
+    fails): blockdiag(SPD, [2^-1060], SPD) -> l_kk = 2^-530 exactly (the MUFU's
+    flush-to-zero input is rescaled, common.cuh rsqrt_nr)."""
+    A = np.asfortranarray(gen.spd(n, 5))
+    A[k, :] = 0.0
+    A[:, k] = 0.0
+    A[k, k] = 2.0 ** -1060
+    G, info, R, rinfo = run_both(A, uplo)
+    assert info == rinfo == 0
+    Lg, Lo = lower_of(G[:n], uplo), lower_of(R[:n], uplo)
+    assert Lo[k, k] == 2.0 ** -530
+    assert Lg[k, k] == 2.0 ** -530
+    assert np.isfinite(Lg).all()
+    floor = np.maximum(1e-4 * np.sqrt(np.diag(A)), 1e-300)[:, None]
+    err = float(np.max(np.tril(np.abs(Lg - Lo) / np.maximum(np.abs(Lo), floor))))
+    assert err <= TOL, err
