@@ -37,8 +37,9 @@
  *
  * Threading / streams.  Entry points are reentrant; the per-device plan
  * cache (captured CUDA graphs) is mutex-guarded.  Work is ordered on the
- * stream set by relapack_set_stream (default: the legacy default stream) or
- * passed explicitly to the _async / _batched variants.
+ * stream set by relapack_set_stream — a per-thread setting (default: the
+ * legacy default stream), so concurrent threads never redirect each other's
+ * calls — or passed explicitly to the _async / _batched variants.
  *
  * Ownership.  The caller owns every matrix buffer; the library never frees
  * caller memory.  The library owns per-device workspace (info scalars,
@@ -72,8 +73,11 @@ typedef void* relapack_stream_t;
  *   A     in/out  DEVICE or HOST pointer to the lda x n column-major matrix.
  *               Device memory (cudaMalloc / PyTorch storage) is factored in
  *               place.  Host memory (pageable or pinned) is staged through a
- *               library-owned device buffer: the uplo triangle is copied in,
- *               factored on the GPU, and only the uplo triangle is copied back.
+ *               library-owned device buffer: the uplo triangle is copied in
+ *               (whole diagonal blocks, whose other-triangle values are never
+ *               used), factored on the GPU, and only the uplo triangle is
+ *               written back (diagonal blocks masked), so the other strict
+ *               triangle of the caller's matrix is never written.
  *   lda   in   leading dimension, lda >= max(1, n)
  *   info  out  host int, see "Errors" above
  * Returns after the factorization completed (stream synchronised).
@@ -98,10 +102,14 @@ RELAPACK_API int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int
  * Per matrix: info as relapack_dpotrf; n outside [0, RELAPACK_BATCH_NMAX] sets
  * that matrix's info to -2, lda < max(1, n) sets -4; such matrices are skipped.
  * Work on `stream`: a bucketing kernel, then one kernel per size class
- * (16/32/48/64) on library streams forked from and joined back into `stream`
- * (capturable into a CUDA graph).  The bucketing workspace is library-owned
- * per device (released by relapack_finalize); calls on different streams are
- * ordered by the library so they never share it concurrently.
+ * (16/32/48/64) on library streams forked from and joined back into `stream`.
+ * Eager calls use a library-owned bucketing workspace per device (released by
+ * relapack_finalize); calls on different streams are ordered by the library
+ * (an event after each call) so they never share it concurrently.  The call
+ * is capturable into a CUDA graph: inside a capture the workspace is a
+ * graph-owned allocation (cudaMallocAsync / cudaFreeAsync nodes of the
+ * captured graph), so replays are independent of later eager calls and of
+ * each other's workspace.
  * Returns 0, -1 (bad uplo), -2 (batch < 0) or <= -1000 (CUDA error).
  */
 #define RELAPACK_BATCH_NMAX 64

@@ -373,32 +373,44 @@ cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* 
   BatchWs& w = g_bws[dev];
   std::lock_guard<std::mutex> lk(w.mu);
   if (w.sms == 0 && (e = cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((size_t)batch > w.cap) {
-    if (w.buf) {
-      if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
-      cudaFree(w.buf);
-      w.buf = nullptr;
-      w.cap = 0;
-    }
-    if ((e = cudaMalloc(&w.buf, sizeof(int) * (kClasses + (size_t)kClasses * batch))) != cudaSuccess) return e;
-    w.cap = (size_t)batch;
-  }
-  // the lists are indexed with stride `batch` of this call
-  int* counts = w.buf;
-  int* lists = w.buf + kClasses;
-  if (!w.done && (e = cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming)) != cudaSuccess) return e;
   cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
   if ((e = cudaStreamIsCapturing(st, &capturing)) != cudaSuccess) return e;
-  // the previous call (any stream) has finished with the workspace; inside a
-  // graph capture the graph's own edges order the calls instead
-  if (capturing == cudaStreamCaptureStatusNone && (e = cudaStreamWaitEvent(st, w.done, 0)) != cudaSuccess) return e;
+  const bool in_capture = capturing != cudaStreamCaptureStatusNone;
+  const size_t ws_bytes = sizeof(int) * (kClasses + (size_t)kClasses * batch);
+  int* ws = nullptr;
+  if (in_capture) {
+    // inside a graph capture the workspace belongs to the graph (an allocation
+    // node freed by the graph's own free node): a replay never touches library
+    // memory that a later eager call may regrow or another replay may share
+    if ((e = cudaMallocAsync(&ws, ws_bytes, st)) != cudaSuccess) return e;
+  } else {
+    if ((size_t)batch > w.cap) {
+      if (w.buf) {
+        if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+        cudaFree(w.buf);
+        w.buf = nullptr;
+        w.cap = 0;
+      }
+      if ((e = cudaMalloc(&w.buf, ws_bytes)) != cudaSuccess) return e;
+      w.cap = (size_t)batch;
+    }
+    ws = w.buf;
+  }
+  // the lists are indexed with stride `batch` of this call
+  int* counts = ws;
+  int* lists = ws + kClasses;
+  if (!w.done && (e = cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+  // eager calls: the previous eager call (any stream) has finished with the
+  // library workspace before this one overwrites it
+  if (!in_capture && (e = cudaStreamWaitEvent(st, w.done, 0)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(counts, 0, kClasses * sizeof(int), st)) != cudaSuccess) return e;
   k_bucket<<<(batch + 255) / 256, 256, 0, st>>>(batch, d_n, d_lda, d_info, counts, lists);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (!batch_streams()) {
     e = layout == kLayoutN ? launch_classes<kLayoutN>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st)
                            : launch_classes<kLayoutT>(batch, counts, lists, d_A, d_n, d_lda, d_info, dev, w.sms, st);
-    return e != cudaSuccess || capturing != cudaStreamCaptureStatusNone ? e : cudaEventRecord(w.done, st);
+    if (e != cudaSuccess) return e;
+    return in_capture ? cudaFreeAsync(ws, st) : cudaEventRecord(w.done, st);
   }
   if (!w.fork) {
     if ((e = cudaEventCreateWithFlags(&w.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -426,7 +438,7 @@ cudaError_t launch_potf2_batched(int layout, int batch, const int* d_n, double* 
     if ((e = cudaStreamWaitEvent(st, w.join[c], 0)) != cudaSuccess) return e;
   }
   // (not inside a capture: an event recorded there cannot be waited on later)
-  return capturing != cudaStreamCaptureStatusNone ? cudaSuccess : cudaEventRecord(w.done, st);
+  return in_capture ? cudaFreeAsync(ws, st) : cudaEventRecord(w.done, st);
 }
 
 void release_batched_workspace() {

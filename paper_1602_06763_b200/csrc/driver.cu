@@ -48,7 +48,11 @@ thread_local TraceRec* g_launch_trace = nullptr;
 
 // ------------------------------------------------------------------ knobs
 static std::atomic<int> g_crossover{-1}, g_split_tile{-1}, g_graphs{-1};
-static std::atomic<uintptr_t> g_stream{0};
+// relapack_set_stream is per calling thread: a thread's set_stream + call pair
+// is never redirected by another thread's set_stream (the Python binding calls
+// them back to back, releasing the GIL in between)
+static thread_local cudaStream_t g_stream = nullptr;
+static thread_local int g_stream_set = 0;
 
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -56,11 +60,7 @@ static int env_int(const char* name, int dflt) {
   return atoi(v);
 }
 
-static std::atomic<int> g_stream_set{0};
-
-cudaStream_t current_stream_or(cudaStream_t fallback) {
-  return g_stream_set.load() ? reinterpret_cast<cudaStream_t>(g_stream.load()) : fallback;
-}
+cudaStream_t current_stream_or(cudaStream_t fallback) { return g_stream_set ? g_stream : fallback; }
 
 // Column width of the TRSM base case (RELAPACK_TRSM_BASE, 64 .. kTrsmFusedMax;
 // default 128: the whole L of the base fits shared memory next to the row
@@ -112,7 +112,7 @@ static int pdl_mode() { return env_int("RELAPACK_PDL", 3); }
 // last-CTA end (tools/trace_timeline.py reads them with relapack_trace_read).
 static bool trace_enabled() { return env_int("RELAPACK_TRACE", 0) != 0; }
 static std::mutex g_trace_mu;
-static const void* g_trace_plan = nullptr;  // the Plan whose trace relapack_trace_read returns
+static const void* g_trace_plan = nullptr;  // the Plan whose trace relapack_trace_read returns (cleared when it dies)
 
 static bool graphs_enabled() {
   int g = g_graphs.load();
@@ -141,6 +141,10 @@ struct Plan {
   int* splitk_cnt = nullptr;    // per-tile arrival counters (self-resetting; zeroed at every run start)
   size_t cnt_bytes = 0;
   ~Plan() {
+    {
+      std::lock_guard<std::mutex> tl(g_trace_mu);
+      if (g_trace_plan == this) g_trace_plan = nullptr;
+    }
     if (exec) cudaGraphExecDestroy(exec);
     if (d_trace) cudaFree(d_trace);
     for (cudaEvent_t e : ev)
@@ -150,7 +154,9 @@ struct Plan {
   }
 };
 
-using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, int, int, int, int, uintptr_t, int64_t>;
+// (A, n, ld, layout, d_info, host, hld, knob signature): every knob that shapes
+// the plan, its launches or the capture is part of the key (knob_signature)
+using PlanKey = std::tuple<uintptr_t, int, int64_t, int, uintptr_t, uintptr_t, int64_t, std::string>;
 
 struct DeviceState {
   std::mutex mu;          // guards the plan cache
@@ -160,6 +166,7 @@ struct DeviceState {
   int* d_info = nullptr;  // library-owned info scalar for the synchronous API
   int* h_info = nullptr;  // pinned
   double* stage = nullptr;  // staging buffer for host matrices
+  double* bounce = nullptr;  // pinned 256 x 256 bounce for the pageable path's diagonal blocks
   size_t stage_elems = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // split-copy streams (one per link direction)
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
@@ -281,9 +288,12 @@ __global__ void k_noop() {}
 // 2-D copy dst[c * dld + r] = src[c * sld + r], r < w (contiguous), c < h; one
 // of the two is pinned host memory addressed through UVA.  16-byte accesses
 // when both sides allow them, many loads in flight per thread.
+// tri (scalar path only): 0 every element, 1 only r >= c, 2 only r <= c (r < w
+// the contiguous index, c < h the strided one): the uplo triangle of a
+// diagonal block, so nothing outside it is written.
 __global__ void __launch_bounds__(256) k_copy2d(double* __restrict__ dst, int64_t dld,
                                                 const double* __restrict__ src, int64_t sld, int64_t w, int64_t h,
-                                                int vec) {
+                                                int vec, int tri) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (vec) {
     const int64_t w2 = w / 2, tot = w2 * h;
@@ -312,20 +322,21 @@ __global__ void __launch_bounds__(256) k_copy2d(double* __restrict__ dst, int64_
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t e = e0 + u * stride;
-        if (e < tot) dst[(e / w) * dld + e % w] = v[u];
+        const int64_t r = e % w, c = e / w;
+        if (e < tot && (tri == 0 || (tri == 1 ? r >= c : r <= c))) dst[c * dld + r] = v[u];
       }
     }
   }
 }
 
 static cudaError_t launch_copy2d(double* dst, int64_t dld, const double* src, int64_t sld, int64_t w, int64_t h,
-                                 cudaStream_t st) {
-  const bool vec = (w % 2 == 0) && (dld % 2 == 0) && (sld % 2 == 0) &&
+                                 cudaStream_t st, int tri = 0) {
+  const bool vec = tri == 0 && (w % 2 == 0) && (dld % 2 == 0) && (sld % 2 == 0) &&
                    ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
   const int64_t items = vec ? (w / 2) * h : w * h;
   int grid = (int)((items + 256 * 4 - 1) / (256 * 4));
   grid = grid < 8 ? (grid < 1 ? 1 : grid) : 8;  // 8 CTAs keep ~32 KB of PCIe requests in flight
-  k_copy2d<<<grid, 256, 0, st>>>(dst, dld, src, sld, w, h, vec ? 1 : 0);
+  k_copy2d<<<grid, 256, 0, st>>>(dst, dld, src, sld, w, h, vec ? 1 : 0, tri);
   return cudaGetLastError();
 }
 
@@ -360,6 +371,13 @@ static cudaError_t copy_block(const Plan& pl, size_t i, double* A, int64_t ld, i
   const size_t height = layout == kLayoutN ? op.k : op.m;
   double* dev = A + lv_off(layout, op.c_i, op.c_j, ld);
   double* host = const_cast<double*>(pl.host) + lv_off(layout, op.c_i, op.c_j, pl.hld);
+  if (op.kind == OP_D2H && op.c_i == op.c_j) {
+    // a diagonal block goes back masked to the uplo triangle (SM copy into
+    // the pinned host matrix through UVA): the other triangle of the caller's
+    // matrix is never written
+    return launch_copy2d(host, pl.hld, dev, ld, (int64_t)(width / sizeof(double)), (int64_t)height, st,
+                         layout == kLayoutN ? 1 : 2);
+  }
   if (copy_kernels()) {
     const int64_t w = (int64_t)(width / sizeof(double)), h = (int64_t)height;
     return op.kind == OP_H2D ? launch_copy2d(dev, ld, host, pl.hld, w, h, st)
@@ -572,6 +590,23 @@ static int copy_rows(int n) {
   return n / 8 < 512 ? 512 : (n / 8 > 2048 ? 2048 : n / 8);
 }
 
+// Every knob the executor reads while building, launching or capturing a plan,
+// as one string (part of the plan-cache key, so changing any of them inside a
+// process never replays a stale graph).  The update kernel's tile / split-K
+// environment knobs are read once per process (update.cu) and are not here.
+static std::string knob_signature(const PlanParams& pp, bool use_graph, bool use_dag) {
+  char b[512];
+  snprintf(b, sizeof(b),
+           "c%d T%d tb%d la%d tr%d ld%d db%d bc%d hg%d g%d d%d bulk%d bmin%g upd%d dl%d sk%d pdl%d tr%d pm%d sc%d ck%d "
+           "cp%d cr%d skip%d",
+           pp.crossover, pp.split_tile, pp.trsm_base, (int)pp.lookahead, pp.trsm_rows, pp.lookahead_depth,
+           (int)pp.defer_b21, pp.b21_chunks, pp.host_gemm_cols, (int)use_graph, (int)use_dag, bulk_ctas(),
+           bulk_min_flops(), upd_ctas(), (int)defer_low_priority(), (int)splitk_enabled(), pdl_mode(),
+           (int)trace_enabled(), env_int("RELAPACK_PRIO_MODE", 1), (int)split_copies_enabled(), (int)copy_kernels(),
+           copy_panel(), env_int("RELAPACK_COPY_ROWS", 0), debug_skip_mask());
+  return b;
+}
+
 // Enqueue the factorization of the device matrix A (already validated).
 int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st, const double* host,
                   int64_t hld) {
@@ -592,11 +627,9 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const bool use_dag = use_graph && dag_enabled();
   const int bulk = bulk_ctas();
   const int upd_cap = upd_ctas();
-  PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info), pp.crossover,
-              pp.split_tile, (use_graph ? 1 : 0) | (use_dag ? 2 : 0) | (pp.lookahead ? 4 : 0) | (pp.trsm_rows << 3) | (pp.lookahead_depth << 24) | (pp.defer_b21 ? 0 : (1 << 27)) | (pp.b21_chunks << 20) |
-                  (trace_enabled() ? (1 << 30) : 0) | (defer_low_priority() ? 0 : (1 << 29)) |
-                  (split_copies_enabled() ? (1 << 28) : 0), bulk * 1024 + upd_cap,
-              reinterpret_cast<uintptr_t>(host), hld};
+  (void)bulk;
+  PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info),
+              reinterpret_cast<uintptr_t>(host), hld, knob_signature(pp, use_graph, use_dag)};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
   if (it != ds->index.end()) {
@@ -798,29 +831,56 @@ static bool is_pinned_host(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
-// Copy the uplo triangle between a host matrix (ld_h) and a device matrix
-// (ld_d) in column panels: only the triangle (plus the diagonal blocks of the
-// panels) crosses PCIe.
+// Copy the uplo triangle between a pageable host matrix and a device matrix in
+// column panels of w columns.  Host -> device: each panel's rows from its
+// diagonal block on (the diagonal block whole; the other-triangle values it
+// carries into the staging buffer are never used).  Device -> host: the part
+// of the panel outside its diagonal block as one 2-D copy, the diagonal block
+// through a pinned bounce buffer and per-column host copies of its uplo part
+// only, so nothing outside the triangle is written in the caller's matrix.
 static cudaError_t copy_triangle(double* dst, int64_t ld_dst, const double* src, int64_t ld_src, int n, int layout,
-                                 cudaMemcpyKind kind, cudaStream_t st) {
+                                 cudaMemcpyKind kind, cudaStream_t st, double* bounce = nullptr) {
   const int w = 256;
   for (int j0 = 0; j0 < n; j0 += w) {
     const int jw = (n - j0 < w) ? n - j0 : w;
-    int64_t r0, rows;
-    if (layout == kLayoutN) {  // lower: memory column j holds rows j..n-1
-      r0 = j0;
-      rows = n - j0;
-    } else {  // upper: memory column j holds rows 0..j
-      r0 = 0;
-      rows = j0 + jw;
+    // memory rows of the panel's triangle part: [r0, r0 + rows)
+    const int64_t r0 = layout == kLayoutN ? j0 : 0;
+    const int64_t rows = layout == kLayoutN ? n - j0 : j0 + jw;
+    cudaError_t e;
+    if (kind == cudaMemcpyHostToDevice || !bounce) {
+      e = cudaMemcpy2DAsync(dst + r0 + (int64_t)j0 * ld_dst, ld_dst * sizeof(double), src + r0 + (int64_t)j0 * ld_src,
+                            ld_src * sizeof(double), rows * sizeof(double), jw, kind, st);
+      if (e != cudaSuccess) return e;
+      continue;
     }
-    cudaError_t e = cudaMemcpy2DAsync(dst + r0 + (int64_t)j0 * ld_dst, ld_dst * sizeof(double),
-                                      src + r0 + (int64_t)j0 * ld_src, ld_src * sizeof(double),
-                                      rows * sizeof(double), jw, kind, st);
-    if (e != cudaSuccess) return e;
+    // the rectangle outside the diagonal block: below it (L) / above it (U)
+    const int64_t q0 = layout == kLayoutN ? j0 + jw : 0;
+    const int64_t qn = layout == kLayoutN ? n - (j0 + jw) : j0;
+    if (qn > 0 && (e = cudaMemcpy2DAsync(dst + q0 + (int64_t)j0 * ld_dst, ld_dst * sizeof(double),
+                                         src + q0 + (int64_t)j0 * ld_src, ld_src * sizeof(double),
+                                         qn * sizeof(double), jw, kind, st)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemcpy2DAsync(bounce, jw * sizeof(double), src + j0 + (int64_t)j0 * ld_src, ld_src * sizeof(double),
+                               jw * sizeof(double), jw, kind, st)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    for (int c = 0; c < jw; ++c) {
+      const int a = layout == kLayoutN ? c : 0, b = layout == kLayoutN ? jw : c + 1;  // rows [a, b) of column c
+      memcpy(dst + (j0 + a) + (int64_t)(j0 + c) * ld_dst, bounce + a + (int64_t)c * jw, (b - a) * sizeof(double));
+    }
   }
   return cudaSuccess;
 }
+
+// Restores the calling thread's current device on every return path.
+struct DeviceGuard {
+  int saved = -1;
+  DeviceGuard() { cudaGetDevice(&saved); }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (saved >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != saved) cudaSetDevice(saved);
+  }
+};
 
 }  // namespace relapack
 
@@ -845,12 +905,12 @@ void relapack_dpotrf(const char* uplo, const int* n_, double* A, const int* lda_
     *info = 0;
     return;
   }
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(g_stream.load());
+  cudaStream_t st = g_stream;
   int dev = 0;
   const bool on_device = is_device_pointer(A, &dev);
   cudaError_t e;
-  int cur = 0;
-  cudaGetDevice(&cur);
+  DeviceGuard guard;
+  const int cur = guard.saved;
   if (on_device && dev != cur) {
     if ((e = cudaSetDevice(dev)) != cudaSuccess) {
       *info = cuda_fail(e, "set device");
@@ -901,7 +961,11 @@ void relapack_dpotrf(const char* uplo, const int* n_, double* A, const int* lda_
     return;
   }
   if (!on_device && !pinned) {
-    if ((e = copy_triangle(A, lda, dA, ld, n, layout, cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
+    if (!ds->bounce && (e = cudaHostAlloc(&ds->bounce, 256 * 256 * sizeof(double), cudaHostAllocDefault)) != cudaSuccess) {
+      *info = cuda_fail(e, "bounce buffer");
+      return;
+    }
+    if ((e = copy_triangle(A, lda, dA, ld, n, layout, cudaMemcpyDeviceToHost, st, ds->bounce)) != cudaSuccess) {
       *info = cuda_fail(e, "D2H");
       return;
     }
@@ -912,7 +976,6 @@ void relapack_dpotrf(const char* uplo, const int* n_, double* A, const int* lda_
     return;
   }
   *info = *ds->h_info;
-  if (on_device && dev != cur) cudaSetDevice(cur);
 }
 
 int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int* d_info, relapack_stream_t stream) {
@@ -930,12 +993,9 @@ int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int* d_info, rel
     cudaError_t e = cudaMemsetAsync(d_info, 0, sizeof(int), st);
     return e == cudaSuccess ? 0 : cuda_fail(e, "memset info");
   }
-  int cur = 0;
-  cudaGetDevice(&cur);
-  if (dev != cur) cudaSetDevice(dev);
-  int r = enqueue_potrf(dev, A, n, lda, layout, d_info, st);
-  if (dev != cur) cudaSetDevice(cur);
-  return r;
+  DeviceGuard guard;
+  if (dev != guard.saved) cudaSetDevice(dev);
+  return enqueue_potrf(dev, A, n, lda, layout, d_info, st);
 }
 
 int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const* d_A, const int* d_lda, int* d_info,
@@ -954,8 +1014,8 @@ int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const*
 }
 
 void relapack_set_stream(relapack_stream_t stream) {
-  g_stream.store(reinterpret_cast<uintptr_t>(stream));
-  g_stream_set.store(1);
+  g_stream = reinterpret_cast<cudaStream_t>(stream);
+  g_stream_set = 1;
 }
 
 const char* relapack_last_error(void) {
@@ -981,6 +1041,7 @@ void relapack_finalize(void) {
       if (ds->stage) cudaFree(ds->stage);
       if (ds->d_info) cudaFree(ds->d_info);
       if (ds->h_info) cudaFreeHost(ds->h_info);
+      if (ds->bounce) cudaFreeHost(ds->bounce);
       if (ds->capture) cudaStreamDestroy(ds->capture);
       if (ds->h2d) cudaStreamDestroy(ds->h2d);
       if (ds->d2h) cudaStreamDestroy(ds->d2h);

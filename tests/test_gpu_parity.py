@@ -325,6 +325,68 @@ def test_batched_graph_capture():
         _batched_check(b, buf, infos)
 
 
+def test_batched_graph_replay_after_regrow():
+    """a graph captured with no library workspace in place, an eager
+    call that (re)grows the library workspace, then replays of the graph
+    concurrent with eager calls on another stream — the replay owns its own
+    (graph-allocated) workspace, so all results stay right."""
+    rl.finalize()  # no library workspace exists: the capture must not allocate one
+    b, buf, ptrs, ns, ldas, infos = _batched_case(1500, 31)
+    pristine = buf.clone()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rl.dpotrf_batched(ns, ptrs, ldas, infos, "L", stream=s)
+    big = _batched_case(6000, 32)  # eager: grows the library workspace
+    assert rl.dpotrf_batched(big[3], big[2], big[4], big[5], "L") == 0
+    torch.cuda.synchronize()
+    _batched_check(big[0], big[1], big[5])
+    other = _batched_case(5000, 33)
+    s2 = torch.cuda.Stream()
+    for _ in range(3):
+        buf.copy_(pristine)
+        infos.fill_(-99)
+        torch.cuda.synchronize()
+        g.replay()
+        with torch.cuda.stream(s2):
+            assert rl.dpotrf_batched(other[3], other[2], other[4], other[5], "L", stream=s2) == 0
+        torch.cuda.synchronize()
+        _batched_check(b, buf, infos)
+    _batched_check(other[0], other[1], other[5])
+
+
+def test_set_stream_is_per_thread():
+    """relapack_set_stream is a per-thread setting — two threads each
+    factor on their own stream, interleaving set_stream and the call."""
+    import threading
+
+    n = 700
+    errs = []
+
+    def work(seed):
+        try:
+            s = torch.cuda.Stream()
+            for it in range(5):
+                A = np.asfortranarray(gen.spd(n, seed + it))
+                with torch.cuda.stream(s):
+                    dA = to_dev(A)
+                    info = rl.dpotrf(dA, "L", stream=s)
+                s.synchronize()
+                R = np.array(A, order="F")
+                assert info == oracle.dpotrf(R, "L") == 0
+                G = dA.cpu().numpy()
+                assert floored_rel_err(np.tril(G), np.tril(R), A) <= TOL
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(100 * k,)) for k in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+
+
 def test_batched_bad_sizes():
     n_ok = 16
     buf = torch.from_numpy(np.asfortranarray(gen.spd(n_ok, 1)).T.copy().reshape(-1)).cuda()
