@@ -13,6 +13,11 @@ Functions (each follows the passage cited in oracle.c):
   dtrsm_rlt(L, B)                        B := B L^{-T}
   dsyrk_ln(A, C)                         tril(C) -= tril(A A^T)
   dgemm_nt(A, B, C)                      C -= A B^T
+  dtrtri(A, uplo, diag)    -> info       A := A^{-1}, triangular
+  dlauum(A, uplo)                        A := L^T L (U U^T)
+  dpotri(A, uplo)          -> info       A := A^{-1} from its Cholesky factor (trtri + lauum)
+  dpotrs(A, B, uplo)                     B := A^{-1} B with the factor in A
+  dgetrf(A)                -> (info, ipiv)  P A = L U, partial pivoting
 
 Arrays are numpy float64 in Fortran (column-major) order and are modified in
 place, mirroring the LAPACK convention the method uses.
@@ -61,6 +66,16 @@ def _load():
         lib.oracle_dsyrk_ln.argtypes = [c_int, c_int, dp, c_int, dp, c_int]
         lib.oracle_dgemm_nt.argtypes = [c_int, c_int, c_int, dp, c_int, dp, c_int, dp, c_int]
         lib.oracle_num_threads.restype = c_int
+        lib.oracle_dtrtri.argtypes = [c_char, c_char, c_int, dp, c_int]
+        lib.oracle_dtrtri.restype = c_int
+        lib.oracle_dlauum.argtypes = [c_char, c_int, dp, c_int]
+        lib.oracle_dlauum.restype = None
+        lib.oracle_dpotri.argtypes = [c_char, c_int, dp, c_int]
+        lib.oracle_dpotri.restype = c_int
+        lib.oracle_dpotrs.argtypes = [c_char, c_int, c_int, dp, c_int, dp, c_int]
+        lib.oracle_dpotrs.restype = None
+        lib.oracle_dgetrf.argtypes = [c_int, c_int, dp, c_int, ip]
+        lib.oracle_dgetrf.restype = c_int
         _lib = lib
     return _lib
 
@@ -147,3 +162,39 @@ def dgemm_nt(A: np.ndarray, B: np.ndarray, C: np.ndarray) -> None:
     m, k = A.shape
     n = B.shape[0]
     _load().oracle_dgemm_nt(m, n, k, _ptr(A), max(1, m), _ptr(B), max(1, n), _ptr(C), max(1, C.shape[0]))
+
+
+def dtrtri(A: np.ndarray, uplo: str = "L", diag: str = "N", n: int | None = None) -> int:
+    """In-place inverse of the uplo triangle of A (LAPACK dtrtri semantics)."""
+    _check_f64_fortran(A, "A")
+    n = A.shape[1] if n is None else n
+    return _load().oracle_dtrtri(uplo.encode(), diag.encode(), n, _ptr(A), max(1, A.shape[0]))
+
+
+def dlauum(A: np.ndarray, uplo: str = "L") -> None:
+    """In-place L^T L (uplo 'L') / U U^T (uplo 'U') of the triangular factor in A."""
+    _check_f64_fortran(A, "A")
+    _load().oracle_dlauum(uplo.encode(), A.shape[1], _ptr(A), max(1, A.shape[0]))
+
+
+def dpotri(A: np.ndarray, uplo: str = "L") -> int:
+    """In-place inverse of the SPD matrix whose Cholesky factor is in A."""
+    _check_f64_fortran(A, "A")
+    return _load().oracle_dpotri(uplo.encode(), A.shape[1], _ptr(A), max(1, A.shape[0]))
+
+
+def dpotrs(A: np.ndarray, B: np.ndarray, uplo: str = "L") -> None:
+    """B := A^{-1} B with A's Cholesky factor in A (B n x nrhs, Fortran)."""
+    _check_f64_fortran(A, "A")
+    _check_f64_fortran(B, "B")
+    n, nrhs = B.shape
+    _load().oracle_dpotrs(uplo.encode(), n, nrhs, _ptr(A), max(1, A.shape[0]), _ptr(B), max(1, n))
+
+
+def dgetrf(A: np.ndarray):
+    """In-place LU with partial pivoting; returns (info, ipiv) with 1-based ipiv."""
+    _check_f64_fortran(A, "A")
+    m, n = A.shape
+    ipiv = np.zeros(max(1, min(m, n)), dtype=np.int32)
+    info = _load().oracle_dgetrf(m, n, _ptr(A), max(1, m), ipiv.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    return info, ipiv[:min(m, n)]

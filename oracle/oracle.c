@@ -205,6 +205,204 @@ void oracle_dgemm_nt(int m, int n, int k, const double* A, int lda, const double
   }
 }
 
+/* ========================================================================
+ * SURVEY §8(f) rows N1-N4 (the other recursive operations of the paper):
+ * each function is the plain definition of what the recursive algorithm
+ * reaches (the recursion reorganises a blocked algorithm, "once the
+ * traversal direction is fixed, all blocked variants result in the same
+ * recursive algorithm"), written out as the unblocked loop.  L-view indexing
+ * (LIDX) as above: uplo 'U' works on L = U^T.
+ * ======================================================================== */
+#include <stdlib.h>
+#include <string.h>
+
+static int parse_lower(char uplo) {
+  if (uplo == 'L' || uplo == 'l') return 1;
+  if (uplo == 'U' || uplo == 'u') return 0;
+  return -1;
+}
+
+/*
+ * oracle_dtrtri — X = L^{-1} in place ("in-place inversion of a
+ * lower triangular matrix A := A^{-1}", the paper's running example; SPEC
+ * rec_trtri / blocked_trtri S:287-296; LAPACK dtrtri).  Definition
+ * L X = I, column j of X by forward substitution (ascending k, one
+ * subtraction per term, true division):
+ *   x_jj = 1 / l_jj;  x_ij = (0 - sum_{k=j}^{i-1} l_ik x_kj) / l_ii   (i > j)
+ * computed as the column-oriented (axpy) sweep with the same per-element
+ * operation order.  diag 'U': l_ii = 1 (not referenced).  uplo 'U': U^{-1} =
+ * (L^{-1})^T of L = U^T.  Returns 0, -1 uplo, -2 diag, -3 n < 0, -5 lda, or
+ * k > 0: l_kk == 0 (singular; A is then not modified, LAPACK's check).
+ */
+int oracle_dtrtri(char uplo, char diag, int n, double* A, int lda) {
+  const int lower = parse_lower(uplo);
+  if (lower < 0) return -1;
+  const int unit = (diag == 'U' || diag == 'u');
+  if (!unit && !(diag == 'N' || diag == 'n')) return -2;
+  if (n < 0) return -3;
+  if (lda < (n > 1 ? n : 1)) return -5;
+  if (!unit)
+    for (int k = 0; k < n; ++k)
+      if (A[LIDX(k, k)] == 0.0) return k + 1;
+  /* dense copy of the L-view: columns of X are computed from the original L */
+  double* Lc = (double*)malloc(sizeof(double) * (size_t)n * (size_t)(n > 0 ? n : 1));
+  for (int j = 0; j < n; ++j)
+    for (int i = j; i < n; ++i) Lc[(size_t)i + (size_t)j * n] = A[LIDX(i, j)];
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+#pragma omp for schedule(dynamic, 8)
+    for (int j = 0; j < n; ++j) {
+      for (int i = j; i < n; ++i) x[i] = 0.0;
+      x[j] = 1.0;
+      for (int k = j; k < n; ++k) {
+        /* x_k is complete once its diagonal division is done */
+        if (!unit) x[k] = x[k] / Lc[(size_t)k + (size_t)k * n];
+        const double xk = x[k];
+        const double* lk = Lc + (size_t)k * n;
+        for (int i = k + 1; i < n; ++i) {
+          double p = lk[i] * xk;
+          x[i] = x[i] - p;
+        }
+      }
+      for (int i = j; i < n; ++i)
+        if (!(unit && i == j)) A[LIDX(i, j)] = x[i];
+    }
+    free(x);
+  }
+  free(Lc);
+  return 0;
+}
+
+/*
+ * oracle_dlauum — the product L^T L of the L-view, lower triangle in place
+ * (uplo 'L': A := L^T L; uplo 'U': A := U U^T = the same in the L-view;
+ * SPEC rec_lauum S:376-384; the macro list P:125-127).  Definition:
+ *   c_ij = sum_{k=i}^{n-1} l_ki l_kj,  i >= j   (ascending k, from 0.0)
+ */
+void oracle_dlauum(char uplo, int n, double* A, int lda) {
+  const int lower = parse_lower(uplo);
+  if (lower < 0 || n <= 0) return;
+  double* Lc = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);
+  for (int j = 0; j < n; ++j)
+    for (int i = j; i < n; ++i) Lc[(size_t)i + (size_t)j * n] = A[LIDX(i, j)];
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int j = 0; j < n; ++j) {
+    const double* lj = Lc + (size_t)j * n;
+    for (int i = j; i < n; ++i) {
+      const double* li = Lc + (size_t)i * n;
+      double s = 0.0;
+      for (int k = i; k < n; ++k) {
+        double p = li[k] * lj[k];
+        s = s + p;
+      }
+      A[LIDX(i, j)] = s;
+    }
+  }
+  free(Lc);
+}
+
+/*
+ * oracle_dpotri — inverse of the SPD matrix from its Cholesky factor, in place
+ * (LAPACK dpotri = dtrtri then dlauum; §8(f) N3):
+ * A^{-1} = L^{-T} L^{-1} (uplo 'L'), U^{-1} U^{-T} (uplo 'U'), uplo triangle.
+ * Returns oracle_dtrtri's info.
+ */
+int oracle_dpotri(char uplo, int n, double* A, int lda) {
+  const int info = oracle_dtrtri(uplo, 'N', n, A, lda);
+  if (info != 0) return info;
+  oracle_dlauum(uplo, n, A, lda);
+  return 0;
+}
+
+/*
+ * oracle_dpotrs — solve A X = B with the Cholesky factor in A (LAPACK dpotrs;
+ * §8(f) N3): B (n x nrhs, column-major, ldb) := A^{-1} B by
+ *   L Y = B  (forward:  y_i = (b_i - sum_{k<i} l_ik y_k) / l_ii)
+ *   L^T X = Y (backward: x_i = (y_i - sum_{k>i} l_ki x_k) / l_ii, i descending)
+ * ascending / descending k as written, true division.  uplo 'U': L = U^T.
+ */
+void oracle_dpotrs(char uplo, int n, int nrhs, const double* A, int lda, double* B, int ldb) {
+  const int lower = parse_lower(uplo);
+  if (lower < 0 || n <= 0 || nrhs <= 0) return;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int c = 0; c < nrhs; ++c) {
+    double* b = B + (size_t)c * (size_t)ldb;
+    for (int i = 0; i < n; ++i) {
+      double s = b[i];
+      for (int k = 0; k < i; ++k) {
+        double p = A[LIDX(i, k)] * b[k];
+        s = s - p;
+      }
+      b[i] = s / A[LIDX(i, i)];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = b[i];
+      for (int k = i + 1; k < n; ++k) {
+        double p = A[LIDX(k, i)] * b[k];
+        s = s - p;
+      }
+      b[i] = s / A[LIDX(i, i)];
+    }
+  }
+}
+
+/*
+ * oracle_dgetrf — LU with partial pivoting, P A = L U (SPEC rec_getrf /
+ * blocked_getrf S:306-312; §8(f) N4), as the unblocked
+ * right-looking getf2 loop (LAPACK order) on the m x n column-major A:
+ *   for j = 0 .. min(m,n)-1:
+ *     p = first index of max_{i>=j} |a_ij|            (ties: smallest i)
+ *     ipiv[j] = p + 1 (1-based);  swap rows j and p over all n columns
+ *     if a_jj != 0:  a_ij = a_ij / a_jj  (i > j, true division)
+ *     else if info == 0: info = j + 1  (factorization continues)
+ *     a_ik = a_ik - a_ij * a_jk  (i > j, k > j)
+ * Returns info (0, or the first zero pivot), or -1 m < 0, -2 n < 0, -4 lda.
+ */
+int oracle_dgetrf(int m, int n, double* A, int lda, int* ipiv) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (lda < (m > 1 ? m : 1)) return -4;
+  int info = 0;
+  const int mn = m < n ? m : n;
+  for (int j = 0; j < mn; ++j) {
+    double* aj = A + (size_t)j * (size_t)lda;
+    int p = j;
+    double best = fabs(aj[j]);
+    for (int i = j + 1; i < m; ++i) {
+      const double v = fabs(aj[i]);
+      if (v > best) {
+        best = v;
+        p = i;
+      }
+    }
+    ipiv[j] = p + 1;
+    if (p != j)
+      for (int k = 0; k < n; ++k) {
+        double* col = A + (size_t)k * (size_t)lda;
+        const double t = col[j];
+        col[j] = col[p];
+        col[p] = t;
+      }
+    const double piv = aj[j];
+    if (piv != 0.0) {
+      for (int i = j + 1; i < m; ++i) aj[i] = aj[i] / piv;
+    } else if (info == 0) {
+      info = j + 1;
+    }
+#pragma omp parallel for schedule(static) if ((size_t)(m - j) * (size_t)(n - j) > 65536)
+    for (int k = j + 1; k < n; ++k) {
+      double* col = A + (size_t)k * (size_t)lda;
+      const double ujk = col[j];
+      for (int i = j + 1; i < m; ++i) {
+        double q = aj[i] * ujk;
+        col[i] = col[i] - q;
+      }
+    }
+  }
+  return info;
+}
+
 /* Number of OpenMP threads the oracle will use (for bench reporting). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP
