@@ -235,6 +235,70 @@ RELAPACK_API int relapack_profile_records(int max, double* out);
  */
 RELAPACK_API int relapack_trace_read(int max, double* out);
 
+/* ---- the paper's other recursive operations ----
+ * Same conventions as relapack_dpotrf: column-major FP64 DEVICE matrices,
+ * LAPACK argument order and info codes (-i: the i-th argument is illegal,
+ * <= -1000: CUDA failure, see relapack_last_error), work ordered on the
+ * calling thread's relapack_set_stream stream, synchronous (info is a host
+ * int).  Each call's plan is captured once per (operation, shape, operand
+ * pointers) into a CUDA graph (footprint-dependency edges) and replayed.
+ * Only the uplo triangle of a triangular / symmetric operand is read or
+ * written.  uplo 'U' runs the lower algorithms on L = U^T (as dpotrf).
+ *
+ * relapack_dtrtri — A := A^{-1} for triangular A (LAPACK dtrtri; the paper's
+ *   running example; recursive algorithm: invert A_TL,
+ *   A_BL := -A_BL A_TL^{-1} (trmm) and A_BL := A_BR^{-1} A_BL (trsm, the
+ *   stable form), invert A_BR; crossover to an unblocked in-SM
+ *   kernel at n <= 64).  diag 'N'/'U' (unit: the diagonal is neither read nor
+ *   written).  Arguments: 1 uplo, 2 diag, 3 n, 4 A, 5 lda.  info = k > 0:
+ *   A(k,k) == 0, A is not modified (checked first, as LAPACK).
+ * relapack_dtrtri_blocked — the blocked algorithm of P:384-409 / S:287-296
+ *   with block size nb (>= 1; argument 6): per step A10 := -A10 A00 (A00
+ *   already inverted), A10 := A11^{-1} A10, A11 := A11^{-1} (the unblocked
+ *   kernel for nb <= 64, the recursive algorithm for larger diagonal blocks).
+ * relapack_dlauum — A := L^T L (uplo 'L') / U U^T (uplo 'U') of the
+ *   triangular factor, uplo triangle in place (recursive: lauum(A_TL);
+ *   A_TL += A_BL^T A_BL; A_BL := A_BR^T A_BL; lauum(A_BR)).
+ *   Arguments: 1 uplo, 2 n, 3 A, 4 lda; info 0.
+ * relapack_dpotri — A := A^{-1} of the SPD matrix whose Cholesky factor (from
+ *   relapack_dpotrf, same uplo) is in A: dtrtri then dlauum.  info = k > 0:
+ *   the factor's k-th diagonal entry is zero.
+ * relapack_dpotrs — B := A^{-1} B with the Cholesky factor in A: two
+ *   recursive triangular solves (L Y = B, L^T X = Y).  B is a DEVICE n x nrhs
+ *   column-major matrix (ldb >= max(1, n)).  Arguments: 1 uplo, 2 n, 3 nrhs,
+ *   4 A, 5 lda, 6 B, 7 ldb.
+ * relapack_dgetrf — P A = L U with partial pivoting (LAPACK dgetrf; recursive
+ *   algorithm: split the columns, factor the left panel, swap and
+ *   solve the right panel, update A22, factor it, swap the left panel).  A is
+ *   m x n (lda >= max(1, m)); ipiv a DEVICE int array of min(m, n) 1-based row
+ *   indices (row i was interchanged with row ipiv[i]).  Pivot = the first
+ *   maximum |a_ij| of the current column (LAPACK idamax).  info = k > 0: U(k,k)
+ *   is exactly zero (the factorization completes).  Panels of <= 32 columns
+ *   run as one cooperative grid.  Arguments: 1 m, 2 n, 3 A, 4 lda, 5 ipiv.
+ * relapack_dpotrf_blocked — the blocked right-looking Cholesky with block nb
+ *   (per step potrf(A11), A21 := A21 L11^{-T}, A22 -=
+ *   A21 A21^T) on the same kernels and executor as relapack_dpotrf, for the
+ *   paper's blocked-vs-recursive comparison.  nb in [16, n]; diagonal blocks
+ *   above 128 are factored by the recursive algorithm.  Arguments: 1 uplo,
+ *   2 n, 3 A, 4 lda, 5 nb.  DEVICE A.
+ * relapack_xplan_count — host-only: the launch count of one of these plans
+ *   (op 0 trtri, 1 trtri_blocked (nb), 2 lauum, 3 potri, 4 potrs (nrhs = nb),
+ *   5 getrf (n x n)), their kinds (0 gemm, 1 tri, 2 trti2, 3 lauu2, 4 potf2,
+ *   5 getf2, 6 laswp, 7 check) and the summed leading-term flops.
+ */
+RELAPACK_API void relapack_dtrtri(const char* uplo, const char* diag, const int* n, double* A, const int* lda,
+                                  int* info);
+RELAPACK_API void relapack_dtrtri_blocked(const char* uplo, const char* diag, const int* n, double* A,
+                                          const int* lda, int nb, int* info);
+RELAPACK_API void relapack_dlauum(const char* uplo, const int* n, double* A, const int* lda, int* info);
+RELAPACK_API void relapack_dpotri(const char* uplo, const int* n, double* A, const int* lda, int* info);
+RELAPACK_API void relapack_dpotrs(const char* uplo, const int* n, const int* nrhs, const double* A, const int* lda,
+                                  double* B, const int* ldb, int* info);
+RELAPACK_API void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int* ipiv, int* info);
+RELAPACK_API void relapack_dpotrf_blocked(const char* uplo, const int* n, double* A, const int* lda, int nb,
+                                          int* info);
+RELAPACK_API int relapack_xplan_count(int op, int n, int nb, int* kinds, int max_kinds, double* flops);
+
 /*
  * Kernel test hooks (synchronous; test infrastructure, not a production API).
  * Each launches ONE kernel of the hot path on caller-provided DEVICE blocks with

@@ -113,6 +113,24 @@ def lib():
         L.relapack_trsm_test.restype = c_int
         L.relapack_potf2_test.argtypes = [c_int, c_int, c_void_p, i64, ip, c_void_p]
         L.relapack_potf2_test.restype = c_int
+        cp = ctypes.c_char_p
+        L.relapack_dtrtri.argtypes = [cp, cp, ip, c_void_p, ip, ip]
+        L.relapack_dtrtri.restype = None
+        L.relapack_dtrtri_blocked.argtypes = [cp, cp, ip, c_void_p, ip, c_int, ip]
+        L.relapack_dtrtri_blocked.restype = None
+        L.relapack_dlauum.argtypes = [cp, ip, c_void_p, ip, ip]
+        L.relapack_dlauum.restype = None
+        L.relapack_dpotri.argtypes = [cp, ip, c_void_p, ip, ip]
+        L.relapack_dpotri.restype = None
+        L.relapack_dpotrs.argtypes = [cp, ip, ip, c_void_p, ip, c_void_p, ip, ip]
+        L.relapack_dpotrs.restype = None
+        L.relapack_dgetrf.argtypes = [ip, ip, c_void_p, ip, c_void_p, ip]
+        L.relapack_dgetrf.restype = None
+        L.relapack_dpotrf_blocked.argtypes = [cp, ip, c_void_p, ip, c_int, ip]
+        L.relapack_dpotrf_blocked.restype = None
+        L.relapack_xplan_count.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_int), c_int,
+                                           ctypes.POINTER(c_double)]
+        L.relapack_xplan_count.restype = c_int
         _lib = L
     return _lib
 
@@ -380,6 +398,112 @@ def potf2_test(A, stream=None) -> int:
     if r != 0:
         raise RelapackError(f"relapack_potf2_test failed ({r}): {last_error()}")
     return info.value
+
+
+def _ci(v: int):
+    return ctypes.byref(ctypes.c_int(int(v)))
+
+
+def _set_stream_for(A, stream):
+    import torch
+
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    lib().relapack_set_stream(ctypes.c_void_p(st.cuda_stream))
+
+
+def _check_info(name: str, v: int) -> int:
+    if v <= -1000:
+        raise RelapackError(f"{name} failed: {last_error()}")
+    return v
+
+
+def dtrtri(A, uplo: str = "L", diag: str = "N", stream=None) -> int:
+    """A := A^{-1} for the uplo-triangular device matrix A (column-major); returns info."""
+    ptr, n, lda = _matrix_args(A)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dtrtri(uplo.encode(), diag.encode(), _ci(n), ctypes.c_void_p(ptr), _ci(lda), ctypes.byref(info))
+    return _check_info("relapack_dtrtri", info.value)
+
+
+def dtrtri_blocked(A, nb: int, uplo: str = "L", diag: str = "N", stream=None) -> int:
+    """Blocked (block nb) triangular inverse, for the blocked-vs-recursive comparison; returns info."""
+    ptr, n, lda = _matrix_args(A)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dtrtri_blocked(uplo.encode(), diag.encode(), _ci(n), ctypes.c_void_p(ptr), _ci(lda), int(nb),
+                                  ctypes.byref(info))
+    return _check_info("relapack_dtrtri_blocked", info.value)
+
+
+def dlauum(A, uplo: str = "L", stream=None) -> int:
+    """A := L^T L (uplo L) / U U^T (uplo U) in place; returns info."""
+    ptr, n, lda = _matrix_args(A)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dlauum(uplo.encode(), _ci(n), ctypes.c_void_p(ptr), _ci(lda), ctypes.byref(info))
+    return _check_info("relapack_dlauum", info.value)
+
+
+def dpotri(A, uplo: str = "L", stream=None) -> int:
+    """A := A^{-1} from the Cholesky factor in A; returns info."""
+    ptr, n, lda = _matrix_args(A)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dpotri(uplo.encode(), _ci(n), ctypes.c_void_p(ptr), _ci(lda), ctypes.byref(info))
+    return _check_info("relapack_dpotri", info.value)
+
+
+def dpotrs(A, B, uplo: str = "L", stream=None) -> int:
+    """B := A^{-1} B with the Cholesky factor in A; B (n, nrhs) column-major device tensor."""
+    ptr, n, lda = _matrix_args(A)
+    if B.dim() != 2 or B.shape[0] != n or (B.shape[1] > 1 and B.stride(0) != 1):
+        raise ValueError("B must be (n, nrhs) column-major")
+    nrhs = B.shape[1]
+    ldb = max(1, B.stride(1) if nrhs > 1 else n)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dpotrs(uplo.encode(), _ci(n), _ci(nrhs), ctypes.c_void_p(ptr), _ci(lda),
+                          ctypes.c_void_p(B.data_ptr()), _ci(ldb), ctypes.byref(info))
+    return _check_info("relapack_dpotrs", info.value)
+
+
+def dgetrf(A, ipiv, stream=None) -> int:
+    """P A = L U in place (A (m, n) column-major device tensor); ipiv int32 device tensor of min(m, n)."""
+    import torch
+
+    if A.dim() != 2 or A.dtype != torch.float64:
+        raise TypeError("A must be a 2-D float64 tensor")
+    m, n = A.shape
+    if n > 1 and A.stride(0) != 1:
+        raise ValueError("A must be column-major")
+    lda = max(1, A.stride(1) if n > 1 else m)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dgetrf(_ci(m), _ci(n), ctypes.c_void_p(A.data_ptr()), _ci(lda), ctypes.c_void_p(ipiv.data_ptr()),
+                          ctypes.byref(info))
+    return _check_info("relapack_dgetrf", info.value)
+
+
+def dpotrf_blocked(A, nb: int, uplo: str = "L", stream=None) -> int:
+    """Blocked right-looking Cholesky with block nb on the library's kernels; returns info."""
+    ptr, n, lda = _matrix_args(A)
+    _set_stream_for(A, stream)
+    info = ctypes.c_int(0)
+    lib().relapack_dpotrf_blocked(uplo.encode(), _ci(n), ctypes.c_void_p(ptr), _ci(lda), int(nb), ctypes.byref(info))
+    return _check_info("relapack_dpotrf_blocked", info.value)
+
+
+def xplan_count(op: str, n: int, nb: int = 0):
+    """Host-only: (launches, kinds, flops) of a §8(f) plan (op in trtri, trtri_blocked, lauum, potri, potrs, getrf)."""
+    code = {"trtri": 0, "trtri_blocked": 1, "lauum": 2, "potri": 3, "potrs": 4, "getrf": 5}[op]
+    fl = ctypes.c_double(0)
+    cnt = lib().relapack_xplan_count(code, n, nb, None, 0, ctypes.byref(fl))
+    if cnt < 0:
+        raise ValueError("bad plan arguments")
+    kinds = (ctypes.c_int * max(cnt, 1))()
+    lib().relapack_xplan_count(code, n, nb, kinds, cnt, ctypes.byref(fl))
+    return cnt, list(kinds)[:cnt], fl.value
 
 
 def split_point(n: int, align: int) -> int:

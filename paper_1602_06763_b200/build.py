@@ -14,14 +14,17 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "librelapack_b200.so")
-BUILD = os.path.join(HERE, "build")
+# RELAPACK_BUILD_OUT / RELAPACK_BUILD_DEFS: an alternative build (A/B experiments,
+# tools/ab_bench.py) into another directory with extra -D flags
+OUT = os.environ.get("RELAPACK_BUILD_OUT") or os.path.join(HERE, "librelapack_b200.so")
+BUILD = os.path.join(os.path.dirname(OUT), "build") if os.environ.get("RELAPACK_BUILD_OUT") else os.path.join(HERE, "build")
+EXTRA_DEFS = [f"-D{d}" for d in os.environ.get("RELAPACK_BUILD_DEFS", "").split()]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+FLAGS = EXTRA_DEFS + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["update.cu", "potf2.cu", "trsm.cu", "trsm_fused.cu", "batched.cu", "driver.cu", "dist.cu", "hooks.cu", "plan.cpp"]
+SOURCES = ["update.cu", "potf2.cu", "trsm.cu", "trsm_fused.cu", "batched.cu", "driver.cu", "dist.cu", "hooks.cu", "xkernels.cu", "xdriver.cu", "plan.cpp", "xplan.cpp"]
 
 
 def _digest() -> str:

@@ -104,7 +104,9 @@ static __device__ __noinline__ double rsqrt_approx_tiny(double d) {
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+#ifndef RELAPACK_RSQRT_NO_TINY  // (A/B experiments only: the round-1 chain without the subnormal branch)
   if (d < 0x1p-1000) y = rsqrt_approx_tiny(d);
+#endif
   const double p = d * y;
   const double e = fma(-p, y, 1.0);
   const double t = fma(0.375, e, 0.5);

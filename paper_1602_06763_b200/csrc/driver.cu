@@ -598,21 +598,22 @@ static std::string knob_signature(const PlanParams& pp, bool use_graph, bool use
   char b[512];
   snprintf(b, sizeof(b),
            "c%d T%d tb%d la%d tr%d ld%d db%d bc%d hg%d g%d d%d bulk%d bmin%g upd%d dl%d sk%d pdl%d tr%d pm%d sc%d ck%d "
-           "cp%d cr%d skip%d",
+           "cp%d cr%d skip%d nb%d",
            pp.crossover, pp.split_tile, pp.trsm_base, (int)pp.lookahead, pp.trsm_rows, pp.lookahead_depth,
            (int)pp.defer_b21, pp.b21_chunks, pp.host_gemm_cols, (int)use_graph, (int)use_dag, bulk_ctas(),
            bulk_min_flops(), upd_ctas(), (int)defer_low_priority(), (int)splitk_enabled(), pdl_mode(),
            (int)trace_enabled(), env_int("RELAPACK_PRIO_MODE", 1), (int)split_copies_enabled(), (int)copy_kernels(),
-           copy_panel(), env_int("RELAPACK_COPY_ROWS", 0), debug_skip_mask());
+           copy_panel(), env_int("RELAPACK_COPY_ROWS", 0), debug_skip_mask(), pp.blocked_nb);
   return b;
 }
 
 // Enqueue the factorization of the device matrix A (already validated).
 int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st, const double* host,
-                  int64_t hld) {
+                  int64_t hld, int blocked_nb) {
   DeviceState* ds = device_state(dev);
   cudaError_t e;
   PlanParams pp = current_params();
+  pp.blocked_nb = blocked_nb;
   if (host) {
     // host-matrix path: the TRSM GEMMs go in copy-panel-wide column chunks,
     // each waiting only for its own host blocks (n = 16384 e2e 57.0 -> 52.7 ms,
@@ -1011,6 +1012,58 @@ int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const*
   if (batch == 0) return 0;
   cudaError_t e = launch_potf2_batched(layout, batch, d_n, d_A, d_lda, d_info, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "batched launch");
+}
+
+void relapack_dpotrf_blocked(const char* uplo, const int* n_, double* A, const int* lda_, int nb, int* info) {
+  if (!info) return;
+  if (!uplo || !n_ || !lda_) {
+    *info = -1;
+    return;
+  }
+  int layout = 0;
+  const int n = *n_, lda = *lda_;
+  int ai = check_args(*uplo, n, A, lda, &layout);
+  if (ai != 0) {
+    *info = ai;
+    return;
+  }
+  if (n == 0) {
+    *info = 0;
+    return;
+  }
+  int dev = 0;
+  if (!is_device_pointer(A, &dev)) {
+    *info = -3;
+    return;
+  }
+  if (nb < 16) {
+    *info = -5;
+    return;
+  }
+  DeviceGuard guard;
+  if (dev != guard.saved) cudaSetDevice(dev);
+  DeviceState* ds = device_state(dev);
+  std::lock_guard<std::mutex> sync_lk(ds->sync_mu);
+  cudaError_t e;
+  {
+    std::lock_guard<std::mutex> lk(ds->mu);
+    if ((e = ensure_device(ds)) != cudaSuccess) {
+      *info = cuda_fail(e, "device setup");
+      return;
+    }
+  }
+  cudaStream_t st = g_stream;
+  const int r = enqueue_potrf(dev, A, n, lda, layout, ds->d_info, st, nullptr, 0, nb < n ? nb : n);
+  if (r != 0) {
+    *info = r;
+    return;
+  }
+  if ((e = cudaMemcpyAsync(ds->h_info, ds->d_info, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    *info = cuda_fail(e, "sync");
+    return;
+  }
+  *info = *ds->h_info;
 }
 
 void relapack_set_stream(relapack_stream_t stream) {

@@ -14,8 +14,9 @@ int trsm_base_cols();
 // Enqueue the whole recursive factorization of the device L-view matrix A on st.
 // With `host` (pinned), A is the device staging buffer and the H2D/D2H copies
 // of the uplo triangle are part of the captured DAG.
+// blocked_nb > 0: the blocked right-looking algorithm (relapack_dpotrf_blocked).
 int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info, cudaStream_t st,
-                  const double* host = nullptr, int64_t hld = 0);
+                  const double* host = nullptr, int64_t hld = 0, int blocked_nb = 0);
 // The stream set with relapack_set_stream, or `fallback` if none was set.
 cudaStream_t current_stream_or(cudaStream_t fallback);
 }  // namespace relapack

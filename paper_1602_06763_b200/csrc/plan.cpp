@@ -136,8 +136,39 @@ void build_potrf(int off, int n, int level, int info_base, const PlanParams& p, 
 
 }  // namespace
 
+// Blocked right-looking Cholesky (SPEC blocked_potrf S:297-305):
+// per step of b columns, potrf(A11) — the base kernel when b <= c, else the
+// recursive algorithm on the diagonal block (as LAPACK >= 3.6 does with
+// dpotrf2) —, A21 := A21 L11^{-T} (the library's TRSM), A22 -= A21 A21^T
+// (one SYRK over the whole trailing matrix, no lookahead: LAPACK's order).
+void build_blocked(int n, const PlanParams& p, std::vector<PlanOp>& ops) {
+  PlanParams q = p;
+  q.blocked_nb = 0;
+  q.lookahead = false;
+  const int b = p.blocked_nb;
+  for (int j = 0; j < n; j += b) {
+    const int jb = std::min(b, n - j), rest = n - j - jb;
+    build_potrf(j, jb, 1, j, q, ops);
+    if (rest <= 0) break;
+    build_trsm(j, BUF_A, j + jb, j, rest, jb, 1, q, ops);
+    PlanOp s{};
+    s.kind = OP_SYRK;
+    s.level = 1;
+    s.c_i = j + jb; s.c_j = j + jb;
+    s.a_i = j + jb; s.a_j = j;
+    s.b_i = j + jb; s.b_j = j;
+    s.n = s.m = rest; s.k = jb;
+    s.flops = (double)rest * rest * jb;
+    ops.push_back(s);
+  }
+}
+
 void build_potrf_plan(int n, const PlanParams& p, std::vector<PlanOp>& ops) {
   ops.clear();
+  if (p.blocked_nb > 0) {
+    build_blocked(n, p, ops);
+    return;
+  }
   build_potrf(0, n, 0, 0, p, ops);
 }
 

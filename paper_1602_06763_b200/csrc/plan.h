@@ -76,6 +76,9 @@ struct PlanParams {
   // as column chunks of this width, so each starts as soon as its own host
   // blocks have arrived instead of waiting for all of B2
   int host_gemm_cols = 0;
+  // > 0: the blocked right-looking algorithm with this block size instead of
+  // the recursive one (relapack_dpotrf_blocked)
+  int blocked_nb = 0;
 };
 
 // Rectangle of an op's footprint in L-view coordinates of buffer `buf`.

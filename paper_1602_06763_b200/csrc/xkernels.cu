@@ -1,0 +1,412 @@
+// xkernels.cu — base-case kernels of the other recursive operations of the
+// paper (N1 trtri, N2 blocked variants, N3 lauum / potri /
+// potrs, N4 getrf).  Their BLAS-3 bulk runs on the update kernel of update.cu
+// (mixed operand layouts); these kernels are the recursion's leaves:
+//
+//   k_tri_rows   every row x of a block B (m x t, t <= 64) against a t x t
+//                lower-triangular block T of the L-view (P:292-295 / S:183-191
+//                and their transposed forms): x := x T^{-T} (forward solve),
+//                x := x T^{-1} (backward solve), x := alpha x T, x := alpha x T^T,
+//                unit or non-unit diagonal.  Left-side operations run on the
+//                transposed view of B, so one kernel serves every TRSM / TRMM
+//                variant the recursions issue.
+//   k_trti2      in-place inverse of a t x t lower-triangular block (t <= 64;
+//                the paper's "unblocked dtrti2")
+//   k_lauu2      in-place L^T L of a t x t lower-triangular block (t <= 64)
+//   k_diag_check first zero diagonal entry of the L-view (dtrtri's info)
+//   k_getf2      LU with partial pivoting of an m x w panel (w <= 32), one
+//                cooperative grid, one grid barrier per column
+//   k_laswp      row interchanges ipiv[k0..k1) on a range of columns
+//
+// Operand X (rows x cols) of layout 0 has element (r, c) at X[r + c*ld],
+// layout 1 at X[c + r*ld] (common.cuh lv_off).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "xkernels.h"
+
+namespace relapack {
+
+namespace {
+
+constexpr int kTriRows = 128;            // rows (threads) per CTA of k_tri_rows
+constexpr int kTriLd = kTriMax + 1;      // odd smem stride: row r's column c at r * kTriLd + c
+
+__device__ __forceinline__ double at(const double* X, int layout, int64_t ld, int r, int c) {
+  return X[lv_off(layout, r, c, ld)];
+}
+
+}  // namespace
+
+// One thread per row of B; the row lives in shared memory (stride 65, so the
+// threads' concurrent accesses to one column hit 32 distinct banks) and T in
+// shared memory read by broadcast.  Solves divide by the diagonal (true
+// division, as the oracle); products accumulate in ascending / descending k.
+__global__ void __launch_bounds__(kTriRows) k_tri_rows(XTriArgs a) {
+  if (ld_info(a.d_info) != 0) return;
+  extern __shared__ double sm[];
+  double* sT = sm;                          // t x t, sT[i * kTriLd + j] = T(i, j)
+  double* sB = sm + kTriMax * kTriLd;       // kTriRows x t
+  const int t = a.t;
+  const int row0 = blockIdx.x * kTriRows;
+  const int rows = min(kTriRows, a.m - row0);
+  // stage T (lower part only; the other triangle is never read)
+  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+    int i, j;
+    if (a.lt == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
+    if (i >= j) sT[i * kTriLd + j] = at(a.T, a.lt, a.ldt, i, j);
+  }
+  // stage the CTA's rows of B, coalesced along B's contiguous index
+  for (int e = threadIdx.x; e < rows * t; e += blockDim.x) {
+    int r, c;
+    if (a.lb == 0) { r = e % rows; c = e / rows; } else { c = e % t; r = e / t; }
+    sB[r * kTriLd + c] = at(a.B, a.lb, a.ldb, row0 + r, c);
+  }
+  __syncthreads();
+  const int r = threadIdx.x;
+  if (r < rows) {
+    double* x = sB + r * kTriLd;
+    const double alpha = a.alpha;
+    switch (a.mode) {
+      case kTriSolveLT:  // x T^T = b: x_j = (b_j - sum_{k<j} x_k T_jk) / T_jj
+        for (int j = 0; j < t; ++j) {
+          double s = alpha * x[j];
+          for (int k = 0; k < j; ++k) s -= x[k] * sT[j * kTriLd + k];
+          x[j] = a.unit ? s : s / sT[j * kTriLd + j];
+        }
+        break;
+      case kTriSolveL:  // x T = b: x_j = (b_j - sum_{k>j} x_k T_kj) / T_jj
+        for (int j = t - 1; j >= 0; --j) {
+          double s = alpha * x[j];
+          for (int k = t - 1; k > j; --k) s -= x[k] * sT[k * kTriLd + j];
+          x[j] = a.unit ? s : s / sT[j * kTriLd + j];
+        }
+        break;
+      case kTriMulL:  // y_j = alpha sum_{k>=j} x_k T_kj (ascending j reads only x_k, k >= j)
+        for (int j = 0; j < t; ++j) {
+          double s = a.unit ? x[j] : x[j] * sT[j * kTriLd + j];
+          for (int k = j + 1; k < t; ++k) s += x[k] * sT[k * kTriLd + j];
+          x[j] = alpha * s;
+        }
+        break;
+      default:  // kTriMulLT: y_j = alpha sum_{k<=j} x_k T_jk (descending j)
+        for (int j = t - 1; j >= 0; --j) {
+          double s = a.unit ? x[j] : x[j] * sT[j * kTriLd + j];
+          for (int k = 0; k < j; ++k) s += x[k] * sT[j * kTriLd + k];
+          x[j] = alpha * s;
+        }
+        break;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * t; e += blockDim.x) {
+    int rr, c;
+    if (a.lb == 0) { rr = e % rows; c = e / rows; } else { c = e % t; rr = e / t; }
+    a.B[lv_off(a.lb, row0 + rr, c, a.ldb)] = sB[rr * kTriLd + c];
+  }
+}
+
+// Inverse of the t x t lower-triangular block in place.  Column j of X = T^{-1}
+// is owned by thread j; rows are produced in ascending order, every thread
+// reading the same T(i, k) (broadcast) and its own column of X:
+//   x_jj = 1 / t_jj;  x_ij = (0 - sum_{k=j}^{i-1} t_ik x_kj) / t_ii.
+// diag unit: t_ii = 1 and the diagonal is left untouched.
+__global__ void __launch_bounds__(kTriMax) k_trti2(XBlockArgs a) {
+  if (ld_info(a.d_info) != 0) return;
+  extern __shared__ double sm[];
+  double* sT = sm;
+  double* sX = sm + kTriMax * kTriLd;  // sX[i * kTriLd + j] = X(i, j)
+  const int t = a.n;
+  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+    int i, j;
+    if (a.layout == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
+    if (i >= j) sT[i * kTriLd + j] = at(a.A, a.layout, a.ld, i, j);
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < t) {
+    for (int i = j; i < t; ++i) {
+      double s = i == j ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s -= sT[i * kTriLd + k] * sX[k * kTriLd + j];
+      sX[i * kTriLd + j] = a.unit ? s : s / sT[i * kTriLd + i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+    int i, jj;
+    if (a.layout == 0) { i = e % t; jj = e / t; } else { jj = e % t; i = e / t; }
+    if (i > jj || (i == jj && !a.unit)) a.A[lv_off(a.layout, i, jj, a.ld)] = sX[i * kTriLd + jj];
+  }
+}
+
+// L^T L of the t x t lower-triangular block, lower triangle in place:
+// c_ij = sum_{k=i}^{t-1} l_ki l_kj (i >= j), ascending k.
+__global__ void __launch_bounds__(256) k_lauu2(XBlockArgs a) {
+  if (ld_info(a.d_info) != 0) return;
+  __shared__ double sT[kTriMax * kTriLd];
+  const int t = a.n;
+  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+    int i, j;
+    if (a.layout == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
+    if (i >= j) sT[i * kTriLd + j] = at(a.A, a.layout, a.ld, i, j);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+    int i, j;
+    if (a.layout == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
+    if (i < j) continue;
+    double s = 0.0;
+    for (int k = i; k < t; ++k) s += sT[k * kTriLd + i] * sT[k * kTriLd + j];
+    a.A[lv_off(a.layout, i, j, a.ld)] = s;
+  }
+}
+
+// info = 1 + first k with T(k, k) == 0 (0 if none): LAPACK dtrtri's
+// singularity check, before anything is modified.
+__global__ void k_diag_check(const double* A, int64_t ld, int layout, int n, int* d_info) {
+  __shared__ int first;
+  if (threadIdx.x == 0) first = 0x7fffffff;
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    if (A[lv_off(layout, k, k, ld)] == 0.0) atomicMin(&first, k);
+  __syncthreads();
+  if (threadIdx.x == 0) *d_info = first == 0x7fffffff ? 0 : first + 1;
+}
+
+// ------------------------------------------------------------------ getrf panel
+namespace {
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier (all CTAs co-resident: cooperative launch); the counter is
+// zeroed before the launch, `phase` counts the barriers passed so far.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& phase) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned target = (phase + 1) * gridDim.x;
+    atomicAdd(bar, 1u);
+    while (ld_acquire_u32(bar) < target) __nanosleep(32);
+    __threadfence();
+  }
+  ++phase;
+  __syncthreads();
+}
+
+}  // namespace
+
+// LU with partial pivoting of the m x w panel P (layout 0, ld), w <= kGetf2Max,
+// rows [0, m); pivots written to ipiv[0..w) as panel-relative row indices plus
+// `pivot_base` (the panel's global first row).  CTA g owns rows [g R, g R + R)
+// in shared memory.  Per column j: local first-maximum candidate -> published
+// with its whole row (and, by the owner, row j) -> grid barrier -> every CTA
+// picks the global first maximum, applies the interchange to its rows,
+// divides its multipliers by the pivot and updates its rows' trailing columns.
+// A zero pivot records info (min over the launch, atomicMin on getrf_info) and
+// skips the division (LAPACK continues).  Candidate slots are double-buffered
+// by column parity (a CTA can be at most one barrier ahead of another).
+__global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
+  if (ld_info(a.d_info) != 0) return;
+  extern __shared__ double sm[];
+  const int w = a.w, R = a.rows_per_cta;
+  const int g = blockIdx.x, G = gridDim.x;
+  const int r0 = g * R;
+  const int rows = max(0, min(R, a.m - r0));
+  double* sP = sm;                          // rows x w, row-major with stride w + 1
+  const int sld = kGetf2Max + 1;
+  double* sPiv = sP + (size_t)R * sld;      // the pivot row (w)
+  double* sDiag = sPiv + kGetf2Max;         // the old row j (w)
+  __shared__ double red_v[kGetf2Threads / 32];
+  __shared__ int red_i[kGetf2Threads / 32];
+  __shared__ int s_p;
+  for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
+    const int r = e % rows, c = e / rows;
+    sP[r * sld + c] = a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld];
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jmax = min(a.m, w);  // pivots exist for the first min(m, w) columns
+  for (int j = 0; j < jmax; ++j) {
+    // (a) local first maximum of |a(i, j)| over owned rows i >= j
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const int gi = r0 + r;
+      if (gi < j) continue;
+      const double v = fabs(sP[r * sld + j]);
+      if (v > bv || (v == bv && gi < bi)) { bv = v; bi = gi; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+      bv = lane < kGetf2Threads / 32 ? red_v[lane] : -1.0;
+      bi = lane < kGetf2Threads / 32 ? red_i[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+    }
+    // (b) publish: value, index and the candidate row; the owner of row j publishes it too
+    const int buf = j & 1;
+    double* slot_row = a.cand_rows + ((int64_t)buf * G + g) * kGetf2Max;
+    if (threadIdx.x == 0) {
+      a.cand_val[buf * G + g] = bv;
+      a.cand_idx[buf * G + g] = bi;
+    }
+    __syncthreads();
+    const int cand_local = __shfl_sync(0xffffffffu, bi, 0) - r0;  // valid in warp 0 only
+    if (warp == 0 && bi != 0x7fffffff)
+      for (int c = lane; c < w; c += 32) slot_row[c] = sP[cand_local * sld + c];
+    if (j >= r0 && j < r0 + rows)
+      for (int c = threadIdx.x; c < w; c += blockDim.x) a.diag_row[buf * kGetf2Max + c] = sP[(j - r0) * sld + c];
+    // (c) barrier
+    grid_sync(a.bar, phase);
+    // (d) global first maximum
+    if (warp == 0) {
+      double v = -1.0;
+      int i = 0x7fffffff, who = -1;
+      for (int q = lane; q < G; q += 32) {
+        const double qv = __ldcg(a.cand_val + buf * G + q);
+        const int qi = __ldcg(a.cand_idx + buf * G + q);
+        if (qi != 0x7fffffff && (qv > v || (qv == v && qi < i))) { v = qv; i = qi; who = q; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+        if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; who = ow; }
+      }
+      if (lane == 0) s_p = i;
+      const double* wr = a.cand_rows + ((int64_t)buf * G + who) * kGetf2Max;
+      for (int c = lane; c < w; c += 32) {
+        sPiv[c] = __ldcg(wr + c);
+        sDiag[c] = __ldcg(a.diag_row + buf * kGetf2Max + c);
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    // (e) interchange rows j and p among the owned rows
+    if (p != j) {
+      if (j >= r0 && j < r0 + rows)
+        for (int c = threadIdx.x; c < w; c += blockDim.x) sP[(j - r0) * sld + c] = sPiv[c];
+      if (p >= r0 && p < r0 + rows)
+        for (int c = threadIdx.x; c < w; c += blockDim.x) sP[(p - r0) * sld + c] = sDiag[c];
+    }
+    if (g == 0 && threadIdx.x == 0) {
+      a.ipiv[j] = a.pivot_base + p;
+      if (sPiv[j] == 0.0) atomicMin(a.getrf_info, a.info_base + j + 1);
+    }
+    __syncthreads();
+    // (f) multipliers and the rank-1 update of the owned rows below row j
+    const double piv = sPiv[j];
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const int gi = r0 + r;
+      if (gi <= j) continue;
+      double l = sP[r * sld + j];
+      if (piv != 0.0) l = l / piv;
+      sP[r * sld + j] = l;
+      for (int c = j + 1; c < w; ++c) sP[r * sld + c] -= l * sPiv[c];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
+    const int r = e % rows, c = e / rows;
+    a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld] = sP[r * sld + c];
+  }
+}
+
+// Row interchanges: for k = k0 .. k1-1 (in order) swap rows k and ipiv[k] - base
+// of the columns [0, ncols) of A (layout 0).  One thread per column.
+__global__ void k_laswp(XLaswpArgs a) {
+  if (ld_info(a.d_info) != 0) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.ncols) return;
+  double* col = a.A + (int64_t)c * a.ld;
+  for (int k = a.k0; k < a.k1; ++k) {
+    const int p = a.ipiv[k] - a.base;
+    if (p != k) {
+      const double t = col[k];
+      col[k] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_tri_rows(const XTriArgs& a, cudaStream_t st) {
+  if (a.m <= 0 || a.t <= 0) return cudaSuccess;
+  if (a.t > kTriMax) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * (size_t)(kTriMax + kTriRows) * kTriLd;
+  k_tri_rows<<<(a.m + kTriRows - 1) / kTriRows, kTriRows, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trti2(const XBlockArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  if (a.n > kTriMax) return cudaErrorInvalidValue;
+  k_trti2<<<1, kTriMax, 2 * sizeof(double) * kTriMax * kTriLd, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lauu2(const XBlockArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  if (a.n > kTriMax) return cudaErrorInvalidValue;
+  k_lauu2<<<1, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diag_check(const double* A, int64_t ld, int layout, int n, int* d_info, cudaStream_t st) {
+  k_diag_check<<<1, 256, 0, st>>>(A, ld, layout, n, d_info);
+  return cudaGetLastError();
+}
+
+size_t getf2_smem(int rows_per_cta) {
+  return sizeof(double) * ((size_t)rows_per_cta * (kGetf2Max + 1) + 2 * kGetf2Max);
+}
+
+cudaError_t launch_getf2(const XGetf2Args& a, int grid, cudaStream_t st) {
+  if (a.m <= 0 || a.w <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGetf2Threads);
+  cfg.dynamicSmemBytes = getf2_smem(a.rows_per_cta);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_getf2, a);
+}
+
+cudaError_t launch_laswp(const XLaswpArgs& a, cudaStream_t st) {
+  if (a.ncols <= 0 || a.k1 <= a.k0) return cudaSuccess;
+  k_laswp<<<(a.ncols + 127) / 128, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t configure_xkernels() {
+  cudaError_t e = cudaFuncSetAttribute(k_tri_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * (kTriMax + kTriRows) * kTriLd));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_trti2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(2 * sizeof(double) * kTriMax * kTriLd));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_getf2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+}  // namespace relapack

@@ -103,7 +103,9 @@ def test_update_hot_instantiations(lay, tile, tma):
     for M, N, K, tri, ks in cases:
         ch = _run_update(M, N, K, la, lb, lc, tri, tile, tma, ks)
         assert ch[0] == tile and ch[2] == ks
-        assert bool(ch[1]) == tma, f"TMA path expected {tma}, got {ch}"
+        # TMA needs even leading dimensions (layout 0: ld = rows, 1: ld = K)
+        even = (K % 2 == 0) if la == 1 else (M % 2 == 0 and N % 2 == 0)
+        assert bool(ch[1]) == (tma and even), f"TMA path expected {tma and even}, got {ch}"
 
 
 @pytest.mark.parametrize("lay", HOT)
