@@ -36,6 +36,18 @@ CONFIGS = {
     "n65536": (65536, "L", "uniform", 3),
     "batch": (None, "L", "uniform", 4),
 }
+# §8(f) rows: the paper's other recursive operations, measured with the
+# same harness (GFLOP/s of the leading-term flop count, % of FP64 peak).
+# name: (flops(n, nrhs), description)
+NEXT = {
+    "trtri": (lambda n, r: n ** 3 / 3.0, "recursive dtrtri (N1), uplo L, the Cholesky factor of the CFG recipe"),
+    "trtri_blocked": (lambda n, r: n ** 3 / 3.0, "blocked dtrtri (N1/N2 comparison), block --block"),
+    "potrf_blocked": (lambda n, r: n ** 3 / 3.0, "blocked right-looking dpotrf (N2), block --block, CFG recipe"),
+    "lauum": (lambda n, r: n ** 3 / 3.0, "recursive dlauum (N3), L^T L of the Cholesky factor"),
+    "potri": (lambda n, r: 2.0 * n ** 3 / 3.0, "dpotri (N3): dtrtri + dlauum of the Cholesky factor"),
+    "potrs": (lambda n, r: 2.0 * n * n * r, "dpotrs (N3): two recursive triangular solves, --nrhs right-hand sides"),
+    "getrf": (lambda n, r: 2.0 * n ** 3 / 3.0, "recursive dgetrf with partial pivoting (N4), A ~ U(-1,1)"),
+}
 FP64_PEAK_TFLOPS_DATASHEET = 37.0  # HGX B200 FP64 / FP64 tensor core datasheet figure
 
 
@@ -148,7 +160,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="n16384", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="n16384", choices=sorted(CONFIGS) + sorted(NEXT))
+    ap.add_argument("--n", type=int, default=16384, help="order for the §8(f) configs")
+    ap.add_argument("--block", type=int, default=128, help="block size of the blocked algorithms")
+    ap.add_argument("--nrhs", type=int, default=1024, help="right-hand sides of potrs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -162,6 +177,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config in NEXT:
+        return run_next(args, rank, world, local_rank)
     n, uplo, dist, cfg_idx = CONFIGS[args.config]
     flops_per_step = n ** 3 / 3.0 if n else None
 
@@ -466,6 +483,211 @@ def run_batch(args, rank, world, dev):
                 if e2e_ms else None),
         "info_parity": "per-matrix info == closed form (k+1 for the 1% negated diagonals)",
     }
+    print(json.dumps(out))
+    return 0
+
+
+def run_next(args, rank, world, local_rank):
+    """One §8(f) operation per step on a fresh copy of its input (restored from a
+    pristine device copy, untimed; inputs >= 2 GiB at n = 16384 > L2).  Replicas
+    only at N > 1 (these operations are not sharded)."""
+    import numpy as np
+    import torch
+
+    import paper_1602_06763_b200 as rl
+    from inputs import gen
+
+    n, op, r = args.n, args.config, args.nrhs
+    flops_fn, desc = NEXT[op]
+    flops = flops_fn(n, r)
+    if args.impl == "reference":
+        return run_next_reference(args, rank, world, op, n, r, flops_fn, desc)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    st = torch.cuda.current_stream(dev)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    if op == "getrf":
+        g = gen.philox(args.seed, 40)
+        P = torch.empty((n, n), dtype=torch.float64, device=dev)
+        for r0 in range(0, n, 4096):
+            P[r0:r0 + 4096] = torch.from_numpy(g.uniform(-1.0, 1.0, size=(min(4096, n - r0), n))).to(dev)
+        P = P.t()  # column-major view
+    else:
+        P = gen.spd_torch(n, args.seed, dist="uniform", device=dev)
+        if op not in ("potrf_blocked",):
+            assert rl.dpotrf(P, "L") == 0  # the factor the triangular operations start from
+    W = torch.empty_like(P.t()).t()
+    B0 = B = None
+    if op == "potrs":
+        g = gen.philox(args.seed, 41)
+        B0 = torch.from_numpy(g.uniform(-1, 1, size=(r, n))).to(dev).t()
+        B = torch.empty_like(B0.t()).t()
+    ipiv = torch.zeros(n, dtype=torch.int32, device=dev)
+
+    def call():
+        if op == "trtri":
+            return rl.dtrtri(W, "L", stream=st)
+        if op == "trtri_blocked":
+            return rl.dtrtri_blocked(W, args.block, "L", stream=st)
+        if op == "potrf_blocked":
+            return rl.dpotrf_blocked(W, args.block, "L", stream=st)
+        if op == "lauum":
+            return rl.dlauum(W, "L", stream=st)
+        if op == "potri":
+            return rl.dpotri(W, "L", stream=st)
+        if op == "potrs":
+            return rl.dpotrs(W, B, "L", stream=st)
+        return rl.dgetrf(W, ipiv, stream=st)
+
+    def step():
+        W.copy_(P)
+        if B is not None:
+            B.copy_(B0)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        info = call()  # synchronous call: info read back inside the timed region
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        assert info == 0, f"info={info}"
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(local_rank) as clk:
+        times = [step() for _ in range(args.steps)]
+    ms = sum(times) / len(times)
+    if world > 1:
+        ms = _max_over_ranks(ms, world, dev)
+    val = flops / (ms / 1e3) / 1e9 * world
+    # per-kind breakdown (serial replay with events on the launch stream)
+    prof = None
+    if not args.no_profile and op != "potrf_blocked":
+        W.copy_(P)
+        if B is not None:
+            B.copy_(B0)
+        torch.cuda.synchronize(dev)
+        prof = rl.xprofile(call)
+    elif not args.no_profile:
+        W.copy_(P)
+        torch.cuda.synchronize(dev)
+        rl.profile_enable(True)
+        try:
+            rl.profile_reset()
+            call()
+            prof = {k: rl.profile_read(k) for k in ("potf2", "trsm", "gemm", "syrk")}
+            rl.profile_reset()
+        finally:
+            rl.profile_enable(False)
+        prof["gemm"] = tuple(a + b for a, b in zip(prof["gemm"], prof.pop("syrk")))
+    roofline = None
+    if prof and "gemm" in prof and prof["gemm"][0] > 0:
+        ach = prof["gemm"][1] / (prof["gemm"][0] / 1e3) / 1e12
+        roofline = {"kernel": "k_update (mixed-layout DMMA GEMM/SYRK of the plan)", "bound": "tensor",
+                    "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS_DATASHEET, "unit": "TFLOP/s",
+                    "frac": round(ach / FP64_PEAK_TFLOPS_DATASHEET, 4), "traffic": None,
+                    "peak_note": "builder-measured DMMA peak 37.05 TF (datasheet 37.0 TF); MEASURED_PEAKS.json "
+                                 "has no FP64 entry", "timing": "serial per-launch CUDA events (no graph)"}
+    out = {
+        "metric": f"{op} FP64 GFLOP/s and % of FP64 peak", "value": round(val, 2), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded Philox)",
+        "config": {"workload": f"{desc}, n={n}" + (f", nrhs={r}" if op == "potrs" else "")
+                   + (f", block={args.block}" if "blocked" in op else ""), "n": n,
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs restored from a pristine device copy between steps (untimed)"},
+        "pct_fp64_peak": round(100 * val / 1e3 / world / FP64_PEAK_TFLOPS_DATASHEET, 2),
+        "roofline": roofline,
+        "kernel_share": {k: {"ms": round(v[0], 3), "launches": v[2],
+                             "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 3) if v[0] > 0 else 0.0}
+                         for k, v in (prof or {}).items()},
+        "step_times_ms": [round(t, 4) for t in times],
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and rank == 0:
+        out["cpu_baseline"] = next_cpu_baseline(op, n, r, args.seed)
+    if rank == 0:
+        print(json.dumps(out))
+    return 0
+
+
+def _next_oracle_case(op, m, r, seed):
+    """Host input of the oracle sample (order m) and the call that times it."""
+    import numpy as np
+
+    import oracle
+    from inputs import gen
+
+    if op == "getrf":
+        A = np.asfortranarray(gen.philox(seed, 40).uniform(-1, 1, size=(m, m)))
+        return A, lambda X: oracle.dgetrf(X)[0]
+    A = np.asfortranarray(gen.spd(m, seed))
+    if op == "potrf_blocked":
+        return A, lambda X: oracle.dpotrf(X, "L")
+    assert oracle.dpotrf(A, "L") == 0
+    if op in ("trtri", "trtri_blocked"):
+        return A, lambda X: oracle.dtrtri(X, "L")
+    if op == "lauum":
+        return A, lambda X: oracle.dlauum(X, "L")
+    if op == "potri":
+        return A, lambda X: oracle.dpotri(X, "L")
+    Bh = np.asfortranarray(gen.philox(seed, 41).uniform(-1, 1, size=(m, r)))
+    return A, lambda X: oracle.dpotrs(X, np.array(Bh, order="F"), "L")
+
+
+def next_cpu_baseline(op, n, r, seed, target_s=6.0):
+    """The oracle as it stands on a bounded sample: the same operation at a
+    smaller order m (doubling from 512 until a call takes ~target_s / 4)."""
+    import numpy as np
+
+    import oracle
+
+    flops_fn = NEXT[op][0]
+    m = 512
+    while True:
+        A, fn = _next_oracle_case(op, m, r, seed)
+        X = np.array(A, order="F")
+        t0 = time.perf_counter()
+        fn(X)
+        dt = time.perf_counter() - t0
+        if dt > target_s / 4 or m >= n:
+            break
+        m = min(n, 2 * m)
+    return {"value": round(flops_fn(m, r) / dt / 1e9, 3), "unit": "GFLOP/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "sample": f"the same operation at n={m} (of {n}){', nrhs=' + str(r) if op == 'potrs' else ''}"
+                                          f": {flops_fn(m, r):.3e} flops in {dt:.2f} s"}
+
+
+def run_next_reference(args, rank, world, op, n, r, flops_fn, desc):
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    base = next_cpu_baseline(op, n, r, args.seed)
+    m = int(base["sample"].split("n=")[1].split(" ")[0])
+    A, fn = _next_oracle_case(op, m, r, args.seed)
+    times = []
+    for i in range(args.warmup + args.steps):
+        X = np.array(A, order="F")
+        t0 = time.perf_counter()
+        fn(X)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    val = flops_fn(m, r) / sec / 1e9
+    out = {"impl": "reference", "metric": f"{op} FP64 GFLOP/s and % of FP64 peak", "value": round(val, 3),
+           "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(1e3 * sec, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (seeded Philox)", "config": {"workload": f"{desc}, n={n}", "n": n},
+           "cpu_baseline": dict(base, value=round(val, 3)),
+           "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
 

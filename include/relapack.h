@@ -298,6 +298,13 @@ RELAPACK_API void relapack_dgetrf(const int* m, const int* n, double* A, const i
 RELAPACK_API void relapack_dpotrf_blocked(const char* uplo, const int* n, double* A, const int* lda, int nb,
                                           int* info);
 RELAPACK_API int relapack_xplan_count(int op, int n, int nb, int* kinds, int max_kinds, double* flops);
+/* Per-kind profiling of these plans (bench.py): while enabled, plans run
+ * serially in plan order (no graph) with CUDA events around every launch;
+ * read returns the summed ms, leading-term flops and launch count of one op
+ * kind (as relapack_xplan_count's kinds) since the last reset. */
+RELAPACK_API int relapack_xprofile_enable(int on);
+RELAPACK_API int relapack_xprofile_read(int kind, double* ms_total, double* flops_total, int* launches);
+RELAPACK_API void relapack_xprofile_reset(void);
 
 /*
  * Kernel test hooks (synchronous; test infrastructure, not a production API).

@@ -131,6 +131,11 @@ def lib():
         L.relapack_xplan_count.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_int), c_int,
                                            ctypes.POINTER(c_double)]
         L.relapack_xplan_count.restype = c_int
+        L.relapack_xprofile_enable.argtypes = [c_int]
+        L.relapack_xprofile_enable.restype = c_int
+        L.relapack_xprofile_read.argtypes = [c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_double), ip]
+        L.relapack_xprofile_read.restype = c_int
+        L.relapack_xprofile_reset.restype = None
         _lib = L
     return _lib
 
@@ -504,6 +509,28 @@ def xplan_count(op: str, n: int, nb: int = 0):
     kinds = (ctypes.c_int * max(cnt, 1))()
     lib().relapack_xplan_count(code, n, nb, kinds, cnt, ctypes.byref(fl))
     return cnt, list(kinds)[:cnt], fl.value
+
+
+XKINDS = {"gemm": 0, "tri": 1, "trti2": 2, "lauu2": 3, "potf2": 4, "getf2": 5, "laswp": 6, "check": 7}
+
+
+def xprofile(fn):
+    """Run fn() with the §8(f) plans profiled per kind; returns {kind: (ms, flops, launches)}."""
+    L = lib()
+    L.relapack_xprofile_reset()
+    L.relapack_xprofile_enable(1)
+    try:
+        fn()
+        out = {}
+        for k, v in XKINDS.items():
+            ms, fl, cnt = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_int(0)
+            L.relapack_xprofile_read(v, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(cnt))
+            if cnt.value:
+                out[k] = (ms.value, fl.value, cnt.value)
+        return out
+    finally:
+        L.relapack_xprofile_enable(0)
+        L.relapack_xprofile_reset()
 
 
 def split_point(n: int, align: int) -> int:

@@ -265,10 +265,13 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
 #if RELAPACK_BATCH_MODE == 1  // tools/microbench only: memory phases alone
     const int fail = 0;
 #else
-    const int fail = reg_potrf<NMAX / 8>(v, lane);
+    int fail = reg_potrf<NMAX / 8>(v, lane);
 #endif
-    // store the lower triangle of L (only the uplo triangle is written)
-    if (n == NMAX) {
+    // store the lower triangle of L (only the uplo triangle is written); a
+    // pivot below kTinyPivotBound: the matrix (still unmodified) is redone exactly
+    if (fail == kTinyPivot) {
+      fail = potf2_exact_global(A, lda, LAYOUT, n, lane);
+    } else if (n == NMAX) {
       // full class size: only diagonal tiles need a predicate; one lane base
       // pointer, tile offsets are (i, k) multiples of 8 rows / columns
       double* Al = A + lv_off(LAYOUT, g, 2 * t, lda);

@@ -90,27 +90,47 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // (truncation ~ 5e^3/16 < 2^-66; ~1 ulp after rounding): four dependent FP64
 // operations after the MUFU instead of six for two Newton steps — this is on
 // the per-column critical path of every base-case factorization.
-// The MUFU flushes subnormal inputs to zero (.ftz): a positive pivot below
-// 2^-1000 takes the approximation of d * 2^128 scaled back by 2^64 (exact
-// power-of-two scalings) in an out-of-line call behind a branch, so the usual
-// chain only gains a compare that runs beside the MUFU (ptxas if-converts an
-// inline version into predicated ops whose latency the chain would pay).
-static __device__ __noinline__ double rsqrt_approx_tiny(double d) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d * 0x1p+128));
-  return y * 0x1p+64;
-}
-
+// The MUFU flushes subnormal inputs to zero (.ftz), so a pivot below
+// kTinyPivotBound would give inf / NaN here; the base-case kernels detect such
+// pivots off the chain (like a failed one) and redo the block with
+// potf2_exact_global (exact sqrt and division) before anything is stored.
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-#ifndef RELAPACK_RSQRT_NO_TINY  // (A/B experiments only: the round-1 chain without the subnormal branch)
-  if (d < 0x1p-1000) y = rsqrt_approx_tiny(d);
-#endif
   const double p = d * y;
   const double e = fma(-p, y, 1.0);
   const double t = fma(0.375, e, 0.5);
   return fma(y * e, t, y);
+}
+
+// Pivots d with 0 < d < kTinyPivotBound take the exact slow path (rsqrt_nr).
+constexpr double kTinyPivotBound = 0x1p-1000;
+// Marker a base-case factorization returns instead of a failing column when a
+// pivot was positive but below kTinyPivotBound.
+constexpr int kTinyPivot = 1 << 24;
+
+// Unblocked Cholesky of the n x n L-view block in GLOBAL memory by one warp,
+// right-looking, correctly rounded sqrt and true division (subnormal pivots
+// handled by IEEE arithmetic).  The rare fallback of the base-case kernels for
+// blocks with a pivot below kTinyPivotBound (the block is still unmodified in
+// global memory when it runs).  Returns 0 or the 1-based failing column.
+static __device__ __noinline__ int potf2_exact_global(double* A, int64_t ld, int layout, int n, int lane) {
+  for (int j = 0; j < n; ++j) {
+    const double d = A[lv_off(layout, j, j, ld)];
+    if (!(d > 0.0)) return j + 1;
+    const double l = sqrt(d);
+    __syncwarp();
+    if (lane == 0) A[lv_off(layout, j, j, ld)] = l;
+    for (int i = j + 1 + lane; i < n; i += 32) A[lv_off(layout, i, j, ld)] = A[lv_off(layout, i, j, ld)] / l;
+    __syncwarp();
+    for (int k = j + 1; k < n; ++k) {
+      const double lkj = A[lv_off(layout, k, j, ld)];
+      for (int i = k + lane; i < n; i += 32)
+        A[lv_off(layout, i, k, ld)] = A[lv_off(layout, i, k, ld)] - A[lv_off(layout, i, j, ld)] * lkj;
+    }
+    __syncwarp();
+  }
+  return 0;
 }
 
 // sqrt(d) from y ~ 1/sqrt(d): r = d*y corrected by one fma-exact residual step

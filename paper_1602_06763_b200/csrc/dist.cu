@@ -20,8 +20,10 @@
 
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/relapack.h"
@@ -45,6 +47,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok() const { return h && GetUniqueId && CommInitRank && CommDestroy && AllGather && AllReduce; }
 };
@@ -68,6 +72,8 @@ static NcclApi& nccl() {
   api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
   api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+  api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(api.h, "ncclCommGetAsyncError");
+  api.CommAbort = (decltype(api.CommAbort))dlsym(api.h, "ncclCommAbort");
   return api;
 }
 
@@ -80,10 +86,12 @@ struct relapack_comm {
   int nranks = 1, rank = 0, device = 0;
   ncclComm_t nccl = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t capture = nullptr;  // graph capture of the distributed plan
   int* d_info = nullptr;  // 2 ints: local info, reduced info
-  // single-entry schedule cache (key: n, lda, layout, nb, dist_min, c, T)
+  bool aborted = false;
+  // single-entry schedule cache (key: n, lda, layout, nb, dist_min, c, T, A)
   relapack::DistPlan* plan = nullptr;
-  long long key[7] = {-1, -1, -1, -1, -1, -1, -1};
+  std::string key;
 };
 
 namespace relapack {
@@ -164,14 +172,22 @@ struct DistPlan {
   std::vector<UpdateOp> upd;           // GEMM/SYRK descriptors (by op index)
   std::vector<int*> d_rows;            // PACK/UNPACK row tables (by op index)
   std::vector<int> rows_pad;           // by op index (PACK/UNPACK/ALLGATHER/TRSM on send)
+  std::vector<int> ncols;              // columns of the current packed chunk (by op index)
   double* send = nullptr;
   double* recv = nullptr;
   int64_t send_elems = 0;
+  double* splitk_ws = nullptr;         // split-K partials (graph executor)
+  int* splitk_cnt = nullptr;
+  size_t cnt_bytes = 0;
+  cudaGraphExec_t exec = nullptr;      // the whole distributed plan, collectives included
   ~DistPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
     for (int* p : d_rows)
       if (p) cudaFree(p);
     if (send) cudaFree(send);
     if (recv) cudaFree(recv);
+    if (splitk_ws) cudaFree(splitk_ws);
+    if (splitk_cnt) cudaFree(splitk_cnt);
   }
 };
 
@@ -290,6 +306,49 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
   return 0;
 }
 
+// One op of the graph executor: kernels as run_local (update descriptors built
+// once, with split-K), the all-gather as an NCCL call on the capturing stream.
+static cudaError_t launch_dist_op(DistPlan& dp, size_t i, int layout, double* A, int64_t lda, int* d_info,
+                                  const DistParams& d, relapack_comm* comm, cudaStream_t st) {
+  const PlanOp& op = dp.ops[i];
+  const int pad = dp.rows_pad[i], nc = dp.ncols[i];
+  int64_t ldc = 0;
+  switch (op.kind) {
+    case OP_POTF2:
+      return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, lda), lda, layout, op.n, d_info, op.info_base, st);
+    case OP_TRSM: {
+      double* B = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
+      return launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, lda), lda, B, ldc, layout, op.m, op.k, d_info, st);
+    }
+    case OP_GEMM:
+    case OP_SYRK:
+      return launch_update(dp.upd[i], st);
+    case OP_PACK: {
+      const int64_t total = (int64_t)pad * op.k;
+      k_pack_rows<<<grid_for(total), 256, 0, st>>>(A, lda, layout, dp.d_rows[i] + (size_t)d.rank * pad, pad, op.c_j,
+                                                   op.k, dp.send, d_info);
+      return cudaGetLastError();
+    }
+    case OP_UNPACK: {
+      const int64_t total = (int64_t)pad * op.k * d.nranks;
+      k_unpack_rows<<<grid_for(total), 256, 0, st>>>(A, lda, layout, dp.d_rows[i], pad, d.nranks, op.c_j, op.k,
+                                                     dp.recv, d_info);
+      return cudaGetLastError();
+    }
+    case OP_ALLGATHER: {
+      const size_t cnt = (size_t)pad * op.k;
+      const ncclResult_t r = nccl().AllGather(dp.send, dp.recv, cnt, ncclDouble_, comm->nccl, st);
+      if (r != 0) {
+        set_error(std::string("ncclAllGather: ") + (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+        return cudaErrorUnknown;
+      }
+      return cudaSuccess;
+    }
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 // Column count of the current packed chunk for every op (TRSM/GEMM on BUF_SEND).
 static std::vector<int> chunk_cols(const DistPlan& dp) {
   std::vector<int> nc(dp.ops.size(), 0);
@@ -348,7 +407,11 @@ int relapack_comm_init(relapack_comm_t** comm, const char uid[128], int nranks, 
     delete c;
     return cuda_fail(e, "comm init");
   }
-  if (nranks > 1) {
+  if ((e = cudaStreamCreateWithFlags(&c->capture, cudaStreamNonBlocking)) != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "comm init");
+  }
+  {  // the communicator exists at every world size (world 1 included: the same path)
     NcclApi& api = nccl();
     if (!api.ok()) {
       set_error("relapack_comm_init: libnccl.so.2 not loadable (set RELAPACK_NCCL_LIB)");
@@ -372,8 +435,9 @@ void relapack_comm_destroy(relapack_comm_t* comm) {
   if (!comm) return;
   if (comm->plan) destroy_dist_plan(comm->plan);
   if (comm->d_info) cudaFree(comm->d_info);
-  if (comm->nccl && nccl().ok()) nccl().CommDestroy(comm->nccl);
+  if (comm->nccl && nccl().ok()) (comm->aborted ? 0 : nccl().CommDestroy(comm->nccl));
   if (comm->stream) cudaStreamDestroy(comm->stream);
+  if (comm->capture) cudaStreamDestroy(comm->capture);
   delete comm;
 }
 
@@ -424,48 +488,114 @@ void relapack_dpotrf_dist(const char* uplo, const int* n_, double* A, const int*
     *info = cuda_fail(e, "configure");
     return;
   }
-  cudaMemsetAsync(d_info, 0, 2 * sizeof(int), st);
-  const long long key[7] = {n, (long long)lda, layout, nb, dist_min, pp.crossover, pp.split_tile};
-  if (!comm->plan || memcmp(key, comm->key, sizeof(key)) != 0) {
+  if (comm->aborted) {
+    set_error("relapack_dpotrf_dist: the communicator was aborted after an earlier NCCL failure / timeout");
+    *info = -1000;
+    return;
+  }
+  char kb[256];
+  snprintf(kb, sizeof(kb), "n%d ld%lld l%d nb%d dm%d c%d T%d tb%d la%d ld%d b21%d A%p", n, (long long)lda, layout,
+           nb, dist_min, pp.crossover, pp.split_tile, pp.trsm_base, (int)pp.lookahead, pp.lookahead_depth,
+           pp.b21_chunks, (void*)A);
+  if (!comm->plan || comm->key != kb) {
     if (comm->plan) destroy_dist_plan(comm->plan);
     comm->plan = new DistPlan();
-    memcpy(comm->key, key, sizeof(key));
-    int r0 = build_exec(*comm->plan, n, layout, pp, d);
+    comm->key = kb;
+    DistPlan& dp = *comm->plan;
+    int r0 = build_exec(dp, n, layout, pp, d);
+    cudaGraph_t g = nullptr;
+    if (r0 == 0) {
+      dp.ncols = chunk_cols(dp);
+      // update descriptors (the packed send buffer or the matrix), split-K
+      // slots from the DAG's ancestor sets, then one capture of the whole plan
+      dp.upd.assign(dp.ops.size(), UpdateOp{});
+      for (size_t i = 0; i < dp.ops.size(); ++i) {
+        const PlanOp& op = dp.ops[i];
+        if (op.kind != OP_GEMM && op.kind != OP_SYRK) continue;
+        int64_t ldc = 0, lda_ = 0, ldb = 0;
+        const int pad = dp.rows_pad[i], nc = dp.ncols[i];
+        double* C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
+        const double* Ap = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, dp.send, pad, nc, &lda_);
+        const double* Bp = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, dp.send, pad, nc, &ldb);
+        const bool syrk = op.kind == OP_SYRK;
+        init_update(dp.upd[i], C, ldc, layout, Ap, lda_, layout, Bp, ldb, layout, syrk ? op.n : op.m, op.n, op.k,
+                    -1.0, syrk ? 1 : 0);
+        dp.upd[i].args.d_info = d_info;
+      }
+      std::vector<std::vector<int>> deps;
+      std::vector<uint64_t> anc;
+      compute_deps(dp.ops, deps, &anc);
+      if ((e = setup_splitk_ops(dp.ops, dp.upd, &anc, &dp.splitk_ws, &dp.splitk_cnt, &dp.cnt_bytes)) != cudaSuccess)
+        r0 = cuda_fail(e, "dist split-K");
+      if (r0 == 0 && (e = cudaStreamBeginCapture(comm->capture, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        r0 = cuda_fail(e, "dist capture");
+      if (r0 == 0) {
+        cudaError_t er = cudaMemsetAsync(d_info, 0, 2 * sizeof(int), comm->capture);
+        if (er == cudaSuccess && dp.splitk_cnt) er = cudaMemsetAsync(dp.splitk_cnt, 0, dp.cnt_bytes, comm->capture);
+        std::vector<cudaGraphNode_t> nodes;
+        std::vector<char> cls;
+        if (er == cudaSuccess)
+          er = capture_plan_dag(
+              dp.ops, deps, comm->capture,
+              [&](size_t i, cudaStream_t s2) { return launch_dist_op(dp, i, layout, A, lda, d_info, d, comm, s2); },
+              nodes, cls);
+        // info identical on every rank (every rank computes the same replicated
+        // leaves; this all-reduce(max) is the guard the ABI promises)
+        if (er == cudaSuccess &&
+            nccl().AllReduce(d_info, d_info + 1, 1, ncclInt32_, ncclMax_, comm->nccl, comm->capture) != 0)
+          er = cudaErrorUnknown;
+        if (er == cudaSuccess)
+          er = cudaMemcpyAsync(d_info, d_info + 1, sizeof(int), cudaMemcpyDeviceToDevice, comm->capture);
+        e = cudaStreamEndCapture(comm->capture, &g);
+        if (er == cudaSuccess && e == cudaSuccess && (e = set_node_priorities(nodes, cls)) == cudaSuccess)
+          e = cudaGraphInstantiateWithFlags(&dp.exec, g, cudaGraphInstantiateFlagUseNodePriority);
+        if (er != cudaSuccess) r0 = cuda_fail(er, "dist capture (launch)");
+        else if (e != cudaSuccess) r0 = cuda_fail(e, "dist graph");
+      }
+      if (g) cudaGraphDestroy(g);
+    }
     if (r0 != 0) {
       destroy_dist_plan(comm->plan);
       comm->plan = nullptr;
+      comm->key.clear();
       *info = r0;
       return;
     }
   }
   DistPlan& dp = *comm->plan;
-  int r = 0;
-  std::vector<int> nc = chunk_cols(dp);
-  size_t beg = 0;
-  for (size_t i = 0; i <= dp.ops.size(); ++i) {
-    if (i < dp.ops.size() && dp.ops[i].kind != OP_ALLGATHER) continue;
-    r = run_local(dp, beg, i, layout, A, lda, d_info, d, d.rank, st, nc);
-    if (r != 0) break;
-    if (i < dp.ops.size()) {
-      const size_t cnt = (size_t)dp.rows_pad[i] * dp.ops[i].k;
-      if (d.nranks > 1) {
-        ncclResult_t nr = nccl().AllGather(dp.send, dp.recv, cnt, ncclDouble_, comm->nccl, st);
-        if (nr != 0) {
-          r = -1000 - nr;
-          set_error("ncclAllGather failed");
-          break;
-        }
-      } else {
-        cudaMemcpyAsync(dp.recv, dp.send, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
-      }
-    }
-    beg = i + 1;
+  if ((e = cudaGraphLaunch(dp.exec, st)) != cudaSuccess) {
+    *info = cuda_fail(e, "dist launch");
+    return;
   }
-  if (r == 0 && d.nranks > 1) {
-    // make info identical everywhere (every rank already computes the same
-    // leaves; this is the consistency guard the ABI promises)
-    nccl().AllReduce(d_info, d_info + 1, 1, ncclInt32_, ncclMax_, comm->nccl, st);
-    cudaMemcpyAsync(d_info, d_info + 1, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  // wait, polling NCCL's asynchronous error state and a timeout (SURVEY §5:
+  // a peer that died must not hang the caller forever)
+  const char* tv = getenv("RELAPACK_DIST_TIMEOUT_S");
+  const double timeout_s = tv ? atof(tv) : 600.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  int r = 0;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      r = cuda_fail(q, "dist wait");
+      break;
+    }
+    ncclResult_t ae = 0;
+    if (nccl().CommGetAsyncError && nccl().CommGetAsyncError(comm->nccl, &ae) == 0 && ae != 0 && ae != 7 /*inProgress*/) {
+      set_error(std::string("NCCL asynchronous error: ") + (nccl().GetErrorString ? nccl().GetErrorString(ae) : "?"));
+      r = -1000 - (int)ae;
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (r == 0 && el > timeout_s) {
+      set_error("relapack_dpotrf_dist: timed out waiting for the collectives (RELAPACK_DIST_TIMEOUT_S)");
+      r = -1999;
+    }
+    if (r != 0) {
+      if (nccl().CommAbort) nccl().CommAbort(comm->nccl);
+      comm->aborted = true;
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
   int h = 0;
   if (r == 0) {

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <list>
 #include <map>
 #include <memory>
@@ -217,20 +218,20 @@ static void fill_update(UpdateOp& u, const PlanOp& op, double* A, int64_t ld, in
 // workspace slot.  Two split-K updates share a slot only if one is an
 // ancestor of the other in the dependency DAG (`anc`, or the serial order
 // when anc is null), so concurrently runnable updates never share partials.
-static cudaError_t setup_splitk(Plan& p, const std::vector<uint64_t>* anc) {
-  const size_t nops = p.ops.size(), words = (nops + 63) / 64;
+cudaError_t setup_splitk_ops(const std::vector<PlanOp>& ops, std::vector<UpdateOp>& upd,
+                             const std::vector<uint64_t>* anc, double** ws_out, int** cnt_out, size_t* cnt_bytes) {
+  const size_t nops = ops.size(), words = (nops + 63) / 64;
   int64_t ws = 0;
   int cnt = 0;
   std::vector<int> slot_last;  // last op assigned to each slot
   std::vector<int> slot_of(nops, -1);
   for (size_t i = 0; i < nops; ++i) {
-    if (p.ops[i].kind != OP_GEMM && p.ops[i].kind != OP_SYRK) continue;
-    UpdateArgs& a = p.upd[i].args;
-    const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, p.upd[i].tile,
-                                     p.ops[i].kind == OP_SYRK && !p.ops[i].deferred);
+    if (ops[i].kind != OP_GEMM && ops[i].kind != OP_SYRK) continue;
+    UpdateArgs& a = upd[i].args;
+    const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, upd[i].tile, ops[i].kind == OP_SYRK && !ops[i].deferred);
     if (ks <= 1) continue;
     a.ksplit = ks;
-    const int64_t e = update_ws_elems(a.M, a.N, a.tri, p.upd[i].tile, ks);
+    const int64_t e = update_ws_elems(a.M, a.N, a.tri, upd[i].tile, ks);
     ws = e > ws ? e : ws;
     cnt = a.ntiles > cnt ? a.ntiles : cnt;
     int s = -1;
@@ -245,19 +246,26 @@ static cudaError_t setup_splitk(Plan& p, const std::vector<uint64_t>* anc) {
     slot_last[s] = (int)i;
     slot_of[i] = s;
   }
+  *ws_out = nullptr;
+  *cnt_out = nullptr;
+  *cnt_bytes = 0;
   if (ws == 0) return cudaSuccess;
   const size_t nslots = slot_last.size();
   cudaError_t e;
-  if ((e = cudaMalloc(&p.splitk_ws, nslots * ws * sizeof(double))) != cudaSuccess) return e;
-  p.cnt_bytes = nslots * cnt * sizeof(int);
-  if ((e = cudaMalloc(&p.splitk_cnt, p.cnt_bytes)) != cudaSuccess) return e;
-  if ((e = cudaMemset(p.splitk_cnt, 0, p.cnt_bytes)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(ws_out, nslots * ws * sizeof(double))) != cudaSuccess) return e;
+  *cnt_bytes = nslots * cnt * sizeof(int);
+  if ((e = cudaMalloc(cnt_out, *cnt_bytes)) != cudaSuccess) return e;
+  if ((e = cudaMemset(*cnt_out, 0, *cnt_bytes)) != cudaSuccess) return e;
   for (size_t i = 0; i < nops; ++i) {
     if (slot_of[i] < 0) continue;
-    p.upd[i].args.ws = p.splitk_ws + (size_t)slot_of[i] * ws;
-    p.upd[i].args.counters = p.splitk_cnt + (size_t)slot_of[i] * cnt;
+    upd[i].args.ws = *ws_out + (size_t)slot_of[i] * ws;
+    upd[i].args.counters = *cnt_out + (size_t)slot_of[i] * cnt;
   }
   return cudaSuccess;
+}
+
+static cudaError_t setup_splitk(Plan& p, const std::vector<uint64_t>* anc) {
+  return setup_splitk_ops(p.ops, p.upd, anc, &p.splitk_ws, &p.splitk_cnt, &p.cnt_bytes);
 }
 
 // ------------------------------------------------------------------ profiling
@@ -483,24 +491,25 @@ static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, in
 // Capture the plan as a DAG on one stream: before each op the capture
 // dependencies are set to the graph nodes of the op's footprint
 // dependencies, so independent ops (the lookahead trailing updates and the
-// next panel's chain) become parallel branches of the graph.  Deferred ops
-// get the lowest node priority, the rest the highest.
-static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int>>& deps, double* A, int64_t ld,
-                               int layout, int* d_info, cudaStream_t st, std::vector<cudaGraphNode_t>& nodes,
-                               std::vector<char>& deferred_node) {
-  cudaError_t e = run_prologue(pl, d_info, st);
-  if (e != cudaSuccess) return e;
+// next panel's chain) become parallel branches of the graph.  `launch(i, st)`
+// issues op i; cls receives each op's priority class (set_node_priorities).
+// Used by the single-GPU executor and by the multi-GPU one (dist.cu, whose
+// collectives are captured nodes too).
+cudaError_t capture_plan_dag(const std::vector<PlanOp>& ops, const std::vector<std::vector<int>>& deps,
+                             cudaStream_t st, const std::function<cudaError_t(size_t, cudaStream_t)>& launch,
+                             std::vector<cudaGraphNode_t>& nodes, std::vector<char>& deferred_node) {
+  cudaError_t e;
   cudaStreamCaptureStatus cs;
   const cudaGraphNode_t* cur = nullptr;
   size_t ncur = 0;
   if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;
   if (ncur != 1) return cudaErrorStreamCaptureInvalidated;
   const cudaGraphNode_t root = cur[0];
-  nodes.assign(pl.ops.size(), nullptr);
+  nodes.assign(ops.size(), nullptr);
   std::vector<cudaGraphNode_t> want;
   std::vector<cudaGraphEdgeData> edge;
-  auto kernel_op = [&](int j) { return pl.ops[j].kind <= OP_SYRK && !(debug_skip_mask() >> pl.ops[j].kind & 1); };
-  for (size_t i = 0; i < pl.ops.size(); ++i) {
+  auto kernel_op = [&](int j) { return ops[j].kind <= OP_SYRK && !(debug_skip_mask() >> ops[j].kind & 1); };
+  for (size_t i = 0; i < ops.size(); ++i) {
     want.clear();
     edge.clear();
     for (int d : deps[i]) {
@@ -512,9 +521,9 @@ static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int
       // dependents' CTAs on the SMs the chain needs
       cudaGraphEdgeData x{};
       const int pm = pdl_mode();
-      const OpKind dk = pl.ops[i].kind;
-      const bool into = pm == 1 || dk == OP_POTF2 || dk == OP_TRSM || (pm == 3 && dk == OP_SYRK && !pl.ops[i].deferred);
-      if (pm > 0 && into && kernel_op((int)i) && kernel_op(d) && !pl.ops[d].deferred) {
+      const OpKind dk = ops[i].kind;
+      const bool into = pm == 1 || dk == OP_POTF2 || dk == OP_TRSM || (pm == 3 && dk == OP_SYRK && !ops[i].deferred);
+      if (pm > 0 && into && kernel_op((int)i) && kernel_op(d) && !ops[d].deferred) {
         x.from_port = cudaGraphKernelNodePortProgrammatic;
         x.type = cudaGraphDependencyTypeProgrammatic;
       }
@@ -527,28 +536,37 @@ static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int
     if ((e = cudaStreamUpdateCaptureDependencies_v2(st, want.data(), edge.data(), want.size(),
                                                     cudaStreamSetCaptureDependencies)) != cudaSuccess)
       return e;
-    if ((e = launch_op(pl, i, A, ld, layout, d_info, st)) != cudaSuccess) return e;
+    if ((e = launch(i, st)) != cudaSuccess) return e;
     if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;
     if (ncur != 1) return cudaErrorStreamCaptureInvalidated;
     nodes[i] = cur[0];
     // priority class: 2 deferred update, 1 other GEMM (the TRSM's updates),
     // 0 the chain (base cases, TRSM bases, the non-deferred SYRKs)
-    const PlanOp& o = pl.ops[i];
+    const PlanOp& o = ops[i];
     deferred_node.push_back((char)(o.deferred ? (o.flops >= bulk_min_flops() ? 3 : 2) : o.kind == OP_GEMM ? 1 : 0));
   }
   // join every sink so the capture ends on one node
-  std::vector<char> has_succ(pl.ops.size(), 0);
-  for (size_t i = 0; i < pl.ops.size(); ++i)
+  std::vector<char> has_succ(ops.size(), 0);
+  for (size_t i = 0; i < ops.size(); ++i)
     for (int d : deps[i]) has_succ[d] = 1;
   want.clear();
-  for (size_t i = 0; i < pl.ops.size(); ++i)
+  for (size_t i = 0; i < ops.size(); ++i)
     if (!has_succ[i]) want.push_back(nodes[i]);
-  if (!want.empty())
-    e = cudaStreamUpdateCaptureDependencies(st, want.data(), want.size(), cudaStreamSetCaptureDependencies);
-  return e;
+  if (want.empty()) want.push_back(root);
+  return cudaStreamUpdateCaptureDependencies(st, want.data(), want.size(), cudaStreamSetCaptureDependencies);
 }
 
-static cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes, const std::vector<char>& deferred) {
+static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int>>& deps, double* A, int64_t ld,
+                               int layout, int* d_info, cudaStream_t st, std::vector<cudaGraphNode_t>& nodes,
+                               std::vector<char>& deferred_node) {
+  cudaError_t e = run_prologue(pl, d_info, st);
+  if (e != cudaSuccess) return e;
+  return capture_plan_dag(
+      pl.ops, deps, st, [&](size_t i, cudaStream_t s) { return launch_op(pl, i, A, ld, layout, d_info, s); }, nodes,
+      deferred_node);
+}
+
+cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes, const std::vector<char>& deferred) {
   int least = 0, greatest = 0;
   cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
   if (e != cudaSuccess) return e;

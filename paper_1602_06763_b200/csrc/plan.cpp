@@ -184,6 +184,7 @@ void append_trsm(int l_off, int b_buf, int b_i, int b_j, int m, int k, int level
 // ---------------------------------------------------------------- dependencies
 void op_regions(const PlanOp& op, Rect* w, Rect* r1, Rect* r2) {
   const Rect none{-1, 0, 0, 0, 0};
+  constexpr int kAll = 1 << 30;
   *r1 = none;
   *r2 = none;
   switch (op.kind) {
@@ -210,7 +211,19 @@ void op_regions(const PlanOp& op, Rect* w, Rect* r1, Rect* r2) {
       *w = none;
       *r1 = Rect{BUF_A, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.k};
       break;
-    default:  // pack / all-gather / unpack: treat as a barrier over everything
+    case OP_PACK:  // owned rows of an A block -> the send buffer
+      *w = Rect{BUF_SEND, 0, kAll, 0, kAll};
+      *r1 = Rect{BUF_A, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.k};
+      break;
+    case OP_ALLGATHER:
+      *w = Rect{BUF_RECV, 0, kAll, 0, kAll};
+      *r1 = Rect{BUF_SEND, 0, kAll, 0, kAll};
+      break;
+    case OP_UNPACK:  // every rank's rows -> the A block
+      *w = Rect{BUF_A, op.c_i, op.c_i + op.m, op.c_j, op.c_j + op.k};
+      *r1 = Rect{BUF_RECV, 0, kAll, 0, kAll};
+      break;
+    default:  // unknown: a barrier over everything
       *w = Rect{-2, 0, 0, 0, 0};
       break;
   }
@@ -304,7 +317,7 @@ void exchange_rows(DistCtx& x, int lo, int hi, int c0, int ncols, int level) {
 
 void dist_potrf(DistCtx& x, int off, int n, int level, int info_base) {
   if (n <= 0) return;
-  if (n < x.d.dist_min || x.d.nranks == 1) {
+  if (n < x.d.dist_min) {
     // replicated leaf: gather the block's rows (their owners hold the updated
     // values) and factor it redundantly on every rank (same info everywhere)
     if (x.d.nranks > 1) exchange_rows(x, off, off + n, off, n, level);

@@ -206,9 +206,13 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
     }
   }
   int fail = 0;
+  bool tiny = false;
 #pragma unroll
-  for (int c = kPanel - 1; c >= 0; --c)
+  for (int c = kPanel - 1; c >= 0; --c) {
     if (c < w && !(dpiv[c] > 0.0)) fail = j0 + c + 1;  // catches d <= 0, -0.0 and NaN
+    if (c < w && dpiv[c] > 0.0 && dpiv[c] < kTinyPivotBound) tiny = true;
+  }
+  if (tiny) fail = kTinyPivot;  // redone exactly by the kernel (rsqrt_nr)
   // diagonal entries l_jj = sqrt(d), off the critical path
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -320,9 +324,13 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   copy_lower<kBaseMax, true>(s, A, ld, layout, n);
   __syncthreads();
   PROBE(1);
-  const int fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
+  int fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
   pdl_trigger();
-  copy_lower<kBaseMax, false>(s, A, ld, layout, n);
+  if (fail == kTinyPivot) {
+    if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
+  } else {
+    copy_lower<kBaseMax, false>(s, A, ld, layout, n);
+  }
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
   PROBE(63);
   trace_end(tr);
@@ -340,10 +348,14 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   copy_lower<64, true>(s, A, ld, layout, n);
   __syncthreads();
   PROBE(1);
-  const int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
+  int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
   PROBE(62);
   pdl_trigger();
-  copy_lower<64, false>(s, A, ld, layout, n);
+  if (fail == kTinyPivot) {
+    if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
+  } else {
+    copy_lower<64, false>(s, A, ld, layout, n);
+  }
   PROBE(63);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
   trace_end(tr);
@@ -643,7 +655,10 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   PROBE(51);
   int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
   PROBE(52);
-  if (fail == 0) {
+  if (fail == kTinyPivot) {  // the block is untouched in global memory: redo it exactly
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
+  } else if (fail == 0) {
     const int n2 = n - kN1;
     if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -659,13 +674,20 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     __syncthreads();
     PROBE(54);
     fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
-    if (fail) fail += kN1;
     PROBE(55);
     pdl_trigger();
-#if !RELAPACK_NODE_EARLY_STORE
-    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
+    if (fail == kTinyPivot) {
+#if RELAPACK_NODE_EARLY_STORE
+#error "the exact fallback needs the block unmodified in global memory"
 #endif
-    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
+      if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
+    } else {
+      if (fail) fail += kN1;
+#if !RELAPACK_NODE_EARLY_STORE
+      copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
+#endif
+      copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
+    }
   } else {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     PROBE(55);
@@ -697,17 +719,21 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
         const int r = 8 * i + g, c = 8 * k + 2 * t + q;
         v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(layout, r, c, ld)] : (r == c ? 1.0 : 0.0);
       }
-  const int fail = reg_potrf<TN>(v, lane);
+  int fail = reg_potrf<TN>(v, lane);
   pdl_trigger();
+  if (fail == kTinyPivot) {
+    fail = potf2_exact_global(A, ld, layout, n, lane);
+  } else {
 #pragma unroll
-  for (int i = 0; i < TN; ++i)
+    for (int i = 0; i < TN; ++i)
 #pragma unroll
-    for (int k = 0; k <= i; ++k)
+      for (int k = 0; k <= i; ++k)
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-        if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q];
-      }
+        for (int q = 0; q < 2; ++q) {
+          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+          if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q];
+        }
+  }
   if (fail && fail <= n && lane == 0) *d_info = info_base + fail;
   trace_end(tr);
 }

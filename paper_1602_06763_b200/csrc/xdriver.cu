@@ -154,6 +154,8 @@ cudaError_t setup_exec(XExec& x, const std::vector<uint64_t>& anc) {
   int cnt = 0;
   std::vector<int> slot_last, slot_of(n, -1);
   int nget = 0;
+  cudaError_t e;
+  if ((e = cudaMalloc(&x.d_info, 4 * sizeof(int))) != cudaSuccess) return e;  // before the descriptors use it
   for (size_t i = 0; i < n; ++i) {
     const XOp& o = x.ops[i];
     if (o.kind == XK_GETF2) x.slot[i] = nget++;
@@ -179,8 +181,6 @@ cudaError_t setup_exec(XExec& x, const std::vector<uint64_t>& anc) {
     slot_last[s] = (int)i;
     slot_of[i] = s;
   }
-  cudaError_t e;
-  if ((e = cudaMalloc(&x.d_info, 4 * sizeof(int))) != cudaSuccess) return e;
   if (ws > 0) {
     const size_t nslots = slot_last.size();
     if ((e = cudaMalloc(&x.splitk_ws, nslots * ws * sizeof(double))) != cudaSuccess) return e;
@@ -247,9 +247,34 @@ cudaError_t capture(const XExec& x, const std::vector<std::vector<int>>& deps, c
   return cudaGetLastError();
 }
 
+// Profiling (bench.py's per-kernel-class breakdown of these plans): with
+// relapack_xprofile_enable(1) plans run serially in plan order with CUDA
+// events around every launch, accumulated per op kind.
+struct XProfRec {
+  cudaEvent_t a, b;
+  int kind;
+  double flops;
+};
+std::mutex g_xprof_mu;
+std::vector<XProfRec> g_xprof;
+int g_xprof_on = 0;
+
 cudaError_t run_serial(const XExec& x, cudaStream_t st) {
   cudaError_t e = run_prologue(x, st);
-  for (size_t i = 0; i < x.ops.size() && e == cudaSuccess; ++i) e = launch_xop(x, i, st);
+  for (size_t i = 0; i < x.ops.size() && e == cudaSuccess; ++i) {
+    XProfRec r{nullptr, nullptr, (int)x.ops[i].kind, x.ops[i].flops};
+    if (g_xprof_on) {
+      cudaEventCreate(&r.a);
+      cudaEventCreate(&r.b);
+      cudaEventRecord(r.a, st);
+    }
+    e = launch_xop(x, i, st);
+    if (g_xprof_on) {
+      cudaEventRecord(r.b, st);
+      std::lock_guard<std::mutex> lk(g_xprof_mu);
+      g_xprof.push_back(r);
+    }
+  }
   if (e == cudaSuccess) {
     k_xepilogue<<<1, 1, 0, st>>>(x.d_info);
     e = cudaGetLastError();
@@ -271,14 +296,6 @@ bool x_graphs() {
   return !(v && v[0] == '0');
 }
 
-// Profiling hook (bench.py's per-kernel-class roofline): with
-// RELAPACK_XPROFILE=1 the plan runs serially with events around every op.
-struct XProf {
-  std::mutex mu;
-  std::vector<std::pair<int, double>> kind_ms;  // (kind, ms)
-  std::vector<double> flops;
-};
-XProf g_xprof;
 
 // Build (or fetch) and launch the plan; returns 0 or an error code.
 int x_run(const std::string& key, const std::vector<XOp>& ops_in, const XBuffers& bufs, bool is_getrf,
@@ -295,7 +312,7 @@ int x_run(const std::string& key, const std::vector<XOp>& ops_in, const XBuffers
       return cuda_fail(e, "capture stream");
     c.configured = true;
   }
-  const bool graphs = x_graphs();
+  const bool graphs = x_graphs() && !g_xprof_on;
   const std::string full = key + (graphs ? " g1" : " g0");
   XExec* x = nullptr;
   for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
@@ -524,6 +541,40 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
                           " A" + ptr_key(A) + " P" + ptr_key(ipiv) + params_key(p);
   int r = x_run(key, ops, b, true, false, current_stream_or(nullptr), info);
   if (r != 0) *info = r;
+}
+
+int relapack_xprofile_enable(int on) {
+  g_xprof_on = on ? 1 : 0;
+  return 0;
+}
+
+int relapack_xprofile_read(int kind, double* ms_total, double* flops_total, int* launches) {
+  std::lock_guard<std::mutex> lk(g_xprof_mu);
+  double ms = 0, fl = 0;
+  int cnt = 0;
+  for (const XProfRec& r : g_xprof) {
+    if (r.kind != kind) continue;
+    float t = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms += t;
+    fl += r.flops;
+    ++cnt;
+  }
+  if (ms_total) *ms_total = ms;
+  if (flops_total) *flops_total = fl;
+  if (launches) *launches = cnt;
+  return 0;
+}
+
+void relapack_xprofile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_xprof_mu);
+  for (XProfRec& r : g_xprof) {
+    cudaEventSynchronize(r.b);
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_xprof.clear();
 }
 
 int relapack_xplan_count(int op, int n, int nb, int* kinds_out, int max_kinds, double* flops_out) {

@@ -130,11 +130,12 @@ def test_update_shapes_sweep(M, N, K):
 def test_update_odd_ld_and_misaligned():
     """Odd leading dimension and a base off 16-byte alignment fall back to the plain-load path."""
     for la in (0, 1):
-        ch = _run_update(200, 170, 129, la, la, la, 0, 0, True, 1, pad=1)
+        # odd ld: layout 0 has ld = rows + pad (200 + 1, 170 + 1), layout 1 ld = K + pad (129 + 2)
+        ch = _run_update(200, 170, 129, la, la, la, 0, 0, True, 1, pad=1 if la == 0 else 2)
         assert ch[1] == 0
         ch = _run_update(200, 170, 129, la, la, la, 0, 0, True, 1, odd=True)
         assert ch[1] == 0
-        ch = _run_update(170, 170, 129, la, la, la, 1, 0, True, 1, pad=2)
+        ch = _run_update(170, 170, 129, la, la, la, 1, 0, True, 1, pad=2 if la == 0 else 1)
         assert ch[1] == 1
 
 
