@@ -376,7 +376,8 @@ def run_batch(args, rank, world, dev):
 
     count = args.batch_count
     b = gen.batched_spd(count, args.seed)
-    lo, hi = rank * count // world, (rank + 1) * count // world
+    bounds = rl.batch_split(b["ns"], world)  # contiguous ranges balanced by sum n^3 (library split, §8e)
+    lo, hi = bounds[rank], bounds[rank + 1]
     ns = b["ns"][lo:hi]
     offs = b["offsets"][lo:hi] - (b["offsets"][lo] if hi > lo else 0)
     base = int(b["offsets"][lo]) if hi > lo else 0

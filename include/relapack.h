@@ -116,6 +116,16 @@ RELAPACK_API int relapack_dpotrf_async(char uplo, int n, double* A, int lda, int
 RELAPACK_API int relapack_dpotrf_batched(char uplo, int batch, const int* d_n, double* const* d_A, const int* d_lda,
                             int* d_info, relapack_stream_t stream);
 
+/*
+ * relapack_batch_split — host-only: the multi-GPU split of a batch (SURVEY
+ * §8e "independent batched small factorizations are simply split across
+ * GPUs"): contiguous ranges [bounds[r], bounds[r+1]) of the batch, r = 0 ..
+ * nranks-1, balanced by the leading-term work sum n_b^3 (n: HOST array of
+ * the batch's orders).  Each rank then calls relapack_dpotrf_batched on its
+ * range; no collective is needed in the data path.  Returns 0 or -1.
+ */
+RELAPACK_API int relapack_batch_split(int batch, const int* n, int nranks, int* bounds);
+
 /* ---- multi-GPU: one process per GPU, NCCL over NVLink ---- */
 typedef struct relapack_comm relapack_comm_t;
 

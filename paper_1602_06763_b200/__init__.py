@@ -136,6 +136,8 @@ def lib():
         L.relapack_xprofile_read.argtypes = [c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_double), ip]
         L.relapack_xprofile_read.restype = c_int
         L.relapack_xprofile_reset.restype = None
+        L.relapack_batch_split.argtypes = [c_int, c_void_p, c_int, c_void_p]
+        L.relapack_batch_split.restype = c_int
         _lib = L
     return _lib
 
@@ -531,6 +533,17 @@ def xprofile(fn):
     finally:
         L.relapack_xprofile_enable(0)
         L.relapack_xprofile_reset()
+
+
+def batch_split(ns, nranks: int):
+    """Host-only: contiguous per-rank ranges of a batch balanced by sum n^3 (list of nranks + 1 bounds)."""
+    import numpy as np
+
+    h = np.ascontiguousarray(ns, dtype=np.int32)
+    out = np.zeros(nranks + 1, dtype=np.int32)
+    if lib().relapack_batch_split(len(h), h.ctypes.data, int(nranks), out.ctypes.data) != 0:
+        raise ValueError("bad batch split arguments")
+    return [int(x) for x in out]
 
 
 def split_point(n: int, align: int) -> int:

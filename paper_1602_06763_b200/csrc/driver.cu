@@ -1084,6 +1084,28 @@ void relapack_dpotrf_blocked(const char* uplo, const int* n_, double* A, const i
   *info = *ds->h_info;
 }
 
+int relapack_batch_split(int batch, const int* n, int nranks, int* bounds) {
+  if (batch < 0 || nranks < 1 || !bounds || (batch > 0 && !n)) return -1;
+  // contiguous ranges balanced by the leading-term work sum n_b^3 / 3 (SURVEY
+  // §8e: the batch is split across GPUs, no collective in the data path)
+  std::vector<double> pre((size_t)batch + 1, 0.0);
+  for (int b = 0; b < batch; ++b) {
+    const double nb = n[b] > 0 ? (double)n[b] : 0.0;
+    pre[b + 1] = pre[b] + nb * nb * nb;
+  }
+  bounds[0] = 0;
+  int cur = 0;
+  for (int r = 1; r < nranks; ++r) {
+    const double target = pre[batch] * r / nranks;
+    while (cur < batch && pre[cur + 1] <= target) ++cur;
+    // the boundary closer to the target (ties: the earlier one)
+    if (cur < batch && pre[cur + 1] - target < target - pre[cur]) ++cur;
+    bounds[r] = cur > bounds[r - 1] ? cur : bounds[r - 1];
+  }
+  bounds[nranks] = batch;
+  return 0;
+}
+
 void relapack_set_stream(relapack_stream_t stream) {
   g_stream = reinterpret_cast<cudaStream_t>(stream);
   g_stream_set = 1;

@@ -199,3 +199,59 @@ def test_dist_schedule_structure():
         per.append(sum(2.0 * o["m"] * o["n"] * o["k"] if o["kind"] == "gemm" else o["n"] ** 2 * o["k"]
                        for o in s if o["kind"] in ("gemm", "syrk") and o["level"] == 1 and o["c_buf"] == 0))
     assert max(per) / min(per) < 1.35
+
+
+# ---------------------------------------------------------------- batched split (CFG[4] across GPUs)
+def _batch_worker(rank, nranks, port, count, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    import oracle
+    import paper_1602_06763_b200 as rl
+    from inputs import gen
+
+    b = gen.batched_spd(count, 5)
+    bounds = rl.batch_split(b["ns"], nranks)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    # this rank's range: the oracle stands in for relapack_dpotrf_batched on CPU
+    ns = b["ns"][lo:hi]
+    offs = b["offsets"][lo:hi] - (b["offsets"][lo] if hi > lo else 0)
+    end = int(b["offsets"][hi - 1] + int(b["ns"][hi - 1]) ** 2) if hi > lo else int(b["offsets"][lo]) if lo < count else 0
+    sub = b["buf"][int(b["offsets"][lo]) if hi > lo else 0:end].copy() if hi > lo else np.zeros(0)
+    info = oracle.dpotrf_batched("L", ns, sub, offs, ns) if hi > lo else np.zeros(0, np.int32)
+    # gather every rank's infos (the optional info gather of §8e) and range sizes
+    sizes = [None] * nranks
+    dist.all_gather_object(sizes, (lo, hi, info.tolist(), float((ns.astype(np.float64) ** 3).sum())))
+    if rank == 0:
+        q.put(sizes)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_batched_split_gloo(nranks):
+    """Each rank takes its contiguous range from the library's split, factors it
+    (oracle on CPU), and the gathered per-matrix infos equal the closed form for
+    the whole batch; the ranges partition the batch and balance sum n^3."""
+    from inputs import gen
+
+    count = 3000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, nranks, port, count, q)) for r in range(nranks)]
+    for p in procs:
+        p.start()
+    sizes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    b = gen.batched_spd(count, 5)
+    los = [s[0] for s in sizes]
+    his = [s[1] for s in sizes]
+    assert los[0] == 0 and his[-1] == count and all(his[r] == los[r + 1] for r in range(nranks - 1))
+    infos = np.concatenate([np.array(s[2], dtype=np.int32) for s in sizes])
+    assert np.array_equal(infos, b["expected_info"])
+    work = [s[3] for s in sizes]
+    assert max(work) / (sum(work) / nranks) < 1.01  # balanced within 1 %
