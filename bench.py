@@ -127,12 +127,36 @@ def gen_matrix(n, uplo, dist, seed, device):
     return gen.spd_torch(n, seed, dist=dist, device=device)  # (n, n) column-major, exactly symmetric
 
 
-def cpu_oracle_sample(A_host, n, uplo, target_s=12.0):
-    """Oracle (as it stands) on a bounded sample of the same factorization:
-    the first J columns of the left-looking loop on the full n x n matrix."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_oracle_sample(A_host, n, uplo, full_max=16384):
+    """The oracle as it stands on the host cores.  Up to n = full_max the WHOLE
+    factorization of the same matrix (~100 s at n = 16384 on 16 cores: the
+    representative rate, every column's k-loop at its real length); beyond,
+    the first J columns of the left-looking loop (a bounded sample)."""
     import numpy as np
 
     import oracle
+
+    if n <= full_max:
+        X = np.array(A_host, order="F", copy=True)
+        t0 = time.perf_counter()
+        info = oracle.dpotrf(X, uplo)
+        dt = time.perf_counter() - t0
+        assert info == 0
+        fl = n ** 3 / 3.0
+        return {"value": round(fl / dt / 1e9, 3), "unit": "GFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                "cpu": _cpu_model(), "nproc": os.cpu_count(),
+                "sample": f"the whole n={n} uplo={uplo} factorization of the same matrix "
+                          f"(left-looking triple loop, {fl:.3e} flops in {dt:.1f} s)"}
 
     def run(J):
         X = np.array(A_host, order="F", copy=True)
@@ -147,10 +171,11 @@ def cpu_oracle_sample(A_host, n, uplo, target_s=12.0):
 
     J = min(n, 128)
     dt = run(J)
-    while dt < target_s / 4 and J < n:
+    while dt < 3.0 and J < n:
         J = min(n, J * 2)
         dt = run(J)
     return {"value": flops(J) / dt / 1e9, "unit": "GFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "cpu": _cpu_model(), "nproc": os.cpu_count(),
             "sample": f"first {J} of {n} columns of the n={n} uplo={uplo} factorization "
                       f"(left-looking triple loop, {flops(J):.3e} flops in {dt:.2f} s)"}
 
@@ -291,6 +316,7 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
     upd_fl = res["gemm"][1] + res["syrk"][1]
     upd_n = res["gemm"][2] + res["syrk"][2]
     achieved = upd_fl / (upd_ms / 1e3) / 1e12 if upd_ms > 0 else 0.0
+    in_graph = _in_graph_update_rate(rl, W, P, d_info, uplo, st, dev, upd_fl)
     traffic, traffic_note = _committed_traffic(W.shape[0])
     roofline = {
         "kernel": "k_update (SYRK + recursive-TRSM GEMM, DMMA.8x8x4)",
@@ -303,8 +329,11 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
         "traffic": traffic,
         "traffic_note": traffic_note,
         "launches_per_step": upd_n,
-        "peak_note": "FP64 datasheet 37 TF (measured DMMA microbenchmark 37.05 TF at 1965 MHz, "
-                     "profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 entry",
+        "timing": "achieved = algorithmic flops of the update launches / their summed CUDA-event durations in a "
+                  "serial (eager, one launch at a time) pass on the launch stream",
+        "in_graph": in_graph,
+        "peak_note": "builder-measured DMMA peak 37.05 TF at 1965 MHz (profiles/fp64_peak_r01.txt; the HGX B200 "
+                     "datasheet FP64 figure is 37.0 TF, used as the denominator); MEASURED_PEAKS.json has no FP64 entry",
     }
     total_prof = sum(v[0] for v in res.values())
     share = {k: {"ms": round(v[0], 3), "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 3) if v[0] > 0 else 0.0,
@@ -313,6 +342,42 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
     share["graph_step_ms"] = round(ms_per_step, 3)
     share["profiled_kernel_sum_ms"] = round(total_prof, 3)
     return roofline, share
+
+
+def _in_graph_update_rate(rl, W, P, d_info, uplo, st, dev, upd_fl):
+    """The update kernels inside the captured graph (RELAPACK_TRACE=1: every
+    kernel records its first-CTA start and last-CTA end): the union of their
+    busy intervals, the step span, and the update flops over that union."""
+    import torch
+
+    os.environ["RELAPACK_TRACE"] = "1"
+    try:
+        for _ in range(2):  # capture the traced plan, then the traced replay read back
+            W.copy_(P)
+            torch.cuda.synchronize(dev)
+            rl.dpotrf_async(W, d_info, uplo, stream=st)
+            torch.cuda.synchronize(dev)
+        recs = rl.trace_records()
+    finally:
+        os.environ.pop("RELAPACK_TRACE", None)
+    iv = sorted((r["t0_us"], r["t1_us"]) for r in recs if r["kind"] in ("gemm", "syrk") and r["t1_us"] >= 0)
+    ivall = [(r["t0_us"], r["t1_us"]) for r in recs if r["t1_us"] >= 0]
+    if not iv or not ivall:
+        return None
+    busy, cs, ce = 0.0, iv[0][0], iv[0][1]
+    for a, b in iv[1:]:
+        if a > ce:
+            busy += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    busy += ce - cs
+    span = max(b for _, b in ivall) - min(a for a, _ in ivall)
+    return {"update_busy_ms": round(busy / 1e3, 3), "step_span_ms": round(span / 1e3, 3),
+            "tflops_over_busy": round(upd_fl / (busy / 1e6) / 1e12, 3),
+            "frac_over_busy": round(upd_fl / (busy / 1e6) / 1e12 / FP64_PEAK_TFLOPS_DATASHEET, 4),
+            "note": "union of the update kernels' [first-CTA start, last-CTA end] intervals inside the captured "
+                    "graph (%globaltimer, RELAPACK_TRACE=1 replay of the same plan)"}
 
 
 def _committed_traffic(n):
@@ -817,29 +882,22 @@ def run_reference(args, rank, n, uplo, dist, cfg_idx, world):
         sample = f"first {S} of {args.batch_count} matrices of the CFG[4] batch"
         workload = f"batched dpotrf, {args.batch_count} matrices n~U{{16,32,48,64}} (BASELINE.json configs[4])"
     else:
-        J = min(n, 256)
-        A = _host_panel(n, max(J, min(n, 2048)), args.seed, dist, uplo)
-        Jmax = max(J, min(n, 2048))
-        # size the sample: ~3 s per step
-        while True:
-            X = np.array(A, order="F")
-            t0 = time.perf_counter()
-            oracle.dpotrf_cols(X, uplo, J)
-            dt = time.perf_counter() - t0
-            if dt > 0.75 or J >= Jmax:
-                break
-            J = min(Jmax, J * 2)
-        sample_flops = sum(2.0 * j * (n - j) for j in range(J))
+        # each step: the WHOLE factorization (left-looking triple loop, every
+        # column's k-loop at full length) of the same recipe at order m =
+        # min(n, 4096) — a bounded step (~1.6 s on 16 cores)
+        m = min(n, 4096)
+        A = gen.spd(m, args.seed, dist=dist)
+        sample_flops = m ** 3 / 3.0
         times = []
         for i in range(args.warmup + args.steps):
             X = np.array(A, order="F")
             t0 = time.perf_counter()
-            info = oracle.dpotrf_cols(X, uplo, J)
+            info = oracle.dpotrf(X, uplo)
             dt = time.perf_counter() - t0
             assert info == 0
             if i >= args.warmup:
                 times.append(dt)
-        sample = (f"first {J} of {n} columns of the n={n} uplo={uplo} factorization "
+        sample = (f"the whole factorization of the same recipe at n={m} (of {n}), uplo={uplo} "
                   f"(left-looking triple loop, {sample_flops:.3e} flops per step)")
         workload = f"single dpotrf n={n} uplo={uplo} B~{dist} (BASELINE.json configs[{cfg_idx}])"
     sec = sum(times) / len(times)

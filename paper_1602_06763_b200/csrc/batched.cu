@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
     int fail = reg_potrf<NMAX / 8>(v, lane);
 #endif
     // store the lower triangle of L (only the uplo triangle is written); a
-    // pivot below kTinyPivotBound: the matrix (still unmodified) is redone exactly
-    if (fail == kTinyPivot) {
+    // flushed (subnormal) pivot: the matrix (still unmodified) is redone exactly
+    if (reg_diag_nonfinite<NMAX / 8>(v, n, fail, lane)) {
       fail = potf2_exact_global(A, lda, LAYOUT, n, lane);
     } else if (n == NMAX) {
       // full class size: only diagonal tiles need a predicate; one lane base

@@ -90,10 +90,10 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // (truncation ~ 5e^3/16 < 2^-66; ~1 ulp after rounding): four dependent FP64
 // operations after the MUFU instead of six for two Newton steps — this is on
 // the per-column critical path of every base-case factorization.
-// The MUFU flushes subnormal inputs to zero (.ftz), so a pivot below
-// kTinyPivotBound would give inf / NaN here; the base-case kernels detect such
-// pivots off the chain (like a failed one) and redo the block with
-// potf2_exact_global (exact sqrt and division) before anything is stored.
+// The MUFU flushes subnormal inputs to zero (.ftz), so a positive subnormal
+// pivot gives inf / NaN here; the base-case kernels detect the resulting
+// non-finite diagonal after the factorization (off the chain) and redo the
+// block with potf2_exact_global (exact sqrt and division) before storing.
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
@@ -103,16 +103,10 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return fma(y * e, t, y);
 }
 
-// Pivots d with 0 < d < kTinyPivotBound take the exact slow path (rsqrt_nr).
-constexpr double kTinyPivotBound = 0x1p-1000;
-// Marker a base-case factorization returns instead of a failing column when a
-// pivot was positive but below kTinyPivotBound.
-constexpr int kTinyPivot = 1 << 24;
-
 // Unblocked Cholesky of the n x n L-view block in GLOBAL memory by one warp,
 // right-looking, correctly rounded sqrt and true division (subnormal pivots
 // handled by IEEE arithmetic).  The rare fallback of the base-case kernels for
-// blocks with a pivot below kTinyPivotBound (the block is still unmodified in
+// blocks with a flushed (subnormal) pivot (the block is still unmodified in
 // global memory when it runs).  Returns 0 or the 1-based failing column.
 static __device__ __noinline__ int potf2_exact_global(double* A, int64_t ld, int layout, int n, int lane) {
   for (int j = 0; j < n; ++j) {

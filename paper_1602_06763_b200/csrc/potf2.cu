@@ -206,13 +206,9 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
     }
   }
   int fail = 0;
-  bool tiny = false;
 #pragma unroll
-  for (int c = kPanel - 1; c >= 0; --c) {
+  for (int c = kPanel - 1; c >= 0; --c)
     if (c < w && !(dpiv[c] > 0.0)) fail = j0 + c + 1;  // catches d <= 0, -0.0 and NaN
-    if (c < w && dpiv[c] > 0.0 && dpiv[c] < kTinyPivotBound) tiny = true;
-  }
-  if (tiny) fail = kTinyPivot;  // redone exactly by the kernel (rsqrt_nr)
   // diagonal entries l_jj = sqrt(d), off the critical path
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -273,6 +269,18 @@ __device__ int potf2_smem(double* s, int n, int* fail_flag) {
   return *fail_flag;
 }
 
+// A non-finite diagonal entry l_jj before the first failed column (`fail`,
+// 0 = none) means a positive pivot the MUFU flushed (subnormal, rsqrt_nr; the
+// NaN it leaves makes a later pivot fail) — the caller then redoes the block
+// exactly.  A genuine failure (d <= 0 or NaN) has only finite l_jj before it.
+// One barrier, off the chain.
+__device__ __forceinline__ bool diag_nonfinite(const double* s, int n, int fail, int lds) {
+  const int lim = fail ? fail - 1 : n;
+  bool bad = false;
+  for (int k = threadIdx.x; k < lim; k += blockDim.x) bad |= !isfinite(s[k * (lds + 1)]);
+  return __syncthreads_or(bad) != 0;
+}
+
 // Copy of the lower triangle of the L-view block between global memory and
 // shared memory, coalesced along the contiguous index (layout N: rows; layout
 // T: columns of L), 32 loads of a thread in flight at once.
@@ -326,7 +334,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   PROBE(1);
   int fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
   pdl_trigger();
-  if (fail == kTinyPivot) {
+  if (diag_nonfinite(s, n, fail, P2<kBaseMax>::LDS)) {
     if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
   } else {
     copy_lower<kBaseMax, false>(s, A, ld, layout, n);
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
   PROBE(62);
   pdl_trigger();
-  if (fail == kTinyPivot) {
+  if (diag_nonfinite(s, n, fail, P2<64>::LDS)) {
     if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
   } else {
     copy_lower<64, false>(s, A, ld, layout, n);
@@ -655,9 +663,10 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   PROBE(51);
   int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
   PROBE(52);
-  if (fail == kTinyPivot) {  // the block is untouched in global memory: redo it exactly
+  // a flushed pivot: redone exactly at the end (the block is untouched in global memory)
+  bool tiny = diag_nonfinite(s, kN1, fail, LDS);
+  if (tiny) {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
   } else if (fail == 0) {
     const int n2 = n - kN1;
     if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
@@ -676,12 +685,11 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
     PROBE(55);
     pdl_trigger();
-    if (fail == kTinyPivot) {
+    tiny = diag_nonfinite(s + kN1 + kN1 * LDS, n2, fail, LDS);
+    if (!tiny) {
 #if RELAPACK_NODE_EARLY_STORE
 #error "the exact fallback needs the block unmodified in global memory"
 #endif
-      if (threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
-    } else {
       if (fail) fail += kN1;
 #if !RELAPACK_NODE_EARLY_STORE
       copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
@@ -694,6 +702,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
     copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
   }
   PROBE(56);
+  if (tiny && threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
   if (fail && threadIdx.x == 0) *d_info = info_base + fail;
   trace_end(tr);
 }
@@ -721,7 +730,7 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
       }
   int fail = reg_potrf<TN>(v, lane);
   pdl_trigger();
-  if (fail == kTinyPivot) {
+  if (reg_diag_nonfinite<TN>(v, n, fail, lane)) {
     fail = potf2_exact_global(A, ld, layout, n, lane);
   } else {
 #pragma unroll

@@ -39,8 +39,8 @@ constexpr int kFLdL = kFC + 4;           // L block row stride (== 4 mod 32)
 template <int NW>
 struct TF {
   static constexpr int ROWS = 8 * NW, THREADS = 32 * NW;
-  // (at least one whole 64-column chunk: the solve walks chunk columns past t)
-  static __host__ __device__ int ldx(int t) { return (((t < kFC ? kFC : t) + 31) & ~31) + 4; }
+  // (whole 64-column chunks: the solve walks the last chunk's columns past t)
+  static __host__ __device__ int ldx(int t) { return ((t + kFC - 1) / kFC) * kFC + 4; }
   // t <= 128: every L block the solve needs (two diagonal, one below) is
   // staged once up front; t > 128: one block at a time
   static __host__ __device__ int lblocks(int t) { return t <= 2 * kFC ? 3 : 1; }

@@ -87,8 +87,10 @@ __device__ __forceinline__ int kmap(int s, int t) {
 }
 
 // Element (i, j) of C belongs to the updated part: every element (tri 0), the
-// lower triangle i >= j (tri 1, SYRK) or the upper triangle i <= j (tri 2).
-__device__ __forceinline__ bool tri_keep(int tri, int i, int j) { return tri == 0 || (tri == 1 ? i >= j : i <= j); }
+// lower triangle i >= j (tri 1, SYRK) or the upper triangle i <= j (tri 2):
+// (i - j) * sign >= 0 with sign = 0 / 1 / -1 — one branch-free test.
+__device__ __forceinline__ int tri_sign(int tri) { return tri == 1 ? 1 : tri == 2 ? -1 : 0; }
+__device__ __forceinline__ bool tri_keep(int sign, int i, int j) { return (i - j) * sign >= 0; }
 
 __device__ __forceinline__ void tri_index(int x, int& ti, int& tj) {
   int r = (int)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
@@ -328,6 +330,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
   const int flim = LAYOUT == kLayoutN ? args.M : args.N;
   const int slim = LAYOUT == kLayoutN ? args.N : args.M;
   const int sbase = LAYOUT == kLayoutN ? n0 : m0;
+  const int tsign = tri_sign(args.tri);
   if (fi < flim) {
     double* Cf = args.C + fi;  // + slow * ldc
 #pragma unroll 1
@@ -338,7 +341,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
       for (int q = 0; q < kQ; ++q) {
         const int sg = sbase + s0 + SLOW_STEP * (q0 + q);
         const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
-        v[q] = (sg < slim && tri_keep(args.tri, i, j)) ? Cf[(int64_t)sg * args.ldc] : 0.0;
+        v[q] = (sg < slim && tri_keep(tsign, i, j)) ? Cf[(int64_t)sg * args.ldc] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
@@ -346,7 +349,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap& tmA, const CUtens
         const int sg = sbase + sl;
         const int i = LAYOUT == kLayoutN ? fi : sg, j = LAYOUT == kLayoutN ? sg : fi;
         // alpha = -1 (the factorization's C -= A B^T) rounds exactly like v - s
-        if (sg < slim && tri_keep(args.tri, i, j)) Cf[(int64_t)sg * args.ldc] = fma(args.alpha, sC[sl * C::CPAD + f], v[q]);
+        if (sg < slim && tri_keep(tsign, i, j)) Cf[(int64_t)sg * args.ldc] = fma(args.alpha, sC[sl * C::CPAD + f], v[q]);
       }
     }
   }

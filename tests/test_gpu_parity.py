@@ -342,10 +342,13 @@ def test_batched_graph_replay_after_regrow():
     torch.cuda.synchronize()
     _batched_check(big[0], big[1], big[5])
     other = _batched_case(5000, 33)
+    other_pristine = other[1].clone()
     s2 = torch.cuda.Stream()
     for _ in range(3):
         buf.copy_(pristine)
         infos.fill_(-99)
+        other[1].copy_(other_pristine)
+        other[5].fill_(-99)
         torch.cuda.synchronize()
         g.replay()
         with torch.cuda.stream(s2):
