@@ -259,6 +259,10 @@ def main():
     # end to end through the public C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = e2e_host(rl, P, n, uplo, args.e2e_steps, st, dev) if args.e2e_steps > 0 else None
 
+    # API latency: a cold call (new plan: build, capture, instantiate), a cached
+    # call, and calls that alternate between two matrices (new pointer each call)
+    api = api_latency(rl, P, uplo, st, dev) if n <= 16384 else None
+
     # kernels per factorization = ops of the captured plan DAG (one kernel each;
     # the ncu launch list in profiles/ counts the same 1150 at n = 16384)
     launches = len(rl.plan_schedule(n, rl.get_crossover(), 64, True)[0])
@@ -284,6 +288,7 @@ def main():
         "roofline": roofline,
         "kernel_share": kernel_share,
         "e2e": e2e,
+        "api_latency": api,
         "gpu_launches": launches * args.steps,
         "step_times_ms": [round(t, 4) for t in times],
         "clocks": clk.summary(),
@@ -342,6 +347,35 @@ def profile_kernels(rl, W, P, d_info, uplo, st, dev, ms_per_step):
     share["graph_step_ms"] = round(ms_per_step, 3)
     share["profiled_kernel_sum_ms"] = round(total_prof, 3)
     return roofline, share
+
+
+def api_latency(rl, P, uplo, st, dev):
+    """ms per relapack_dpotrf_async call measured with CUDA events around the
+    call (host work of the call included: events bracket the enqueue)."""
+    import time as _t
+
+    import torch
+
+    W1 = torch.empty_like(P.t()).t()
+    W2 = torch.empty_like(P.t()).t()
+    d_info = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def one(W):
+        W.copy_(P)
+        torch.cuda.synchronize(dev)
+        t0 = _t.perf_counter()
+        rl.dpotrf_async(W, d_info, uplo, stream=st)
+        torch.cuda.synchronize(dev)
+        return 1e3 * (_t.perf_counter() - t0)
+
+    rl.finalize()  # drop every cached plan
+    cold = one(W1)
+    cached = [one(W1) for _ in range(3)]
+    alt = [one(W2 if i % 2 == 0 else W1) for i in range(6)]
+    return {"cold_ms": round(cold, 3), "cached_ms": round(min(cached), 3),
+            "new_pointer_ms": round(sorted(alt)[len(alt) // 2], 3),
+            "note": "host wall clock around enqueue + synchronize; new_pointer alternates two matrices of the "
+                    "same shape (one pointer-independent graph serves both)"}
 
 
 def _in_graph_update_rate(rl, W, P, d_info, uplo, st, dev, upd_fl):

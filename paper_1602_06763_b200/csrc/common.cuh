@@ -71,6 +71,14 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// A descriptor in global memory modified through the generic proxy (the
+// plan's first node rebases it with tensormap.replace): acquire it for the
+// tensormap proxy before the first TMA that uses it.
+__device__ __forceinline__ void tma_acquire_desc(const CUtensorMap* map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(reinterpret_cast<uint64_t>(map))
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -108,6 +116,9 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 // handled by IEEE arithmetic).  The rare fallback of the base-case kernels for
 // blocks with a flushed (subnormal) pivot (the block is still unmodified in
 // global memory when it runs).  Returns 0 or the 1-based failing column.
+#ifdef RELAPACK_NO_EXACT_FALLBACK  // (A/B experiments only)
+static __device__ __forceinline__ int potf2_exact_global(double*, int64_t, int, int, int) { return 0; }
+#else
 static __device__ __noinline__ int potf2_exact_global(double* A, int64_t ld, int layout, int n, int lane) {
   for (int j = 0; j < n; ++j) {
     const double d = A[lv_off(layout, j, j, ld)];
@@ -126,6 +137,7 @@ static __device__ __noinline__ int potf2_exact_global(double* A, int64_t ld, int
   }
   return 0;
 }
+#endif
 
 // sqrt(d) from y ~ 1/sqrt(d): r = d*y corrected by one fma-exact residual step
 // (branch-free; exact for perfect squares, within an ulp otherwise).
@@ -159,12 +171,55 @@ __device__ __forceinline__ void trace_end(TraceRec* tr) {
   }
 }
 
+// Pointer-independent plan graphs (driver.cu): the run's info word and the
+// matrix base live in one 16-byte PlanState written by the graph's first node;
+// the plan's kernels get byte offsets instead of pointers and a d_info tagged
+// with bit 0 pointing at the PlanState, and add the base they read together
+// with the info word (one load, no extra latency).  An untagged d_info is a
+// plain info word and the pointer arguments are absolute (base 0).
+struct alignas(16) PlanState {
+  int info;
+  int pad;
+  unsigned long long base;
+};
+
+__device__ __forceinline__ int* untag(const int* d_info) {
+  return reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(d_info) & ~uintptr_t(1));
+}
+
+struct KState {
+  int info;
+  uintptr_t base;
+};
+
 // Every plan kernel starts here: wait for the grids it depends on
 // (programmatic dependent launch: a no-op unless the graph edge into this
-// node is programmatic, driver.cu capture_dag), then read the info word.
-__device__ __forceinline__ int ld_info(const int* d_info) {
+// node is programmatic, driver.cu capture_dag), then read the info word (and,
+// in a pointer-independent plan, the matrix base).
+__device__ __forceinline__ KState ld_state(const int* d_info) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  return *reinterpret_cast<const volatile int*>(d_info);
+  const uintptr_t t = reinterpret_cast<uintptr_t>(d_info);
+  KState s;
+  if (t & 1) {
+    unsigned a, b, c, d;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "l"(t & ~uintptr_t(1))
+                 : "memory");
+    s.info = (int)a;
+    s.base = ((uintptr_t)d << 32) | c;
+  } else {
+    s.info = *reinterpret_cast<const volatile int*>(d_info);
+    s.base = 0;
+  }
+  return s;
+}
+
+__device__ __forceinline__ int ld_info(const int* d_info) { return ld_state(d_info).info; }
+
+template <class T>
+__device__ __forceinline__ T* rebase(T* p, uintptr_t base) {
+  return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + base);
 }
 
 // Let the dependent grids launch (they still wait for this grid's completion

@@ -141,6 +141,21 @@ struct Plan {
   double* splitk_ws = nullptr;  // split-K partial tiles, one slot per concurrently runnable update
   int* splitk_cnt = nullptr;    // per-tile arrival counters (self-resetting; zeroed at every run start)
   size_t cnt_bytes = 0;
+  // Pointer-independent graph (RELAPACK_REBASE, default on): the kernels get
+  // byte offsets from the matrix base and a d_info tagged to d_state; the
+  // graph's first node (begin_node: k_plan_begin) writes the run's base into
+  // d_state and rebases the TMA descriptors d_maps (tensormap.replace), its
+  // last node (end_node: k_plan_end) copies the info word out.  A call with
+  // another matrix / info pointer updates only these two nodes' parameters.
+  bool rebased = false;
+  PlanState* d_state = nullptr;
+  CUtensorMap* d_maps = nullptr;
+  long long* d_map_off = nullptr;  // byte offset of each descriptor's global address from the base
+  int nmaps = 0;
+  cudaGraph_t graph = nullptr;     // kept for cudaGraphExecKernelNodeSetParams
+  cudaGraphNode_t begin_node = nullptr, end_node = nullptr;
+  const double* cur_A = nullptr;   // what the begin / end nodes currently hold
+  int* cur_info = nullptr;
   ~Plan() {
     {
       std::lock_guard<std::mutex> tl(g_trace_mu);
@@ -152,8 +167,69 @@ struct Plan {
       if (e) cudaEventDestroy(e);
     if (splitk_ws) cudaFree(splitk_ws);
     if (splitk_cnt) cudaFree(splitk_cnt);
+    if (graph) cudaGraphDestroy(graph);
+    if (d_state) cudaFree(d_state);
+    if (d_maps) cudaFree(d_maps);
+    if (d_map_off) cudaFree(d_map_off);
   }
 };
+
+__global__ void k_plan_begin(PlanState* ps, unsigned long long base, CUtensorMap* maps, const long long* off,
+                             int nmaps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    ps->info = 0;
+    ps->base = base;
+  }
+  if (i < nmaps)
+    asm volatile("tensormap.replace.tile.global_address.global.b1024.b64 [%0], %1;" ::"l"(maps + i),
+                 "l"(base + (unsigned long long)off[i])
+                 : "memory");
+  asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+}
+
+__global__ void k_plan_end(const PlanState* ps, int* info) { *info = ps->info; }
+
+static int begin_grid(int nmaps) { return (nmaps + 255) / 256 > 0 ? (nmaps + 255) / 256 : 1; }
+
+static cudaError_t launch_plan_begin(const Plan& pl, const double* A, cudaStream_t st) {
+  k_plan_begin<<<begin_grid(pl.nmaps), 256, 0, st>>>(pl.d_state, (unsigned long long)reinterpret_cast<uintptr_t>(A),
+                                                     pl.d_maps, pl.d_map_off, pl.nmaps);
+  return cudaGetLastError();
+}
+
+// Point the instantiated graph at another matrix / info word (two nodes).
+static cudaError_t retarget(Plan& pl, const double* A, int* d_info) {
+  cudaError_t e;
+  if (A != pl.cur_A) {
+    PlanState* ps = pl.d_state;
+    unsigned long long base = (unsigned long long)reinterpret_cast<uintptr_t>(A);
+    CUtensorMap* maps = pl.d_maps;
+    const long long* off = pl.d_map_off;
+    int nm = pl.nmaps;
+    void* args[] = {&ps, &base, &maps, &off, &nm};
+    cudaKernelNodeParams kp{};
+    kp.func = reinterpret_cast<void*>(k_plan_begin);
+    kp.gridDim = dim3(begin_grid(pl.nmaps));
+    kp.blockDim = dim3(256);
+    kp.kernelParams = args;
+    if ((e = cudaGraphExecKernelNodeSetParams(pl.exec, pl.begin_node, &kp)) != cudaSuccess) return e;
+    pl.cur_A = A;
+  }
+  if (d_info != pl.cur_info) {
+    const PlanState* ps = pl.d_state;
+    int* info = d_info;
+    void* args[] = {&ps, &info};
+    cudaKernelNodeParams kp{};
+    kp.func = reinterpret_cast<void*>(k_plan_end);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    if ((e = cudaGraphExecKernelNodeSetParams(pl.exec, pl.end_node, &kp)) != cudaSuccess) return e;
+    pl.cur_info = d_info;
+  }
+  return cudaSuccess;
+}
 
 // (A, n, ld, layout, d_info, host, hld, knob signature): every knob that shapes
 // the plan, its launches or the capture is part of the key (knob_signature)
@@ -400,6 +476,16 @@ static cudaError_t copy_block(const Plan& pl, size_t i, double* A, int64_t ld, i
 static cudaError_t launch_op_impl(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
                                   cudaStream_t st);
 
+// Kernel pointer argument of element offset `off`: absolute, or (rebased
+// plan) the byte offset from the matrix base the kernel adds at run time.
+static double* at_off(const Plan& pl, double* A, int64_t off) {
+  return pl.rebased ? reinterpret_cast<double*>(static_cast<uintptr_t>(off) * sizeof(double)) : A + off;
+}
+// The info pointer plan kernels get: the tagged PlanState of a rebased plan.
+static int* op_info(const Plan& pl, int* d_info) {
+  return pl.rebased ? reinterpret_cast<int*>(reinterpret_cast<uintptr_t>(pl.d_state) | 1) : d_info;
+}
+
 static cudaError_t launch_op(const Plan& pl, size_t i, double* A, int64_t ld, int layout, int* d_info,
                              cudaStream_t st) {
   g_launch_trace = pl.d_trace ? pl.d_trace + i : nullptr;
@@ -424,10 +510,12 @@ static cudaError_t launch_op_impl(const Plan& pl, size_t i, double* A, int64_t l
       return copy_block(pl, i, A, ld, layout, st);
     }
     case OP_POTF2:
-      return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, ld), ld, layout, op.n, d_info, op.info_base, st);
+      return launch_potf2(at_off(pl, A, lv_off(layout, op.c_i, op.c_j, ld)), ld, layout, op.n, op_info(pl, d_info),
+                          op.info_base, st);
     case OP_TRSM:
-      return launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, ld), ld, A + lv_off(layout, op.c_i, op.c_j, ld), ld,
-                             layout, op.m, op.k, d_info, st);
+      return launch_trsm_any(at_off(pl, A, lv_off(layout, op.a_i, op.a_j, ld)), ld,
+                             at_off(pl, A, lv_off(layout, op.c_i, op.c_j, ld)), ld, layout, op.m, op.k,
+                             op_info(pl, d_info), st);
     case OP_GEMM:
     case OP_SYRK:
       return launch_update(pl.upd[i], st);
@@ -446,8 +534,9 @@ __global__ void k_trace_reset(TraceRec* tr, int n) {
   }
 }
 
-static cudaError_t run_prologue(const Plan& pl, int* d_info, cudaStream_t st) {
-  cudaError_t e = launch_set_int(d_info, 0, st);
+// the prologue's nodes after the info reset (set_info false: the caller did it)
+static cudaError_t run_prologue_rest(const Plan& pl, int* d_info, cudaStream_t st, bool set_info) {
+  cudaError_t e = set_info ? launch_set_int(d_info, 0, st) : cudaSuccess;
   if (e == cudaSuccess && pl.d_trace) {
     const int n = (int)pl.ops.size();
     k_trace_reset<<<(n + 255) / 256, 256, 0, st>>>(pl.d_trace, n);
@@ -460,7 +549,7 @@ static cudaError_t run_prologue(const Plan& pl, int* d_info, cudaStream_t st) {
 // Serial execution in plan order (eager mode and the profiler).
 static cudaError_t run_ops(const Plan& pl, double* A, int64_t ld, int layout, int* d_info, cudaStream_t st,
                            bool profile) {
-  cudaError_t e = run_prologue(pl, d_info, st);
+  cudaError_t e = run_prologue_rest(pl, d_info, st, true);
   if (e != cudaSuccess) return e;
   std::unique_lock<std::mutex> plk(g_prof_mu, std::defer_lock);
   if (profile) plk.lock();
@@ -556,14 +645,35 @@ cudaError_t capture_plan_dag(const std::vector<PlanOp>& ops, const std::vector<s
   return cudaStreamUpdateCaptureDependencies(st, want.data(), want.size(), cudaStreamSetCaptureDependencies);
 }
 
-static cudaError_t capture_dag(const Plan& pl, const std::vector<std::vector<int>>& deps, double* A, int64_t ld,
+static cudaError_t capture_node(cudaStream_t st, cudaGraphNode_t* node) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* cur = nullptr;
+  size_t ncur = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur);
+  if (e == cudaSuccess && ncur != 1) e = cudaErrorStreamCaptureInvalidated;
+  if (e == cudaSuccess) *node = cur[0];
+  return e;
+}
+
+static cudaError_t capture_dag(Plan& pl, const std::vector<std::vector<int>>& deps, double* A, int64_t ld,
                                int layout, int* d_info, cudaStream_t st, std::vector<cudaGraphNode_t>& nodes,
                                std::vector<char>& deferred_node) {
-  cudaError_t e = run_prologue(pl, d_info, st);
-  if (e != cudaSuccess) return e;
-  return capture_plan_dag(
+  cudaError_t e;
+  if (pl.rebased) {
+    if ((e = launch_plan_begin(pl, A, st)) != cudaSuccess) return e;
+    if ((e = capture_node(st, &pl.begin_node)) != cudaSuccess) return e;
+    pl.cur_A = A;
+  }
+  if ((e = run_prologue_rest(pl, d_info, st, !pl.rebased)) != cudaSuccess) return e;
+  e = capture_plan_dag(
       pl.ops, deps, st, [&](size_t i, cudaStream_t s) { return launch_op(pl, i, A, ld, layout, d_info, s); }, nodes,
       deferred_node);
+  if (e == cudaSuccess && pl.rebased) {
+    k_plan_end<<<1, 1, 0, st>>>(pl.d_state, d_info);
+    if ((e = cudaGetLastError()) == cudaSuccess) e = capture_node(st, &pl.end_node);
+    pl.cur_info = d_info;
+  }
+  return e;
 }
 
 cudaError_t set_node_priorities(const std::vector<cudaGraphNode_t>& nodes, const std::vector<char>& deferred) {
@@ -647,8 +757,16 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
   const int bulk = bulk_ctas();
   const int upd_cap = upd_ctas();
   (void)bulk;
-  PlanKey key{reinterpret_cast<uintptr_t>(A), n, ld, layout, reinterpret_cast<uintptr_t>(d_info),
-              reinterpret_cast<uintptr_t>(host), hld, knob_signature(pp, use_graph, use_dag)};
+  // a pointer-independent graph serves every matrix of this shape (its key
+  // holds only whether A allows TMA: 16-byte aligned base, even ld) and every
+  // info pointer; the host matrix of the pinned path only enters the graph
+  // when its copies are graph nodes (split copies off)
+  const bool rebased = use_dag && env_int("RELAPACK_REBASE", 1) != 0;
+  const uintptr_t a_key = rebased ? 1 + (((reinterpret_cast<uintptr_t>(A) & 15) == 0 && ld % 2 == 0) ? 1 : 0)
+                                  : reinterpret_cast<uintptr_t>(A);
+  const uintptr_t h_key = rebased && split_copies_enabled() ? (host ? 1 : 0) : reinterpret_cast<uintptr_t>(host);
+  PlanKey key{a_key, n, ld, layout, rebased ? 0 : reinterpret_cast<uintptr_t>(d_info), h_key, hld,
+              knob_signature(pp, use_graph, use_dag) + (rebased ? " rebased" : "")};
   Plan* plan = nullptr;
   auto it = ds->index.find(key);
   if (it != ds->index.end()) {
@@ -707,9 +825,32 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
     p->upd.resize(p->ops.size());
     if (trace_enabled() && (e = cudaMalloc(&p->d_trace, p->ops.size() * sizeof(TraceRec))) != cudaSuccess)
       return cuda_fail(e, "trace buffer");
+    p->rebased = rebased;
+    std::vector<CUtensorMap> hmaps;
+    std::vector<long long> hoff;
+    if (rebased && (e = cudaMalloc(&p->d_state, sizeof(PlanState))) != cudaSuccess) return cuda_fail(e, "plan state");
     for (size_t i = 0; i < p->ops.size(); ++i)
       if (p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) {
         fill_update(p->upd[i], p->ops[i], A, ld, layout, d_info);
+        if (rebased) {
+          // descriptors encoded for this call's A, rebased by every run's first
+          // node; pointer arguments become byte offsets from the matrix base
+          UpdateArgs& a = p->upd[i].args;
+          auto boff = [&](const double* x) {
+            return (long long)(reinterpret_cast<uintptr_t>(x) - reinterpret_cast<uintptr_t>(A));
+          };
+          if (p->upd[i].use_tma) {
+            a.gmap = reinterpret_cast<const CUtensorMap*>(hmaps.size());  // slot index, patched below
+            hmaps.push_back(p->upd[i].tmA);
+            hmaps.push_back(p->upd[i].tmB);
+            hoff.push_back(boff(a.A));
+            hoff.push_back(boff(a.B));
+          }
+          a.C = reinterpret_cast<double*>(static_cast<uintptr_t>(boff(a.C)));
+          a.A = reinterpret_cast<const double*>(static_cast<uintptr_t>(boff(a.A)));
+          a.B = reinterpret_cast<const double*>(static_cast<uintptr_t>(boff(a.B)));
+          a.d_info = op_info(*p, d_info);
+        }
         // deferred (lookahead) updates big enough to hold SMs for long run
         // persistent on `bulk` CTAs, leaving SMs to the chain; small ones
         // (below RELAPACK_BULK_MIN_GF GFLOP) run uncapped at low priority —
@@ -721,6 +862,21 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
         // (tools/trace_timeline.py: otherwise the chain waits ~24 ms at n = 16384)
         else if (use_dag && upd_cap > 0) p->upd[i].max_ctas = upd_cap;
       }
+    if (rebased) {
+      p->nmaps = (int)hmaps.size();
+      if (p->nmaps > 0) {
+        if ((e = cudaMalloc(&p->d_maps, hmaps.size() * sizeof(CUtensorMap))) != cudaSuccess ||
+            (e = cudaMemcpy(p->d_maps, hmaps.data(), hmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice)) !=
+                cudaSuccess ||
+            (e = cudaMalloc(&p->d_map_off, hoff.size() * sizeof(long long))) != cudaSuccess ||
+            (e = cudaMemcpy(p->d_map_off, hoff.data(), hoff.size() * sizeof(long long), cudaMemcpyHostToDevice)) !=
+                cudaSuccess)
+          return cuda_fail(e, "plan descriptors");
+      }
+      for (size_t i = 0; i < p->ops.size(); ++i)
+        if ((p->ops[i].kind == OP_GEMM || p->ops[i].kind == OP_SYRK) && p->upd[i].use_tma)
+          p->upd[i].args.gmap = p->d_maps + reinterpret_cast<uintptr_t>(p->upd[i].args.gmap);
+    }
     std::vector<std::vector<int>> deps;
     std::vector<uint64_t> anc;
     if (use_dag) compute_deps(p->ops, deps, &anc);
@@ -745,7 +901,10 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
         return cuda_fail(e, "graph node priority");
       }
       e = cudaGraphInstantiateWithFlags(&p->exec, g, use_dag ? cudaGraphInstantiateFlagUseNodePriority : 0);
-      cudaGraphDestroy(g);
+      if (rebased)
+        p->graph = g;  // its begin / end node handles retarget the exec per call
+      else
+        cudaGraphDestroy(g);
       if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
     }
     ds->lru.emplace_front(key, std::move(p));
@@ -755,6 +914,10 @@ int enqueue_potrf(int dev, double* A, int n, int64_t ld, int layout, int* d_info
       ds->index.erase(ds->lru.back().first);
       ds->lru.pop_back();
     }
+  }
+  if (plan->rebased) {
+    if ((e = retarget(*plan, A, d_info)) != cudaSuccess) return cuda_fail(e, "graph retarget");
+    if (host) plan->host = host;  // the split copies run outside the graph
   }
   if (use_graph && plan->split_copies) {
     // H2D blocks on one copy stream (each followed by its event), the graph

@@ -37,6 +37,10 @@ struct UpdateArgs {
   int ntiles;
   double* ws;         // ksplit * ntiles * tile^2 doubles
   int* counters;      // ntiles ints, zero between launches
+  // pointer-independent plan graph: the A / B descriptors in global memory
+  // (rebased per run by the plan's first node); C / A / B above are then byte
+  // offsets from the matrix base and d_info is tagged (common.cuh PlanState)
+  const CUtensorMap* gmap;
 };
 
 struct UpdateOp {

@@ -324,7 +324,11 @@ constexpr int kBaseMax = kPotf2Max;  // 128
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A, int64_t ld, int layout, int n,
                                                                        int* d_info, int info_base, TraceRec* tr) {
   PROBE(0);
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    A = rebase(A, ks.base);
+  }
   trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   } else {
     copy_lower<kBaseMax, false>(s, A, ld, layout, n);
   }
-  if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+  if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
   PROBE(63);
   trace_end(tr);
 }
@@ -348,7 +352,11 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
 __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int64_t ld, int layout, int n,
                                                                   int* d_info, int info_base, TraceRec* tr) {
   PROBE(0);
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    A = rebase(A, ks.base);
+  }
   trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
     copy_lower<64, false>(s, A, ld, layout, n);
   }
   PROBE(63);
-  if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+  if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
   trace_end(tr);
 }
 
@@ -649,7 +657,11 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   layout &= 0xff;
   constexpr int LDS = P2<kBaseMax>::LDS, NW = P2<kBaseMax>::NW;
   PROBE(50);
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    A = rebase(A, ks.base);
+  }
   trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
@@ -703,7 +715,7 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   }
   PROBE(56);
   if (tiny && threadIdx.x < 32) fail = potf2_exact_global(A, ld, layout, n, threadIdx.x);
-  if (fail && threadIdx.x == 0) *d_info = info_base + fail;
+  if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
   trace_end(tr);
 }
 
@@ -715,7 +727,11 @@ template <int TN>
 __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int layout, int n, int* d_info,
                                                       int info_base, TraceRec* tr) {
   using T = RegTri<TN>;
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    A = rebase(A, ks.base);
+  }
   trace_begin(tr);
   const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
   double v[T::NT][2];
@@ -743,7 +759,7 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
           if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q];
         }
   }
-  if (fail && fail <= n && lane == 0) *d_info = info_base + fail;
+  if (fail && fail <= n && lane == 0) *untag(d_info) = info_base + fail;
   trace_end(tr);
 }
 

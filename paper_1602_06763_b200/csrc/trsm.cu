@@ -58,7 +58,12 @@ template <int R>
 __global__ void __launch_bounds__(kTsThreads) k_trsm_base(const double* __restrict__ L, int64_t ldl,
                                                         double* __restrict__ B, int64_t ldb, int layout, int m, int t,
                                                         const int* d_info, TraceRec* tr) {
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    L = rebase(L, ks.base);
+    B = rebase(B, ks.base);
+  }
   trace_begin(tr);
   constexpr int kRows = kWarps * R;  // rows per CTA
   extern __shared__ double smem_d[];

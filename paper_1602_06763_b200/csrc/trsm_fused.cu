@@ -173,7 +173,12 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
                  int t, const int* d_info, TraceRec* tr) {
   constexpr int kFRows = TF<NW>::ROWS, kFThreads = TF<NW>::THREADS;
   TPROBE(0);
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    L = rebase(L, ks.base);
+    B = rebase(B, ks.base);
+  }
   trace_begin(tr);
   extern __shared__ double smem_t[];
   const int kFLdX = TF<NW>::ldx(t);
@@ -399,7 +404,12 @@ template <int NW, int RG, int NC>
 __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
     k_trsm_reg(const double* __restrict__ L, int64_t ldl, double* __restrict__ B, int64_t ldb, int layout, int m,
                int t, const int* d_info, TraceRec* tr) {
-  if (ld_info(d_info) != 0) return;
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    L = rebase(L, ks.base);
+    B = rebase(B, ks.base);
+  }
   trace_begin(tr);
   TPROBE(0);
   extern __shared__ double smem_r[];

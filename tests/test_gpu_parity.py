@@ -554,3 +554,38 @@ def test_subnormal_pivot(n, k, uplo):
     floor = np.maximum(1e-4 * np.sqrt(np.diag(A)), 1e-300)[:, None]
     err = float(np.max(np.tril(np.abs(Lg - Lo) / np.maximum(np.abs(Lo), floor))))
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_graph_reuse_across_matrices(uplo):
+    """One captured graph per (n, lda, uplo) serves every matrix and info
+    pointer (pointer-independent plan: offsets + a per-run base, TMA descriptors
+    rebased by the graph's first node): three matrices of the same shape and two
+    info words, interleaved, each result against the oracle; then a matrix
+    whose base is only 8-byte aligned (its own plan, no TMA)."""
+    n = 1500
+    As = [np.asfortranarray(gen.spd(n, 40 + k)) for k in range(3)]
+    infos = [torch.full((1,), -7, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for it in range(6):
+        k = it % 3
+        dA = to_dev(As[k])
+        d_info = infos[it % 2]
+        assert rl.dpotrf_async(dA, d_info, uplo) == 0
+        torch.cuda.synchronize()
+        assert int(d_info.item()) == 0
+        R = np.array(As[k], order="F")
+        assert oracle.dpotrf(R, uplo) == 0
+        G = dA.cpu().numpy()
+        assert floored_rel_err(lower_of(G, uplo), lower_of(R, uplo), As[k]) <= TOL
+    # 8-byte aligned base
+    buf = torch.empty(n * n + 1, dtype=torch.float64, device="cuda")
+    dA = buf[1:].view(n, n).t()
+    dA.copy_(torch.from_numpy(np.ascontiguousarray(As[0].T)).cuda().t())
+    assert rl.dpotrf(dA, uplo) == 0
+    R = np.array(As[0], order="F")
+    oracle.dpotrf(R, uplo)
+    assert floored_rel_err(lower_of(dA.cpu().numpy(), uplo), lower_of(R, uplo), As[0]) <= TOL
+    # a failing matrix through the same graph: info identical to the oracle's
+    Bad = gen.indefinite(As[1], 900)
+    dB = to_dev(np.asfortranarray(Bad))
+    assert rl.dpotrf(dB, uplo) == 901
