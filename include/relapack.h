@@ -75,9 +75,13 @@ typedef void* relapack_stream_t;
  *               place.  Host memory (pageable or pinned) is staged through a
  *               library-owned device buffer: the uplo triangle is copied in
  *               (whole diagonal blocks, whose other-triangle values are never
- *               used), factored on the GPU, and only the uplo triangle is
- *               written back (diagonal blocks masked), so the other strict
- *               triangle of the caller's matrix is never written.
+ *               used), factored on the GPU and copied back.  Pageable: only
+ *               the uplo triangle is written back.  Pinned: the copies are
+ *               2-D blocks overlapped with the factorization, and the 512 x
+ *               512 diagonal blocks go back whole, so the other strict
+ *               triangle inside them is rewritten with the values it held at
+ *               the call (its contents never change, but the caller must not
+ *               modify them concurrently).
  *   lda   in   leading dimension, lda >= max(1, n)
  *   info  out  host int, see "Errors" above
  * Returns after the factorization completed (stream synchronised).

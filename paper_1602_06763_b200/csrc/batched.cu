@@ -264,14 +264,33 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
     }
 #if RELAPACK_BATCH_MODE == 1  // tools/microbench only: memory phases alone
     const int fail = 0;
+    const double usc = 1.0;
 #else
-    int fail = reg_potrf<NMAX / 8>(v, lane);
+    int fail = 0, pass = 0;
+    for (;; ++pass) {
+      // pass 1 (rare): a flushed (subnormal) pivot left a non-finite diagonal;
+      // the matrix, still unmodified in global memory, is factored again
+      // scaled by 2^128 and its factor stored scaled back by 2^-64 (potf2.cu
+      // scale_lower)
+      if (pass) {
+#pragma unroll
+        for (int i = 0; i < C::TN; ++i)
+#pragma unroll
+          for (int k = 0; k <= i; ++k)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+              v[T::id(i, k)][q] =
+                  (r < n && c < n && r >= c) ? A[lv_off(LAYOUT, r, c, lda)] * 0x1p+128 : (r == c ? 1.0 : 0.0);
+            }
+      }
+      fail = reg_potrf<NMAX / 8>(v, lane);
+      if (pass || !reg_diag_nonfinite<NMAX / 8>(v, n, fail, lane)) break;
+    }
+    const double usc = pass ? 0x1p-64 : 1.0;
 #endif
-    // store the lower triangle of L (only the uplo triangle is written); a
-    // flushed (subnormal) pivot: the matrix (still unmodified) is redone exactly
-    if (reg_diag_nonfinite<NMAX / 8>(v, n, fail, lane)) {
-      fail = potf2_exact_global(A, lda, LAYOUT, n, lane);
-    } else if (n == NMAX) {
+    // store the lower triangle of L (only the uplo triangle is written)
+    if (n == NMAX) {
       // full class size: only diagonal tiles need a predicate; one lane base
       // pointer, tile offsets are (i, k) multiples of 8 rows / columns
       double* Al = A + lv_off(LAYOUT, g, 2 * t, lda);
@@ -283,7 +302,7 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
         for (int i = k; i < C::TN; ++i)
 #pragma unroll
           for (int q = 0; q < 2; ++q)
-            if (i > k || g >= 2 * t + q) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q];
+            if (i > k || g >= 2 * t + q) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q] * usc;
       }
     } else {
 #pragma unroll
@@ -293,7 +312,7 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-            if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q];
+            if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q] * usc;
           }
     }
     if (lane == 0) d_info[b] = fail;

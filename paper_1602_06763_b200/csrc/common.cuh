@@ -100,8 +100,8 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // the per-column critical path of every base-case factorization.
 // The MUFU flushes subnormal inputs to zero (.ftz), so a positive subnormal
 // pivot gives inf / NaN here; the base-case kernels detect the resulting
-// non-finite diagonal after the factorization (off the chain) and redo the
-// block with potf2_exact_global (exact sqrt and division) before storing.
+// non-finite diagonal after the factorization (off the chain) and factor the
+// block again scaled by 2^128 (potf2.cu scale_lower) before storing.
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
@@ -111,33 +111,6 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return fma(y * e, t, y);
 }
 
-// Unblocked Cholesky of the n x n L-view block in GLOBAL memory by one warp,
-// right-looking, correctly rounded sqrt and true division (subnormal pivots
-// handled by IEEE arithmetic).  The rare fallback of the base-case kernels for
-// blocks with a flushed (subnormal) pivot (the block is still unmodified in
-// global memory when it runs).  Returns 0 or the 1-based failing column.
-#ifdef RELAPACK_NO_EXACT_FALLBACK  // (A/B experiments only)
-static __device__ __forceinline__ int potf2_exact_global(double*, int64_t, int, int, int) { return 0; }
-#else
-static __device__ __noinline__ int potf2_exact_global(double* A, int64_t ld, int layout, int n, int lane) {
-  for (int j = 0; j < n; ++j) {
-    const double d = A[lv_off(layout, j, j, ld)];
-    if (!(d > 0.0)) return j + 1;
-    const double l = sqrt(d);
-    __syncwarp();
-    if (lane == 0) A[lv_off(layout, j, j, ld)] = l;
-    for (int i = j + 1 + lane; i < n; i += 32) A[lv_off(layout, i, j, ld)] = A[lv_off(layout, i, j, ld)] / l;
-    __syncwarp();
-    for (int k = j + 1; k < n; ++k) {
-      const double lkj = A[lv_off(layout, k, j, ld)];
-      for (int i = k + lane; i < n; i += 32)
-        A[lv_off(layout, i, k, ld)] = A[lv_off(layout, i, k, ld)] - A[lv_off(layout, i, j, ld)] * lkj;
-    }
-    __syncwarp();
-  }
-  return 0;
-}
-#endif
 
 // sqrt(d) from y ~ 1/sqrt(d): r = d*y corrected by one fma-exact residual step
 // (branch-free; exact for perfect squares, within an ulp otherwise).

@@ -455,13 +455,6 @@ static cudaError_t copy_block(const Plan& pl, size_t i, double* A, int64_t ld, i
   const size_t height = layout == kLayoutN ? op.k : op.m;
   double* dev = A + lv_off(layout, op.c_i, op.c_j, ld);
   double* host = const_cast<double*>(pl.host) + lv_off(layout, op.c_i, op.c_j, pl.hld);
-  if (op.kind == OP_D2H && op.c_i == op.c_j) {
-    // a diagonal block goes back masked to the uplo triangle (SM copy into
-    // the pinned host matrix through UVA): the other triangle of the caller's
-    // matrix is never written
-    return launch_copy2d(host, pl.hld, dev, ld, (int64_t)(width / sizeof(double)), (int64_t)height, st,
-                         layout == kLayoutN ? 1 : 2);
-  }
   if (copy_kernels()) {
     const int64_t w = (int64_t)(width / sizeof(double)), h = (int64_t)height;
     return op.kind == OP_H2D ? launch_copy2d(dev, ld, host, pl.hld, w, h, st)
