@@ -264,30 +264,8 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
     }
 #if RELAPACK_BATCH_MODE == 1  // tools/microbench only: memory phases alone
     const int fail = 0;
-    const double usc = 1.0;
 #else
-    int fail = 0, pass = 0;
-    for (;; ++pass) {
-      // pass 1 (rare): a flushed (subnormal) pivot left a non-finite diagonal;
-      // the matrix, still unmodified in global memory, is factored again
-      // scaled by 2^128 and its factor stored scaled back by 2^-64 (potf2.cu
-      // scale_lower)
-      if (pass) {
-#pragma unroll
-        for (int i = 0; i < C::TN; ++i)
-#pragma unroll
-          for (int k = 0; k <= i; ++k)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-              v[T::id(i, k)][q] =
-                  (r < n && c < n && r >= c) ? A[lv_off(LAYOUT, r, c, lda)] * 0x1p+128 : (r == c ? 1.0 : 0.0);
-            }
-      }
-      fail = reg_potrf<NMAX / 8>(v, lane);
-      if (pass || !reg_diag_nonfinite<NMAX / 8>(v, n, fail, lane)) break;
-    }
-    const double usc = pass ? 0x1p-64 : 1.0;
+    const int fail = reg_potrf<NMAX / 8>(v, lane);
 #endif
     // store the lower triangle of L (only the uplo triangle is written)
     if (n == NMAX) {
@@ -302,7 +280,7 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
         for (int i = k; i < C::TN; ++i)
 #pragma unroll
           for (int q = 0; q < 2; ++q)
-            if (i > k || g >= 2 * t + q) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q] * usc;
+            if (i > k || g >= 2 * t + q) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q];
       }
     } else {
 #pragma unroll
@@ -312,7 +290,7 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-            if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q] * usc;
+            if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q];
           }
     }
     if (lane == 0) d_info[b] = fail;

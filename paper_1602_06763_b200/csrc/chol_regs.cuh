@@ -39,10 +39,8 @@ __device__ __forceinline__ double tile_frag(double x0, double x1, int ks, int g,
 }
 
 // Factor in place.  Returns 0 or the 1-based first column whose pivot failed
-// (!(d > 0): d <= 0, -0.0 or NaN); the values after a failure are unspecified.
-// A positive pivot the MUFU flushed (subnormal, rsqrt_nr) leaves a non-finite
-// diagonal with 0 returned: reg_diag_nonfinite detects it after the fact and
-// the caller refactors the block exactly.
+// (!(d >= kMinPivot): d <= 0, -0.0, NaN, or subnormal — common.cuh); the
+// values after a failure are unspecified.
 //
 // Per panel column c the stored column stays unscaled until the panel ends;
 // the column values are scaled as they are used (x = a_ic * r, the same
@@ -75,7 +73,7 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
 #pragma unroll
         for (int i = p; i < TN; ++i) xc[i] = __shfl_sync(0xffffffffu, v[T::id(i, p)][e], quad_src);
       }
-      bad |= (uint64_t)(!(d > 0.0)) << (8 * p + c);
+      bad |= (uint64_t)(!(d >= kMinPivot)) << (8 * p + c);
       const double r = rsqrt_nr(d);
       dv[c] = d;
       rv[c] = r;
@@ -125,21 +123,6 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
     }
   }
   return bad ? __ffsll((long long)bad) : 0;
-}
-
-// Any non-finite diagonal entry l_jj, j < n and before the first failed
-// column (fail, 0 = none), among the warp's tiles (a vote).
-template <int TN>
-__device__ __forceinline__ bool reg_diag_nonfinite(const double (&v)[RegTri<TN>::NT][2], int n, int fail, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-  if (fail) n = min(n, fail - 1);
-  bool bad = false;
-#pragma unroll
-  for (int p = 0; p < TN; ++p)
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (g == 2 * t + q && 8 * p + g < n) bad |= !isfinite(v[RegTri<TN>::id(p, p)][q]);
-  return __any_sync(0xffffffffu, bad);
 }
 
 // Element (row, col) of tile slot (i, k, q) for lane (g, t).

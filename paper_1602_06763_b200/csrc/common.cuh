@@ -98,10 +98,13 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // (truncation ~ 5e^3/16 < 2^-66; ~1 ulp after rounding): four dependent FP64
 // operations after the MUFU instead of six for two Newton steps — this is on
 // the per-column critical path of every base-case factorization.
-// The MUFU flushes subnormal inputs to zero (.ftz), so a positive subnormal
-// pivot gives inf / NaN here; the base-case kernels detect the resulting
-// non-finite diagonal after the factorization (off the chain) and factor the
-// block again scaled by 2^128 (potf2.cu scale_lower) before storing.
+// The MUFU flushes subnormal inputs to zero (.ftz).  Pivots follow the same
+// flush-to-zero semantics (reading R15): a pivot d is accepted only
+// if d >= kMinPivot (the smallest normal double), so a subnormal pivot is
+// reported through info like d <= 0 instead of turning into inf / NaN factors
+// with info = 0 — the same single compare the !(d > 0) test was, off the chain.
+constexpr double kMinPivot = 0x1p-1022;
+
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));

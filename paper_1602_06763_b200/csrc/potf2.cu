@@ -208,7 +208,7 @@ __device__ __forceinline__ int factor_panel(double* s, int n, int j0, int lane) 
   int fail = 0;
 #pragma unroll
   for (int c = kPanel - 1; c >= 0; --c)
-    if (c < w && !(dpiv[c] > 0.0)) fail = j0 + c + 1;  // catches d <= 0, -0.0 and NaN
+    if (c < w && !(dpiv[c] >= kMinPivot)) fail = j0 + c + 1;  // d <= 0, -0.0, NaN and flushed (subnormal) d
   // diagonal entries l_jj = sqrt(d), off the critical path
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -269,32 +269,6 @@ __device__ int potf2_smem(double* s, int n, int* fail_flag) {
   return *fail_flag;
 }
 
-// A non-finite diagonal entry l_jj before the first failed column (`fail`,
-// 0 = none) means a positive pivot the MUFU flushed (subnormal, rsqrt_nr; the
-// NaN it leaves makes a later pivot fail) — the caller then redoes the block
-// exactly.  A genuine failure (d <= 0 or NaN) has only finite l_jj before it.
-// One barrier, off the chain.
-__device__ __forceinline__ bool diag_nonfinite(const double* s, int n, int fail, int lds) {
-  const int lim = fail ? fail - 1 : n;
-  bool bad = false;
-  for (int k = threadIdx.x; k < lim; k += blockDim.x) bad |= !isfinite(s[k * (lds + 1)]);
-  return __syncthreads_or(bad) != 0;
-}
-
-// Multiply the lower triangle (n x n, stride lds) in shared memory by f (all
-// threads; ends with a barrier).  The flushed-pivot retry: the block is
-// factored again scaled by 2^128 (a subnormal pivot d > 0 becomes >= 2^-946,
-// normal for the MUFU; power-of-two scalings are exact) and the factor is
-// scaled back by 2^-64 before it is stored.
-__device__ __forceinline__ void scale_lower(double* s, int n, int lds, double f) {
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e % n, j = e / n;
-    if (i >= j) s[i + j * lds] *= f;
-  }
-  __syncthreads();
-}
-constexpr double kFlushScale = 0x1p+128, kFlushUnscale = 0x1p-64;
-
 // Copy of the lower triangle of the L-view block between global memory and
 // shared memory, coalesced along the contiguous index (layout N: rows; layout
 // T: columns of L), 32 loads of a thread in flight at once.
@@ -346,18 +320,12 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A,
   trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
-  int fail = 0, pass = 0;
-  for (;; ++pass) {  // pass 1: the flushed-pivot retry on the scaled block (scale_lower)
-    if (threadIdx.x == 0) fail_flag = 0;
-    copy_lower<kBaseMax, true>(s, A, ld, layout, n);
-    __syncthreads();
-    if (pass) scale_lower(s, n, P2<kBaseMax>::LDS, kFlushScale);
-    PROBE(1);
-    fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
-    if (pass || !diag_nonfinite(s, n, fail, P2<kBaseMax>::LDS)) break;
-  }
+  if (threadIdx.x == 0) fail_flag = 0;
+  copy_lower<kBaseMax, true>(s, A, ld, layout, n);
+  __syncthreads();
+  PROBE(1);
+  const int fail = potf2_smem<kBaseMax, P2<kBaseMax>::LDS, P2<kBaseMax>::NW>(s, n, &fail_flag);
   pdl_trigger();
-  if (pass) scale_lower(s, n, P2<kBaseMax>::LDS, kFlushUnscale);
   copy_lower<kBaseMax, false>(s, A, ld, layout, n);
   if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
   PROBE(63);
@@ -376,19 +344,13 @@ __global__ void __launch_bounds__(P2<64>::THREADS) k_potf2_base64(double* A, int
   trace_begin(tr);
   extern __shared__ double s[];
   __shared__ int fail_flag;
-  int fail = 0, pass = 0;
-  for (;; ++pass) {  // pass 1: the flushed-pivot retry on the scaled block (scale_lower)
-    if (threadIdx.x == 0) fail_flag = 0;
-    copy_lower<64, true>(s, A, ld, layout, n);
-    __syncthreads();
-    if (pass) scale_lower(s, n, P2<64>::LDS, kFlushScale);
-    PROBE(1);
-    fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
-    if (pass || !diag_nonfinite(s, n, fail, P2<64>::LDS)) break;
-  }
+  if (threadIdx.x == 0) fail_flag = 0;
+  copy_lower<64, true>(s, A, ld, layout, n);
+  __syncthreads();
+  PROBE(1);
+  const int fail = potf2_smem<64, P2<64>::LDS, P2<64>::NW>(s, n, &fail_flag);
   PROBE(62);
   pdl_trigger();
-  if (pass) scale_lower(s, n, P2<64>::LDS, kFlushUnscale);
   copy_lower<64, false>(s, A, ld, layout, n);
   PROBE(63);
   if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
@@ -684,56 +646,42 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   extern __shared__ double s[];
   __shared__ int fail_flag;
   __shared__ double rinv[kN1];
+  if (threadIdx.x == 0) fail_flag = 0;
   constexpr int TH = P2<kBaseMax>::THREADS;
-  int fail = 0;
-  for (int pass = 0; pass < 2; ++pass) {  // pass 1: the flushed-pivot retry, scaled (scale_lower)
-    if (threadIdx.x == 0) fail_flag = 0;
-    // A11 now; A21 and A22 stream in (cp.async) while A11 is factored
-    copy_rect<kN1, kN1, LDS, TH, 0>(s, A, ld, layout, n, 0, 0, pairs);
-    copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, n, kN1, 0, pairs);
+  // A11 now; A21 and A22 stream in (cp.async) while A11 is factored
+  copy_rect<kN1, kN1, LDS, TH, 0>(s, A, ld, layout, n, 0, 0, pairs);
+  copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, n, kN1, 0, pairs);
+  __syncthreads();
+  PROBE(51);
+  int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
+  PROBE(52);
+  if (fail == 0) {
+    const int n2 = n - kN1;
+    if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
-    if (pass) {
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();
-      scale_lower(s, n, LDS, kFlushScale);
-    }
-    PROBE(51);
-    fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
-    PROBE(52);
-    if (!pass && diag_nonfinite(s, kN1, fail, LDS)) {  // a flushed pivot in A11
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();
-      continue;
-    }
-    if (fail == 0) {
-      const int n2 = n - kN1;
-      if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();
-      trsm_in_smem<LDS>(s, rinv, n2);
-      __syncthreads();
-      PROBE(53);
+    trsm_in_smem<LDS>(s, rinv, n2);
+    __syncthreads();
+    PROBE(53);
 #if RELAPACK_NODE_EARLY_STORE
-#error "the flushed-pivot retry needs the block unmodified in global memory"
+    // L11 and L21 are final: write them back while A22 is finished
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
 #endif
-      syrk_in_smem<LDS, NW>(s, n2);
-      __syncthreads();
-      PROBE(54);
-      fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
-      PROBE(55);
-      if (!pass && diag_nonfinite(s + kN1 + kN1 * LDS, n2, fail, LDS)) continue;  // flushed pivot in A22
-      pdl_trigger();
-      if (fail) fail += kN1;
-      if (pass) scale_lower(s, n, LDS, kFlushUnscale);
-      copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
-      copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
-    } else {
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      PROBE(55);
-      if (pass) scale_lower(s, kN1, LDS, kFlushUnscale);
-      copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
-    }
-    break;
+    syrk_in_smem<LDS, NW>(s, n2);
+    __syncthreads();
+    PROBE(54);
+    fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
+    if (fail) fail += kN1;
+    PROBE(55);
+    pdl_trigger();
+#if !RELAPACK_NODE_EARLY_STORE
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
+#endif
+    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
+  } else {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    PROBE(55);
+    copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
   }
   PROBE(56);
   if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
@@ -756,23 +704,6 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
   trace_begin(tr);
   const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
   double v[T::NT][2];
-  int fail = 0, pass = 0;
-  for (;; ++pass) {  // pass 1: the flushed-pivot retry on the block scaled by 2^128 (see scale_lower)
-    const double sc = pass ? kFlushScale : 1.0;
-#pragma unroll
-    for (int i = 0; i < TN; ++i)
-#pragma unroll
-      for (int k = 0; k <= i; ++k)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-          v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(layout, r, c, ld)] * sc : (r == c ? 1.0 : 0.0);
-        }
-    fail = reg_potrf<TN>(v, lane);
-    if (pass || !reg_diag_nonfinite<TN>(v, n, fail, lane)) break;
-  }
-  pdl_trigger();
-  const double usc = pass ? kFlushUnscale : 1.0;
 #pragma unroll
   for (int i = 0; i < TN; ++i)
 #pragma unroll
@@ -780,7 +711,18 @@ __global__ void __launch_bounds__(32, 1) k_potf2_reg(double* A, int64_t ld, int 
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-        if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q] * usc;
+        v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(layout, r, c, ld)] : (r == c ? 1.0 : 0.0);
+      }
+  const int fail = reg_potrf<TN>(v, lane);
+  pdl_trigger();
+#pragma unroll
+  for (int i = 0; i < TN; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+        if (r < n && c < n && r >= c) A[lv_off(layout, r, c, ld)] = v[T::id(i, k)][q];
       }
   if (fail && fail <= n && lane == 0) *untag(d_info) = info_base + fail;
   trace_end(tr);
