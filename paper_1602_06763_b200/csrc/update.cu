@@ -169,8 +169,14 @@ __device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::
 // One work item (tile, split) of the update; the CTA may process several
 // (persistent launch with a capped grid, see launch_tbm).
 template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM>
-__device__ __forceinline__ void update_item(const CUtensorMap* tmA, const CUtensorMap* tmB, const UpdateArgs& args,
-                                            uint8_t* smem, int work, bool last, uintptr_t base) {
+__device__ __forceinline__ void update_item(const CUtensorMap* const* s_map, const UpdateArgs& args, uint8_t* smem,
+                                            int work, bool last, const uintptr_t* s_base) {
+  // the A / B descriptors (kernel parameters, or in a pointer-independent plan
+  // the global copies its first node rebased) and the matrix base are read
+  // from shared memory where they are used, so no register stays live across
+  // the main loop for them (a register-held select spilled the 128-tile kernel)
+#define RELAPACK_TMA_A (*(const CUtensorMap* const volatile*)&s_map[0])
+#define RELAPACK_TMA_B (*(const CUtensorMap* const volatile*)&s_map[1])
   using C = Cfg<TBM>;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
@@ -217,7 +223,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA, const CUtens
     constexpr int kLineD = 16;  // doubles per 128-byte line
     const int lines = (fext + kLineD - 1) / kLineD;
     for (int e = threadIdx.x; e < lines * sext; e += C::THREADS) {
-      const double* pc = rebase(args.C, base) + (f0 + (e % lines) * kLineD) + (int64_t)(s0 + e / lines) * args.ldc;
+      const double* pc = rebase(args.C, *s_base) + (f0 + (e % lines) * kLineD) + (int64_t)(s0 + e / lines) * args.ldc;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pc));
     }
   }
@@ -237,21 +243,24 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA, const CUtens
         mbar_init(&empty[s], C::NUM_WARPS);
       }
       fence_barrier_init();
+#ifndef RELAPACK_NO_TMAP_ACQUIRE  // (A/B experiments only: unsafe without the fence)
       if (args.gmap) {  // descriptors in global memory, rebased by the plan's first node
-        tma_acquire_desc(tmA);
-        tma_acquire_desc(tmB);
+        tma_acquire_desc(RELAPACK_TMA_A);
+        tma_acquire_desc(RELAPACK_TMA_B);
       }
-      tma_prefetch_desc(tmA);
-      tma_prefetch_desc(tmB);
+#endif
+      tma_prefetch_desc(RELAPACK_TMA_A);
+      tma_prefetch_desc(RELAPACK_TMA_B);
     }
     __syncthreads();
     if (threadIdx.x == 0)
       for (int it = 0; it < STAGES - 1 && it < KT; ++it)
-        issue_stage<LA, LB, TBM>(smem, full, tmA, tmB, it, kt0 + it, m0, n0);
+        issue_stage<LA, LB, TBM>(smem, full, RELAPACK_TMA_A, RELAPACK_TMA_B, it, kt0 + it, m0, n0);
     for (int kt = 0; kt < KT; ++kt) {
       if (threadIdx.x == 0 && kt + STAGES - 1 < KT) {
         if (kt >= 1) mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
-        issue_stage<LA, LB, TBM>(smem, full, tmA, tmB, kt + STAGES - 1, kt0 + kt + STAGES - 1, m0, n0);
+        issue_stage<LA, LB, TBM>(smem, full, RELAPACK_TMA_A, RELAPACK_TMA_B, kt + STAGES - 1, kt0 + kt + STAGES - 1,
+                                 m0, n0);
       }
       const int s = kt % STAGES;
       mbar_wait(&full[s], (kt / STAGES) & 1);
@@ -263,8 +272,8 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA, const CUtens
   } else {
     for (int kt = 0; kt < KT; ++kt) {
       __syncthreads();
-      fill_tile_ldg<LA, TBM, C::THREADS>(smem, rebase(args.A, base), args.lda, args.M, m0, args.K, (kt0 + kt) * BK);
-      fill_tile_ldg<LB, TBM, C::THREADS>(smem + C::TILE_BYTES, rebase(args.B, base), args.ldb, args.N, n0, args.K,
+      fill_tile_ldg<LA, TBM, C::THREADS>(smem, rebase(args.A, *s_base), args.lda, args.M, m0, args.K, (kt0 + kt) * BK);
+      fill_tile_ldg<LB, TBM, C::THREADS>(smem + C::TILE_BYTES, rebase(args.B, *s_base), args.ldb, args.N, n0, args.K,
                                          (kt0 + kt) * BK);
       __syncthreads();
       mma_stage<LA, LB, TBM>(acc, smem, smem + C::TILE_BYTES, wm, wn, g, t);
@@ -337,7 +346,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA, const CUtens
   const int sbase = LAYOUT == kLayoutN ? n0 : m0;
   const int tsign = tri_sign(args.tri);
   if (fi < flim) {
-    double* Cf = rebase(args.C, base) + fi;  // + slow * ldc
+    double* Cf = rebase(args.C, *s_base) + fi;  // + slow * ldc
 #pragma unroll 1
     constexpr int kRows = TBM / SLOW_STEP, kQ = kRows < 16 ? kRows : 16;  // rows per thread, in flight
     for (int q0 = 0; q0 < kRows; q0 += kQ) {
@@ -360,6 +369,9 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA, const CUtens
   }
 }
 
+#undef RELAPACK_TMA_A
+#undef RELAPACK_TMA_B
+
 template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM>
 __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
     k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args,
@@ -367,14 +379,20 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
   const KState ks = ld_state(args.d_info);
   if (ks.info != 0) return;  // dpotrf2 semantics: stop after a failed pivot
   trace_begin(tr);
-  const CUtensorMap* mA = args.gmap ? args.gmap : &tmA;
-  const CUtensorMap* mB = args.gmap ? args.gmap + 1 : &tmB;
+  __shared__ uintptr_t s_base;  // read back where the offsets become pointers
+  __shared__ const CUtensorMap* s_map[2];
+  if (threadIdx.x == 0) {
+    s_base = ks.base;
+    s_map[0] = args.gmap ? args.gmap : &tmA;
+    s_map[1] = args.gmap ? args.gmap + 1 : &tmB;
+  }
+  __syncthreads();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nwork = args.ntiles * args.ksplit;
   for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
     if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
-    update_item<LA, LB, LAYOUT, USE_TMA, TBM>(mA, mB, args, smem, work, work + (int)gridDim.x >= nwork, ks.base);
+    update_item<LA, LB, LAYOUT, USE_TMA, TBM>(s_map, args, smem, work, work + (int)gridDim.x >= nwork, &s_base);
   }
   trace_end(tr);
 }
