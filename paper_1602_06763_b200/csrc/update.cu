@@ -168,15 +168,16 @@ __device__ __forceinline__ void mma_stage(double (&acc)[Cfg<TBM>::MT][Cfg<TBM>::
 
 // One work item (tile, split) of the update; the CTA may process several
 // (persistent launch with a capped grid, see launch_tbm).
-template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM>
-__device__ __forceinline__ void update_item(const CUtensorMap* const* s_map, const UpdateArgs& args, uint8_t* smem,
-                                            int work, bool last, const uintptr_t* s_base) {
-  // the A / B descriptors (kernel parameters, or in a pointer-independent plan
-  // the global copies its first node rebased) and the matrix base are read
-  // from shared memory where they are used, so no register stays live across
-  // the main loop for them (a register-held select spilled the 128-tile kernel)
-#define RELAPACK_TMA_A (*(const CUtensorMap* const volatile*)&s_map[0])
-#define RELAPACK_TMA_B (*(const CUtensorMap* const volatile*)&s_map[1])
+// GM: the A / B descriptors are the global copies a pointer-independent plan's
+// first node rebased (args.gmap, a parameter-space pointer) instead of the
+// kernel's own __grid_constant__ parameters — a compile-time choice, so the
+// producer's loop holds no runtime select (a register-held select spilled the
+// 128-tile kernel; reading it from shared memory slowed the producer).
+template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM, bool GM>
+__device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUtensorMap* tmB_p, const UpdateArgs& args,
+                                            uint8_t* smem, int work, bool last, const uintptr_t* s_base) {
+#define RELAPACK_TMA_A (GM ? args.gmap : tmA_p)
+#define RELAPACK_TMA_B (GM ? args.gmap + 1 : tmB_p)
   using C = Cfg<TBM>;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
@@ -243,12 +244,6 @@ __device__ __forceinline__ void update_item(const CUtensorMap* const* s_map, con
         mbar_init(&empty[s], C::NUM_WARPS);
       }
       fence_barrier_init();
-#ifndef RELAPACK_NO_TMAP_ACQUIRE  // (A/B experiments only: unsafe without the fence)
-      if (args.gmap) {  // descriptors in global memory, rebased by the plan's first node
-        tma_acquire_desc(RELAPACK_TMA_A);
-        tma_acquire_desc(RELAPACK_TMA_B);
-      }
-#endif
       tma_prefetch_desc(RELAPACK_TMA_A);
       tma_prefetch_desc(RELAPACK_TMA_B);
     }
@@ -372,41 +367,47 @@ __device__ __forceinline__ void update_item(const CUtensorMap* const* s_map, con
 #undef RELAPACK_TMA_A
 #undef RELAPACK_TMA_B
 
-template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM>
+template <int LA, int LB, int LAYOUT, bool USE_TMA, int TBM, bool GM>
 __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
     k_update(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UpdateArgs args,
              TraceRec* tr) {
+  // the global descriptors were rewritten through the generic proxy by the
+  // plan's first node (complete before any plan kernel starts, PDL included):
+  // acquire them for the tensormap proxy before griddepcontrol.wait, so the
+  // fence overlaps the wait instead of delaying the first TMA
+  if (GM && threadIdx.x == 0) {
+    tma_acquire_desc(args.gmap);
+    tma_acquire_desc(args.gmap + 1);
+  }
   const KState ks = ld_state(args.d_info);
   if (ks.info != 0) return;  // dpotrf2 semantics: stop after a failed pivot
   trace_begin(tr);
   __shared__ uintptr_t s_base;  // read back where the offsets become pointers
-  __shared__ const CUtensorMap* s_map[2];
-  if (threadIdx.x == 0) {
-    s_base = ks.base;
-    s_map[0] = args.gmap ? args.gmap : &tmA;
-    s_map[1] = args.gmap ? args.gmap + 1 : &tmB;
-  }
+  if (threadIdx.x == 0) s_base = ks.base;
   __syncthreads();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nwork = args.ntiles * args.ksplit;
   for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
     if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
-    update_item<LA, LB, LAYOUT, USE_TMA, TBM>(s_map, args, smem, work, work + (int)gridDim.x >= nwork, &s_base);
+    update_item<LA, LB, LAYOUT, USE_TMA, TBM, GM>(&tmA, &tmB, args, smem, work, work + (int)gridDim.x >= nwork,
+                                                  &s_base);
   }
   trace_end(tr);
 }
 
-template <int LA, int LB, int LC, bool USE_TMA, int TBM>
+template <int LA, int LB, int LC, bool USE_TMA, int TBM, bool GM>
 cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const UpdateArgs& a, int grid, cudaStream_t st) {
-  k_update<LA, LB, LC, USE_TMA, TBM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a, g_launch_trace);
+  k_update<LA, LB, LC, USE_TMA, TBM, GM><<<grid, Cfg<TBM>::THREADS, Cfg<TBM>::SMEM_BYTES, st>>>(ta, tb, a,
+                                                                                              g_launch_trace);
   return cudaGetLastError();
 }
 
 template <int LA, int LB, int LC, int TBM>
 cudaError_t launch_combo(const UpdateOp& op, int grid, cudaStream_t st) {
-  return op.use_tma ? launch_one<LA, LB, LC, true, TBM>(op.tmA, op.tmB, op.args, grid, st)
-                    : launch_one<LA, LB, LC, false, TBM>(op.tmA, op.tmB, op.args, grid, st);
+  if (!op.use_tma) return launch_one<LA, LB, LC, false, TBM, false>(op.tmA, op.tmB, op.args, grid, st);
+  return op.args.gmap ? launch_one<LA, LB, LC, true, TBM, true>(op.tmA, op.tmB, op.args, grid, st)
+                      : launch_one<LA, LB, LC, true, TBM, false>(op.tmA, op.tmB, op.args, grid, st);
 }
 
 // Operand-layout combinations (la, lb, lc): the factorization's (N,N,N) and
@@ -433,8 +434,9 @@ cudaError_t configure_combo() {
   cudaError_t e;
   const int sm = Cfg<TBM>::SMEM_BYTES;
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_update<LA, LB, LC, true, TBM>, attr, sm)) != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_update<LA, LB, LC, false, TBM>, attr, sm);
+  if ((e = cudaFuncSetAttribute(k_update<LA, LB, LC, true, TBM, false>, attr, sm)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_update<LA, LB, LC, true, TBM, true>, attr, sm)) != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_update<LA, LB, LC, false, TBM, false>, attr, sm);
 }
 
 template <int TBM>
