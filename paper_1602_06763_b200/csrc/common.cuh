@@ -193,6 +193,13 @@ __device__ __forceinline__ KState ld_state(const int* d_info) {
 
 __device__ __forceinline__ int ld_info(const int* d_info) { return ld_state(d_info).info; }
 
+// The matrix base again (a cached load of the PlanState; 0 for an untagged
+// d_info), for uses before the kernel's first barrier.
+__device__ __forceinline__ uintptr_t plan_base(const int* d_info) {
+  const uintptr_t t = reinterpret_cast<uintptr_t>(d_info);
+  return (t & 1) ? reinterpret_cast<const PlanState*>(t & ~uintptr_t(1))->base : 0;
+}
+
 template <class T>
 __device__ __forceinline__ T* rebase(T* p, uintptr_t base) {
   return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + base);

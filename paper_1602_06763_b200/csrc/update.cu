@@ -224,7 +224,8 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
     constexpr int kLineD = 16;  // doubles per 128-byte line
     const int lines = (fext + kLineD - 1) / kLineD;
     for (int e = threadIdx.x; e < lines * sext; e += C::THREADS) {
-      const double* pc = rebase(args.C, *s_base) + (f0 + (e % lines) * kLineD) + (int64_t)(s0 + e / lines) * args.ldc;
+      const double* pc = rebase(args.C, plan_base(args.d_info)) + (f0 + (e % lines) * kLineD) +
+                         (int64_t)(s0 + e / lines) * args.ldc;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pc));
     }
   }
@@ -382,9 +383,10 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
   const KState ks = ld_state(args.d_info);
   if (ks.info != 0) return;  // dpotrf2 semantics: stop after a failed pivot
   trace_begin(tr);
-  __shared__ uintptr_t s_base;  // read back where the offsets become pointers
+  // the base is read back from shared memory where the offsets become
+  // pointers after the main loop (every such use follows a barrier)
+  __shared__ uintptr_t s_base;
   if (threadIdx.x == 0) s_base = ks.base;
-  __syncthreads();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nwork = args.ntiles * args.ksplit;

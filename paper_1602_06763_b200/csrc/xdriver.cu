@@ -73,8 +73,18 @@ struct XExec {
 
 constexpr size_t kCandDoubles = 2 * 160 + 2 * 160 * kGetf2Max + 2 * kGetf2Max;
 
+// CTAs of a getrf panel: one per RELAPACK_GETF2_ROWS rows (default 128), at
+// most one per SM — fewer CTAs make the per-column grid barrier cheaper, more
+// spread the rank-1 updates (tools/experiments r2j sweep).
 int getf2_grid(int m, int sms) {
-  int g = (m + 31) / 32;
+  static const int rows = [] {
+    const char* v = getenv("RELAPACK_GETF2_ROWS");
+    const int r = v ? atoi(v) : 128;
+    return r < 16 ? 16 : r;
+  }();
+  int g = (m + rows - 1) / rows;
+  // shared memory holds the CTA's rows: at most ~700 rows of 32 columns
+  g = std::max(g, (m + 699) / 700);
   return std::max(1, std::min(g, sms));
 }
 
