@@ -153,6 +153,14 @@ RELAPACK_API void relapack_comm_destroy(relapack_comm_t* comm);
  * full factor and the same info.
  *   nb        row-block size of the block-cyclic distribution (>= 64, mult. of 64)
  *   dist_min  subproblem order below which the recursion is replicated
+ * (SURVEY §8(b) sketched `const int* nb`; nb and dist_min are SPMD tuning
+ * knobs, not LAPACK arguments, so both are passed by value; -5 if either is
+ * out of range or comm is NULL.)  Every rank captures the whole distributed
+ * plan — kernels, NCCL all-gathers and the final info all-reduce — once per
+ * (shape, knobs, A) into a CUDA graph and replays it; the wait polls
+ * ncclCommGetAsyncError with a timeout (env RELAPACK_DIST_TIMEOUT_S, default
+ * 600 s) and aborts the communicator on an error (info <= -1000; later calls
+ * on it fail with -1000).
  */
 RELAPACK_API void relapack_dpotrf_dist(const char* uplo, const int* n, double* A, const int* lda, int nb, int dist_min,
                           relapack_comm_t* comm, int* info);

@@ -34,7 +34,7 @@ struct XBuffers {
   int64_t ld[2] = {1, 1};
   int layout[2] = {kLayoutN, kLayoutN};  // logical -> memory layout of each buffer
   int* ipiv = nullptr;                   // buffer 2 (1-based pivots, indexed by row / column)
-  int total_rows = 0;
+  int total_rows = 0, total_cols = 0;
 };
 
 struct XOperand {
@@ -137,6 +137,9 @@ cudaError_t launch_xop(const XExec& x, size_t i, cudaStream_t st) {
       a.cand_rows = c + 2 * 160;
       a.diag_row = c + 2 * 160 + 2 * 160 * kGetf2Max;
       a.cand_idx = x.cand_idx + (size_t)x.slot[i] * 2 * 160;
+      a.A0 = resolve(b, XView{o.c.buf, o.c.r0, 0, 0}).p;
+      a.ncols = b.total_cols;
+      a.c0 = o.c.c0;
       a.d_info = x.d_info;
       return launch_getf2(a, G, st);
     }
@@ -547,6 +550,7 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
   b.layout[0] = kLayoutN;
   b.ipiv = ipiv;
   b.total_rows = *m;
+  b.total_cols = *n;
   const std::string key = "getrf m" + std::to_string(*m) + " n" + std::to_string(*n) + " ld" + std::to_string(*lda) +
                           " A" + ptr_key(A) + " P" + ptr_key(ipiv) + params_key(p);
   int r = x_run(key, ops, b, true, false, current_stream_or(nullptr), info);

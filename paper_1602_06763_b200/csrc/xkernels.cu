@@ -38,71 +38,78 @@ __device__ __forceinline__ double at(const double* X, int layout, int64_t ld, in
 
 }  // namespace
 
-// One thread per row of B; the row lives in shared memory (stride 65, so the
-// threads' concurrent accesses to one column hit 32 distinct banks) and T in
-// shared memory read by broadcast.  Solves divide by the diagonal (true
-// division, as the oracle); products accumulate in ascending / descending k.
+// One thread per row of B; the CTA's rows are staged through shared memory
+// both ways (global accesses along B's contiguous index; row stride 65, so the
+// threads' accesses to one column hit distinct banks).  T is staged once per
+// CTA as the strictly triangular part the mode reads — Tm[j][k] = T(j, k) for
+// k < j (row sweeps) or Tu[j][k] = T(k, j) for k > j (column sweeps), zero
+// elsewhere — plus its diagonal (1 for a unit diagonal), so every dot product
+// runs over whole groups of 8 with no bounds: inner loops unrolled by 8 into
+// four interleaved partial sums (a quarter of the dependent-FMA chain), T read
+// by broadcast.  Solves divide by the diagonal (true division, as the oracle).
+template <int MODE>
 __global__ void __launch_bounds__(kTriRows) k_tri_rows(XTriArgs a) {
   if (ld_info(a.d_info) != 0) return;
+  constexpr int W = kTriMax;                       // 64
+  constexpr bool kRows = MODE == kTriSolveLT || MODE == kTriMulLT;  // reads T by rows (else by columns)
   extern __shared__ double sm[];
-  double* sT = sm;                          // t x t, sT[i * kTriLd + j] = T(i, j)
-  double* sB = sm + kTriMax * kTriLd;       // kTriRows x t
+  double* sT = sm;                                 // W x W masked copy (see above)
+  double* sD = sm + W * W;                         // W diagonal entries
+  double* sB = sD + W;                             // kTriRows x (W + 1)
   const int t = a.t;
   const int row0 = blockIdx.x * kTriRows;
   const int rows = min(kTriRows, a.m - row0);
-  // stage T (lower part only; the other triangle is never read)
-  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
-    int i, j;
-    if (a.lt == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
-    if (i >= j) sT[i * kTriLd + j] = at(a.T, a.lt, a.ldt, i, j);
+  for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+    int i, j;  // element T(i, j) read in the contiguous order of T's layout
+    if (a.lt == 0) { i = e % W; j = e / W; } else { j = e % W; i = e / W; }
+    const double v = (i > j && i < t) ? at(a.T, a.lt, a.ldt, i, j) : 0.0;
+    if (kRows)
+      sT[i * W + j] = v;   // Tm[i][j] = T(i, j), j < i
+    else
+      sT[j * W + i] = v;   // Tu[j][i] = T(i, j), i > j
   }
-  // stage the CTA's rows of B, coalesced along B's contiguous index
+  for (int j = threadIdx.x; j < W; j += blockDim.x)
+    sD[j] = (a.unit || j >= t) ? 1.0 : at(a.T, a.lt, a.ldt, j, j);
   for (int e = threadIdx.x; e < rows * t; e += blockDim.x) {
     int r, c;
     if (a.lb == 0) { r = e % rows; c = e / rows; } else { c = e % t; r = e / t; }
-    sB[r * kTriLd + c] = at(a.B, a.lb, a.ldb, row0 + r, c);
+    sB[r * (W + 1) + c] = at(a.B, a.lb, a.ldb, row0 + r, c);
   }
   __syncthreads();
   const int r = threadIdx.x;
   if (r < rows) {
-    double* x = sB + r * kTriLd;
+    double* x = sB + r * (W + 1);
+    for (int c = t; c < W; ++c) x[c] = 0.0;  // padding columns (never stored)
     const double alpha = a.alpha;
-    switch (a.mode) {
-      case kTriSolveLT:  // x T^T = b: x_j = (b_j - sum_{k<j} x_k T_jk) / T_jj
-        for (int j = 0; j < t; ++j) {
-          double s = alpha * x[j];
-          for (int k = 0; k < j; ++k) s -= x[k] * sT[j * kTriLd + k];
-          x[j] = a.unit ? s : s / sT[j * kTriLd + j];
+    // sum_{k in [k0, k1)} x_k * row[k], k0 and k1 multiples of 8
+    auto dot = [&](const double* row, int k0, int k1) {
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      for (int k = k0; k < k1; k += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; u += 4) {
+          p0 = fma(x[k + u], row[k + u], p0);
+          p1 = fma(x[k + u + 1], row[k + u + 1], p1);
+          p2 = fma(x[k + u + 2], row[k + u + 2], p2);
+          p3 = fma(x[k + u + 3], row[k + u + 3], p3);
         }
-        break;
-      case kTriSolveL:  // x T = b: x_j = (b_j - sum_{k>j} x_k T_kj) / T_jj
-        for (int j = t - 1; j >= 0; --j) {
-          double s = alpha * x[j];
-          for (int k = t - 1; k > j; --k) s -= x[k] * sT[k * kTriLd + j];
-          x[j] = a.unit ? s : s / sT[j * kTriLd + j];
-        }
-        break;
-      case kTriMulL:  // y_j = alpha sum_{k>=j} x_k T_kj (ascending j reads only x_k, k >= j)
-        for (int j = 0; j < t; ++j) {
-          double s = a.unit ? x[j] : x[j] * sT[j * kTriLd + j];
-          for (int k = j + 1; k < t; ++k) s += x[k] * sT[k * kTriLd + j];
-          x[j] = alpha * s;
-        }
-        break;
-      default:  // kTriMulLT: y_j = alpha sum_{k<=j} x_k T_jk (descending j)
-        for (int j = t - 1; j >= 0; --j) {
-          double s = a.unit ? x[j] : x[j] * sT[j * kTriLd + j];
-          for (int k = 0; k < j; ++k) s += x[k] * sT[j * kTriLd + k];
-          x[j] = alpha * s;
-        }
-        break;
+      }
+      return (p0 + p1) + (p2 + p3);
+    };
+    if (MODE == kTriSolveLT) {  // x T^T = alpha b: x_j = (alpha b_j - sum_{k<j} x_k T_jk) / T_jj
+      for (int j = 0; j < W; ++j) x[j] = (alpha * x[j] - dot(sT + j * W, 0, (j + 7) & ~7)) / sD[j];
+    } else if (MODE == kTriSolveL) {  // x T = alpha b: x_j = (alpha b_j - sum_{k>j} x_k T_kj) / T_jj
+      for (int j = W - 1; j >= 0; --j) x[j] = (alpha * x[j] - dot(sT + j * W, j & ~7, W)) / sD[j];
+    } else if (MODE == kTriMulL) {  // y_j = alpha (x_j T_jj + sum_{k>j} x_k T_kj), ascending j
+      for (int j = 0; j < W; ++j) x[j] = alpha * fma(x[j], sD[j], dot(sT + j * W, j & ~7, W));
+    } else {  // kTriMulLT: y_j = alpha (x_j T_jj + sum_{k<j} x_k T_jk), descending j
+      for (int j = W - 1; j >= 0; --j) x[j] = alpha * fma(x[j], sD[j], dot(sT + j * W, 0, (j + 7) & ~7));
     }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < rows * t; e += blockDim.x) {
     int rr, c;
     if (a.lb == 0) { rr = e % rows; c = e / rows; } else { c = e % t; rr = e / t; }
-    a.B[lv_off(a.lb, row0 + rr, c, a.ldb)] = sB[rr * kTriLd + c];
+    a.B[lv_off(a.lb, row0 + rr, c, a.ldb)] = sB[rr * (W + 1) + c];
   }
 }
 
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
     // (a) local first maximum of |a(i, j)| over owned rows i >= j
     double bv = -1.0;
     int bi = 0x7fffffff;
-    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    for (int r = threadIdx.x; r < rows && threadIdx.x < kGetf2RowThreads; r += kGetf2RowThreads) {
       const int gi = r0 + r;
       if (gi < j) continue;
       const double v = fabs(sP[r * sld + j]);
@@ -311,9 +318,23 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
       if (sPiv[j] == 0.0) atomicMin(a.getrf_info, a.info_base + j + 1);
     }
     __syncthreads();
+    // (e') the same interchange in every column of the matrix outside the
+    // panel (the left factor and the trailing columns: the recursion's laswp
+    // calls folded in), by the warps the row updates leave free — this CTA's
+    // slice of those columns, loads and stores off the panel's chain
+    if (p != j && threadIdx.x >= kGetf2RowThreads) {
+      const int total = a.ncols - w;
+      const int lo = (int)((int64_t)total * g / G), hi = (int)((int64_t)total * (g + 1) / G);
+      for (int x = lo + threadIdx.x - kGetf2RowThreads; x < hi; x += blockDim.x - kGetf2RowThreads) {
+        double* col = a.A0 + (int64_t)(x < a.c0 ? x : x + w) * a.ld;
+        const double u = col[j], v = col[p];
+        col[j] = v;
+        col[p] = u;
+      }
+    }
     // (f) multipliers and the rank-1 update of the owned rows below row j
     const double piv = sPiv[j];
-    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    for (int r = threadIdx.x; r < rows && threadIdx.x < kGetf2RowThreads; r += kGetf2RowThreads) {
       const int gi = r0 + r;
       if (gi <= j) continue;
       double l = sP[r * sld + j];
@@ -347,12 +368,28 @@ __global__ void k_laswp(XLaswpArgs a) {
 }
 
 // ------------------------------------------------------------------ launchers
+constexpr size_t kTriSmem = sizeof(double) * ((size_t)kTriMax * kTriMax + kTriMax + (size_t)kTriRows * (kTriMax + 1));
+
+template <int MODE>
+cudaError_t launch_tri_mode(const XTriArgs& a, cudaStream_t st) {
+  k_tri_rows<MODE><<<(a.m + kTriRows - 1) / kTriRows, kTriRows, kTriSmem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t configure_tri_mode() {
+  return cudaFuncSetAttribute(k_tri_rows<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
+}
+
 cudaError_t launch_tri_rows(const XTriArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.t <= 0) return cudaSuccess;
   if (a.t > kTriMax) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(double) * (size_t)(kTriMax + kTriRows) * kTriLd;
-  k_tri_rows<<<(a.m + kTriRows - 1) / kTriRows, kTriRows, smem, st>>>(a);
-  return cudaGetLastError();
+  switch (a.mode) {
+    case kTriSolveLT: return launch_tri_mode<kTriSolveLT>(a, st);
+    case kTriSolveL: return launch_tri_mode<kTriSolveL>(a, st);
+    case kTriMulL: return launch_tri_mode<kTriMulL>(a, st);
+    default: return launch_tri_mode<kTriMulLT>(a, st);
+  }
 }
 
 cudaError_t launch_trti2(const XBlockArgs& a, cudaStream_t st) {
@@ -400,9 +437,11 @@ cudaError_t launch_laswp(const XLaswpArgs& a, cudaStream_t st) {
 }
 
 cudaError_t configure_xkernels() {
-  cudaError_t e = cudaFuncSetAttribute(k_tri_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * (kTriMax + kTriRows) * kTriLd));
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
+  if ((e = configure_tri_mode<kTriSolveLT>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mode<kTriSolveL>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mode<kTriMulL>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mode<kTriMulLT>()) != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_trti2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(2 * sizeof(double) * kTriMax * kTriLd));
   if (e != cudaSuccess) return e;

@@ -9,6 +9,7 @@ namespace relapack {
 constexpr int kTriMax = 64;        // widest triangular block of k_tri_rows / k_trti2 / k_lauu2
 constexpr int kGetf2Max = 32;      // widest getrf panel of k_getf2
 constexpr int kGetf2Threads = 256;
+constexpr int kGetf2RowThreads = 128;  // threads on the panel rows; the rest swap rows outside the panel
 
 enum XTriMode : int {
   kTriSolveLT = 0,  // x := alpha x T^{-T}   (x T^T = alpha b, forward)
@@ -50,6 +51,8 @@ struct XGetf2Args {
   int* cand_idx;      // 2 x grid
   double* cand_rows;  // 2 x grid x kGetf2Max
   double* diag_row;   // 2 x kGetf2Max
+  double* A0;         // element (panel row 0, column 0) of the matrix: the interchanges apply to every column
+  int ncols, c0;      // the matrix's columns; the panel's first column
   const int* d_info;
 };
 

@@ -177,30 +177,17 @@ void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m,
   // split the columns at n1; getrf(left panel) -> P1; laswp P1 on
   // the right panel; A12 := L11^{-1} A12 (unit); A22 -= A21 A12; getrf(A22)
   // -> P2; laswp P2 on the left panel's lower rows.
+  // The interchanges of a panel are applied by the panel kernel itself to every
+  // column of the matrix (k_getf2 step e'), which is what the two laswp calls
+  // of the recursion do (P1 on the right part before its solve and update, P2
+  // on the left part's lower rows after the right recursion): nothing reads
+  // those rows of the other columns in between, so the order does not matter.
   const int n1 = mn <= p.getrf_base ? mn : xsplit(mn, p.getrf_base);
   xplan_getrf(ops, p, r0, c0, m, n1, level + 1);
-  XOp sw;
-  sw.kind = XK_LASWP;
-  sw.level = level + 1;
-  sw.c = XView{0, r0, c0 + n1, 0};
-  sw.n = n - n1;
-  sw.m = r0;       // pivots [r0, r0 + n1): rows r0.. of the whole matrix
-  sw.k = r0 + n1;
-  ops.push_back(sw);
   const XView L11{0, r0, c0, 0}, A12{0, r0, c0 + n1, 0}, A21{0, r0 + n1, c0, 0}, A22{0, r0 + n1, c0 + n1, 0};
   xplan_tri(ops, p, kTriSolveLT, L11, tr(A12), n - n1, n1, 1.0, 1, level + 1);
   gemm(ops, A22, A21, tr(A12), m - n1, n - n1, n1, -1.0, 0, level + 1);
   xplan_getrf(ops, p, r0 + n1, c0 + n1, m - n1, n - n1, level + 1);
-  if (mn > n1) {
-    XOp sw2;
-    sw2.kind = XK_LASWP;
-    sw2.level = level + 1;
-    sw2.c = XView{0, r0, c0, 0};
-    sw2.n = n1;
-    sw2.m = r0 + n1;
-    sw2.k = r0 + mn;
-    ops.push_back(sw2);
-  }
 }
 
 // ------------------------------------------------------------------ dependencies
@@ -239,8 +226,8 @@ void footprint(const XOp& o, int total_rows, XRect* w, XRect* r) {
     case XK_POTF2:
       w[0] = rect(o.c, o.n, o.n);
       break;
-    case XK_GETF2:
-      w[0] = rect(o.c, o.m, o.n);
+    case XK_GETF2:  // the panel, and its interchanges in every other column: rows [r0, m) of the matrix
+      w[0] = XRect{o.c.buf, o.c.r0, total_rows, 0, 1 << 30};
       w[1] = XRect{2, 0, 1, o.c.r0, o.c.r0 + std::min(o.m, o.n)};  // its pivots
       break;
     case XK_LASWP:
