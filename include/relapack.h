@@ -327,6 +327,9 @@ RELAPACK_API int relapack_xplan_count(int op, int n, int nb, int* kinds, int max
 RELAPACK_API int relapack_xprofile_enable(int on);
 RELAPACK_API int relapack_xprofile_read(int kind, double* ms_total, double* flops_total, int* launches);
 RELAPACK_API void relapack_xprofile_reset(void);
+/* Per-launch records since the last reset, 4 doubles each: kind, recursion
+ * level (top split = 1), leading-term flops, milliseconds.  Returns the count. */
+RELAPACK_API int relapack_xprofile_records(int max, double* out);
 
 /*
  * Kernel test hooks (synchronous; test infrastructure, not a production API).

@@ -136,6 +136,8 @@ def lib():
         L.relapack_xprofile_read.argtypes = [c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_double), ip]
         L.relapack_xprofile_read.restype = c_int
         L.relapack_xprofile_reset.restype = None
+        L.relapack_xprofile_records.argtypes = [c_int, ctypes.POINTER(c_double)]
+        L.relapack_xprofile_records.restype = c_int
         L.relapack_batch_split.argtypes = [c_int, c_void_p, c_int, c_void_p]
         L.relapack_batch_split.restype = c_int
         _lib = L
@@ -514,6 +516,23 @@ def xplan_count(op: str, n: int, nb: int = 0):
 
 
 XKINDS = {"gemm": 0, "tri": 1, "trti2": 2, "lauu2": 3, "potf2": 4, "getf2": 5, "laswp": 6, "check": 7}
+
+
+def xprofile_records(fn, max_records: int = 200000):
+    """Run fn() with the §8(f) plans profiled; per-launch (kind, level, flops, ms) records."""
+    L = lib()
+    L.relapack_xprofile_reset()
+    L.relapack_xprofile_enable(1)
+    try:
+        fn()
+        buf = (ctypes.c_double * (4 * max_records))()
+        cnt = L.relapack_xprofile_records(max_records, buf)
+        kinds = {v: k for k, v in XKINDS.items()}
+        return [dict(kind=kinds[int(buf[4 * i])], level=int(buf[4 * i + 1]), flops=buf[4 * i + 2], ms=buf[4 * i + 3])
+                for i in range(cnt)]
+    finally:
+        L.relapack_xprofile_enable(0)
+        L.relapack_xprofile_reset()
 
 
 def xprofile(fn):

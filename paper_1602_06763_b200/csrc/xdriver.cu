@@ -265,7 +265,7 @@ cudaError_t capture(const XExec& x, const std::vector<std::vector<int>>& deps, c
 // events around every launch, accumulated per op kind.
 struct XProfRec {
   cudaEvent_t a, b;
-  int kind;
+  int kind, level;
   double flops;
 };
 std::mutex g_xprof_mu;
@@ -275,7 +275,7 @@ int g_xprof_on = 0;
 cudaError_t run_serial(const XExec& x, cudaStream_t st) {
   cudaError_t e = run_prologue(x, st);
   for (size_t i = 0; i < x.ops.size() && e == cudaSuccess; ++i) {
-    XProfRec r{nullptr, nullptr, (int)x.ops[i].kind, x.ops[i].flops};
+    XProfRec r{nullptr, nullptr, (int)x.ops[i].kind, x.ops[i].level, x.ops[i].flops};
     if (g_xprof_on) {
       cudaEventCreate(&r.a);
       cudaEventCreate(&r.b);
@@ -579,6 +579,24 @@ int relapack_xprofile_read(int kind, double* ms_total, double* flops_total, int*
   if (flops_total) *flops_total = fl;
   if (launches) *launches = cnt;
   return 0;
+}
+
+int relapack_xprofile_records(int max, double* out) {
+  std::lock_guard<std::mutex> lk(g_xprof_mu);
+  int cnt = 0;
+  for (const XProfRec& r : g_xprof) {
+    if (cnt >= max) break;
+    float t = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&t, r.a, r.b);
+    double* o = out + 4 * cnt;
+    o[0] = r.kind;
+    o[1] = r.level;
+    o[2] = r.flops;
+    o[3] = t;
+    ++cnt;
+  }
+  return cnt;
 }
 
 void relapack_xprofile_reset(void) {
