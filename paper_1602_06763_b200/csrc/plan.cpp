@@ -367,12 +367,17 @@ void dist_potrf(DistCtx& x, int off, int n, int level, int info_base) {
       g.flops = 2.0 * g.m * g.n * g.k;
       x.ops.push_back(g);
     }
+    // the diagonal block needs only this rank's own rows of L21: read them
+    // from the packed send buffer (solved in place there), so this SYRK —
+    // the local x local tiles — runs while the all-gather is in flight
+    // (SURVEY §8e); the GEMM above reads other ranks' rows after the unpack
     PlanOp sy{};
     sy.kind = OP_SYRK;
     sy.level = level + 1;
     sy.c_i = g0; sy.c_j = g0;
-    sy.a_i = g0; sy.a_j = off;
-    sy.b_i = g0; sy.b_j = off;
+    sy.a_buf = BUF_SEND; sy.b_buf = BUF_SEND;
+    sy.a_i = dist_owned_rows(lo, g0, x.d.rank, x.d); sy.a_j = 0;
+    sy.b_i = sy.a_i; sy.b_j = 0;
     sy.n = sy.m = g1 - g0; sy.k = n1;
     sy.flops = (double)sy.n * sy.n * n1;
     x.ops.push_back(sy);

@@ -36,6 +36,28 @@ __device__ __forceinline__ double at(const double* X, int layout, int64_t ld, in
   return X[lv_off(layout, r, c, ld)];
 }
 
+// Global -> shared staging with B loads of a thread in flight at once (a
+// plain loop waits for every load before the next one: ~0.5 us each).
+// idx(e, &src_offset, &dst_offset) -> false if element e is skipped.
+template <int B, class Idx>
+__device__ __forceinline__ void stage_in(double* dst, const double* src, int total, Idx idx) {
+  for (int e0 = threadIdx.x; e0 < total; e0 += blockDim.x * B) {
+    double v[B];
+    int64_t so[B];
+    int dof[B];
+    bool ok[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      ok[u] = e < total && idx(e, so[u], dof[u]);
+      v[u] = ok[u] ? src[so[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (ok[u]) dst[dof[u]] = v[u];
+  }
+}
+
 }  // namespace
 
 // One thread per row of B; the CTA's rows are staged through shared memory
@@ -59,22 +81,25 @@ __global__ void __launch_bounds__(kTriRows) k_tri_rows(XTriArgs a) {
   const int t = a.t;
   const int row0 = blockIdx.x * kTriRows;
   const int rows = min(kTriRows, a.m - row0);
-  for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
-    int i, j;  // element T(i, j) read in the contiguous order of T's layout
-    if (a.lt == 0) { i = e % W; j = e / W; } else { j = e % W; i = e / W; }
-    const double v = (i > j && i < t) ? at(a.T, a.lt, a.ldt, i, j) : 0.0;
-    if (kRows)
-      sT[i * W + j] = v;   // Tm[i][j] = T(i, j), j < i
-    else
-      sT[j * W + i] = v;   // Tu[j][i] = T(i, j), i > j
-  }
+  for (int e = threadIdx.x; e < W * W; e += blockDim.x) sT[e] = 0.0;
   for (int j = threadIdx.x; j < W; j += blockDim.x)
     sD[j] = (a.unit || j >= t) ? 1.0 : at(a.T, a.lt, a.ldt, j, j);
-  for (int e = threadIdx.x; e < rows * t; e += blockDim.x) {
+  __syncthreads();
+  // T(i, j), i > j, i < t, read in the contiguous order of T's layout
+  stage_in<8>(sT, a.T, t * t, [&](int e, int64_t& so, int& dof) {
+    int i, j;
+    if (a.lt == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
+    so = lv_off(a.lt, i, j, a.ldt);
+    dof = kRows ? i * W + j : j * W + i;  // Tm[i][j] = T(i, j) (j < i), or Tu[j][i] = T(i, j) (i > j)
+    return i > j;
+  });
+  stage_in<16>(sB, a.B, rows * t, [&](int e, int64_t& so, int& dof) {
     int r, c;
     if (a.lb == 0) { r = e % rows; c = e / rows; } else { c = e % t; r = e / t; }
-    sB[r * (W + 1) + c] = at(a.B, a.lb, a.ldb, row0 + r, c);
-  }
+    so = lv_off(a.lb, row0 + r, c, a.ldb);
+    dof = r * (W + 1) + c;
+    return true;
+  });
   __syncthreads();
   const int r = threadIdx.x;
   if (r < rows) {
@@ -124,11 +149,13 @@ __global__ void __launch_bounds__(kTriMax) k_trti2(XBlockArgs a) {
   double* sT = sm;
   double* sX = sm + kTriMax * kTriLd;  // sX[i * kTriLd + j] = X(i, j)
   const int t = a.n;
-  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+  stage_in<16>(sT, a.A, t * t, [&](int e, int64_t& so, int& dof) {
     int i, j;
     if (a.layout == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
-    if (i >= j) sT[i * kTriLd + j] = at(a.A, a.layout, a.ld, i, j);
-  }
+    so = lv_off(a.layout, i, j, a.ld);
+    dof = i * kTriLd + j;
+    return i >= j;
+  });
   __syncthreads();
   const int j = threadIdx.x;
   if (j < t) {
@@ -152,11 +179,13 @@ __global__ void __launch_bounds__(256) k_lauu2(XBlockArgs a) {
   if (ld_info(a.d_info) != 0) return;
   __shared__ double sT[kTriMax * kTriLd];
   const int t = a.n;
-  for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+  stage_in<8>(sT, a.A, t * t, [&](int e, int64_t& so, int& dof) {
     int i, j;
     if (a.layout == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
-    if (i >= j) sT[i * kTriLd + j] = at(a.A, a.layout, a.ld, i, j);
-  }
+    so = lv_off(a.layout, i, j, a.ld);
+    dof = i * kTriLd + j;
+    return i >= j;
+  });
   __syncthreads();
   for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
     int i, j;
@@ -189,10 +218,17 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// Grid-wide barrier (all CTAs co-resident: cooperative launch); the counter is
-// zeroed before the launch, `phase` counts the barriers passed so far.
+// Barrier of the panel warps only (named barrier 1, kGetf2RowThreads threads):
+// the interchange warps run decoupled (k_getf2).
+__device__ __forceinline__ void panel_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kGetf2RowThreads) : "memory");
+}
+
+// Grid-wide barrier of the panel warps (all CTAs co-resident: cooperative
+// launch); the counter is zeroed before the launch, `phase` counts the
+// barriers passed so far.
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& phase) {
-  __syncthreads();
+  panel_sync();
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned target = (phase + 1) * gridDim.x;
@@ -201,7 +237,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& phase) {
     __threadfence();
   }
   ++phase;
-  __syncthreads();
+  panel_sync();
 }
 
 }  // namespace
@@ -209,13 +245,17 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& phase) {
 // LU with partial pivoting of the m x w panel P (layout 0, ld), w <= kGetf2Max,
 // rows [0, m); pivots written to ipiv[0..w) as panel-relative row indices plus
 // `pivot_base` (the panel's global first row).  CTA g owns rows [g R, g R + R)
-// in shared memory.  Per column j: local first-maximum candidate -> published
-// with its whole row (and, by the owner, row j) -> grid barrier -> every CTA
-// picks the global first maximum, applies the interchange to its rows,
-// divides its multipliers by the pivot and updates its rows' trailing columns.
-// A zero pivot records info (min over the launch, atomicMin on getrf_info) and
-// skips the division (LAPACK continues).  Candidate slots are double-buffered
-// by column parity (a CTA can be at most one barrier ahead of another).
+// in shared memory.  The panel warps (threads < kGetf2RowThreads), per column
+// j: local first-maximum candidate -> published with its whole row (and, by
+// the owner, row j) -> grid barrier -> every CTA picks the global first
+// maximum, applies the interchange to its rows, divides its multipliers by the
+// pivot and updates its rows' trailing columns.  A zero pivot records info
+// (min over the launch, atomicMin on getrf_info) and skips the division
+// (LAPACK continues).  Candidate slots are double-buffered by column parity (a
+// CTA can be at most one barrier ahead of another).  The other warps apply
+// each interchange to this CTA's slice of every column outside the panel (the
+// recursion's laswp calls, folded in), following the pivots through a
+// shared-memory list at their own pace, off the panel's chain.
 __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
   if (ld_info(a.d_info) != 0) return;
   extern __shared__ double sm[];
@@ -227,123 +267,138 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
   const int sld = kGetf2Max + 1;
   double* sPiv = sP + (size_t)R * sld;      // the pivot row (w)
   double* sDiag = sPiv + kGetf2Max;         // the old row j (w)
-  __shared__ double red_v[kGetf2Threads / 32];
-  __shared__ int red_i[kGetf2Threads / 32];
+  constexpr int NPW = kGetf2RowThreads / 32;  // panel warps
+  __shared__ double red_v[NPW];
+  __shared__ int red_i[NPW];
   __shared__ int s_p;
+  __shared__ int s_pivots[kGetf2Max];       // panel-relative pivot row of each column (interchange warps)
+  __shared__ volatile int s_ready;          // columns whose pivot is in s_pivots
+  if (threadIdx.x == 0) s_ready = 0;
   for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
     const int r = e % rows, c = e / rows;
     sP[r * sld + c] = a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld];
   }
   __syncthreads();
-  unsigned phase = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jmax = min(a.m, w);  // pivots exist for the first min(m, w) columns
-  for (int j = 0; j < jmax; ++j) {
-    // (a) local first maximum of |a(i, j)| over owned rows i >= j
-    double bv = -1.0;
-    int bi = 0x7fffffff;
-    for (int r = threadIdx.x; r < rows && threadIdx.x < kGetf2RowThreads; r += kGetf2RowThreads) {
-      const int gi = r0 + r;
-      if (gi < j) continue;
-      const double v = fabs(sP[r * sld + j]);
-      if (v > bv || (v == bv && gi < bi)) { bv = v; bi = gi; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
-    __syncthreads();
-    if (warp == 0) {
-      bv = lane < kGetf2Threads / 32 ? red_v[lane] : -1.0;
-      bi = lane < kGetf2Threads / 32 ? red_i[lane] : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-    }
-    // (b) publish: value, index and the candidate row; the owner of row j publishes it too
-    const int buf = j & 1;
-    double* slot_row = a.cand_rows + ((int64_t)buf * G + g) * kGetf2Max;
-    if (threadIdx.x == 0) {
-      a.cand_val[buf * G + g] = bv;
-      a.cand_idx[buf * G + g] = bi;
-    }
-    __syncthreads();
-    const int cand_local = __shfl_sync(0xffffffffu, bi, 0) - r0;  // valid in warp 0 only
-    if (warp == 0 && bi != 0x7fffffff)
-      for (int c = lane; c < w; c += 32) slot_row[c] = sP[cand_local * sld + c];
-    if (j >= r0 && j < r0 + rows)
-      for (int c = threadIdx.x; c < w; c += blockDim.x) a.diag_row[buf * kGetf2Max + c] = sP[(j - r0) * sld + c];
-    // (c) barrier
-    grid_sync(a.bar, phase);
-    // (d) global first maximum
-    if (warp == 0) {
-      double v = -1.0;
-      int i = 0x7fffffff, who = -1;
-      for (int q = lane; q < G; q += 32) {
-        const double qv = __ldcg(a.cand_val + buf * G + q);
-        const int qi = __ldcg(a.cand_idx + buf * G + q);
-        if (qi != 0x7fffffff && (qv > v || (qv == v && qi < i))) { v = qv; i = qi; who = q; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-        const int ow = __shfl_xor_sync(0xffffffffu, who, o);
-        if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; who = ow; }
-      }
-      if (lane == 0) s_p = i;
-      const double* wr = a.cand_rows + ((int64_t)buf * G + who) * kGetf2Max;
-      for (int c = lane; c < w; c += 32) {
-        sPiv[c] = __ldcg(wr + c);
-        sDiag[c] = __ldcg(a.diag_row + buf * kGetf2Max + c);
-      }
-    }
-    __syncthreads();
-    const int p = s_p;
-    // (e) interchange rows j and p among the owned rows
-    if (p != j) {
-      if (j >= r0 && j < r0 + rows)
-        for (int c = threadIdx.x; c < w; c += blockDim.x) sP[(j - r0) * sld + c] = sPiv[c];
-      if (p >= r0 && p < r0 + rows)
-        for (int c = threadIdx.x; c < w; c += blockDim.x) sP[(p - r0) * sld + c] = sDiag[c];
-    }
-    if (g == 0 && threadIdx.x == 0) {
-      a.ipiv[j] = a.pivot_base + p;
-      if (sPiv[j] == 0.0) atomicMin(a.getrf_info, a.info_base + j + 1);
-    }
-    __syncthreads();
-    // (e') the same interchange in every column of the matrix outside the
-    // panel (the left factor and the trailing columns: the recursion's laswp
-    // calls folded in), by the warps the row updates leave free — this CTA's
-    // slice of those columns, loads and stores off the panel's chain
-    if (p != j && threadIdx.x >= kGetf2RowThreads) {
-      const int total = a.ncols - w;
-      const int lo = (int)((int64_t)total * g / G), hi = (int)((int64_t)total * (g + 1) / G);
-      for (int x = lo + threadIdx.x - kGetf2RowThreads; x < hi; x += blockDim.x - kGetf2RowThreads) {
+  if (threadIdx.x >= kGetf2RowThreads) {
+    // ---- interchange warps: every column of the matrix outside the panel
+    const int total = a.ncols - w;
+    const int lo = (int)((int64_t)total * g / G), hi = (int)((int64_t)total * (g + 1) / G);
+    const int tid = threadIdx.x - kGetf2RowThreads, nt = blockDim.x - kGetf2RowThreads;
+    for (int j = 0; j < jmax; ++j) {
+      while (s_ready <= j) __nanosleep(64);
+      const int p = s_pivots[j];
+      if (p == j) continue;
+      for (int x = lo + tid; x < hi; x += nt) {
         double* col = a.A0 + (int64_t)(x < a.c0 ? x : x + w) * a.ld;
         const double u = col[j], v = col[p];
         col[j] = v;
         col[p] = u;
       }
     }
-    // (f) multipliers and the rank-1 update of the owned rows below row j
-    const double piv = sPiv[j];
-    for (int r = threadIdx.x; r < rows && threadIdx.x < kGetf2RowThreads; r += kGetf2RowThreads) {
-      const int gi = r0 + r;
-      if (gi <= j) continue;
-      double l = sP[r * sld + j];
-      if (piv != 0.0) l = l / piv;
-      sP[r * sld + j] = l;
-      for (int c = j + 1; c < w; ++c) sP[r * sld + c] -= l * sPiv[c];
+  } else {
+    // ---- panel warps
+    unsigned phase = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = 0; j < jmax; ++j) {
+      // (a) local first maximum of |a(i, j)| over owned rows i >= j
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int r = threadIdx.x; r < rows; r += kGetf2RowThreads) {
+        const int gi = r0 + r;
+        if (gi < j) continue;
+        const double v = fabs(sP[r * sld + j]);
+        if (v > bv || (v == bv && gi < bi)) { bv = v; bi = gi; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+      panel_sync();
+      if (warp == 0) {
+        bv = lane < NPW ? red_v[lane] : -1.0;
+        bi = lane < NPW ? red_i[lane] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+      }
+      // (b) publish: value, index and the candidate row; the owner of row j publishes it too
+      const int buf = j & 1;
+      double* slot_row = a.cand_rows + ((int64_t)buf * G + g) * kGetf2Max;
+      if (threadIdx.x == 0) {
+        a.cand_val[buf * G + g] = bv;
+        a.cand_idx[buf * G + g] = bi;
+      }
+      if (warp == 0 && bi != 0x7fffffff) {
+        const int cand_local = bi - r0;
+        for (int c = lane; c < w; c += 32) slot_row[c] = sP[cand_local * sld + c];
+      }
+      if (j >= r0 && j < r0 + rows)
+        for (int c = threadIdx.x; c < w; c += kGetf2RowThreads) a.diag_row[buf * kGetf2Max + c] = sP[(j - r0) * sld + c];
+      // (c) barrier
+      grid_sync(a.bar, phase);
+      // (d) global first maximum
+      if (warp == 0) {
+        double v = -1.0;
+        int i = 0x7fffffff, who = -1;
+        for (int q = lane; q < G; q += 32) {
+          const double qv = __ldcg(a.cand_val + buf * G + q);
+          const int qi = __ldcg(a.cand_idx + buf * G + q);
+          if (qi != 0x7fffffff && (qv > v || (qv == v && qi < i))) { v = qv; i = qi; who = q; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+          const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+          if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; who = ow; }
+        }
+        if (lane == 0) {
+          s_p = i;
+          s_pivots[j] = i;
+          __threadfence_block();
+          s_ready = j + 1;  // the interchange warps may apply it
+        }
+        const double* wr = a.cand_rows + ((int64_t)buf * G + who) * kGetf2Max;
+        for (int c = lane; c < w; c += 32) {
+          sPiv[c] = __ldcg(wr + c);
+          sDiag[c] = __ldcg(a.diag_row + buf * kGetf2Max + c);
+        }
+      }
+      panel_sync();
+      const int p = s_p;
+      // (e) interchange rows j and p among the owned rows
+      if (p != j) {
+        if (j >= r0 && j < r0 + rows)
+          for (int c = threadIdx.x; c < w; c += kGetf2RowThreads) sP[(j - r0) * sld + c] = sPiv[c];
+        if (p >= r0 && p < r0 + rows)
+          for (int c = threadIdx.x; c < w; c += kGetf2RowThreads) sP[(p - r0) * sld + c] = sDiag[c];
+      }
+      if (g == 0 && threadIdx.x == 0) {
+        a.ipiv[j] = a.pivot_base + p;
+        if (sPiv[j] == 0.0) atomicMin(a.getrf_info, a.info_base + j + 1);
+      }
+      panel_sync();
+      // (f) multipliers and the rank-1 update of the owned rows below row j
+      const double piv = sPiv[j];
+      for (int r = threadIdx.x; r < rows; r += kGetf2RowThreads) {
+        const int gi = r0 + r;
+        if (gi <= j) continue;
+        double l = sP[r * sld + j];
+        if (piv != 0.0) l = l / piv;
+        sP[r * sld + j] = l;
+        for (int c = j + 1; c < w; ++c) sP[r * sld + c] -= l * sPiv[c];
+      }
+      panel_sync();
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
     const int r = e % rows, c = e / rows;
     a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld] = sP[r * sld + c];
