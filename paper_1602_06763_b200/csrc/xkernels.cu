@@ -106,28 +106,61 @@ __global__ void __launch_bounds__(kTriRows) k_tri_rows(XTriArgs a) {
     double* x = sB + r * (W + 1);
     for (int c = t; c < W; ++c) x[c] = 0.0;  // padding columns (never stored)
     const double alpha = a.alpha;
-    // sum_{k in [k0, k1)} x_k * row[k], k0 and k1 multiples of 8
-    auto dot = [&](const double* row, int k0, int k1) {
-      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-      for (int k = k0; k < k1; k += 8) {
+    constexpr bool kAsc = MODE == kTriSolveLT || MODE == kTriMulL;  // block order
+    constexpr bool kSolve = MODE == kTriSolveLT || MODE == kTriSolveL;
+    // 8-column blocks J: the off-diagonal part off[jj] = sum over the blocks K
+    // the mode reads (K < J for row sweeps, K > J for column sweeps) of
+    // x_K . S[8J + jj][8K .. 8K+7] — eight independent FMA chains, x_K loaded
+    // once per block pair, S by 16-byte broadcast loads — then the 8 x 8
+    // diagonal block (sequential for the solves).
+    for (int bi = 0; bi < W / 8; ++bi) {
+      const int J = kAsc ? bi : W / 8 - 1 - bi;
+      const int K0 = kRows ? 0 : J + 1, K1 = kRows ? J : W / 8;
+      double off[8];
 #pragma unroll
-        for (int u = 0; u < 8; u += 4) {
-          p0 = fma(x[k + u], row[k + u], p0);
-          p1 = fma(x[k + u + 1], row[k + u + 1], p1);
-          p2 = fma(x[k + u + 2], row[k + u + 2], p2);
-          p3 = fma(x[k + u + 3], row[k + u + 3], p3);
+      for (int jj = 0; jj < 8; ++jj) off[jj] = 0.0;
+      for (int K = K0; K < K1; ++K) {
+        double xk[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) xk[kk] = x[8 * K + kk];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const double2* srow = reinterpret_cast<const double2*>(sT + (8 * J + jj) * W + 8 * K);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 sv = srow[q];
+            off[jj] = fma(xk[2 * q], sv.x, off[jj]);
+            off[jj] = fma(xk[2 * q + 1], sv.y, off[jj]);
+          }
         }
       }
-      return (p0 + p1) + (p2 + p3);
-    };
-    if (MODE == kTriSolveLT) {  // x T^T = alpha b: x_j = (alpha b_j - sum_{k<j} x_k T_jk) / T_jj
-      for (int j = 0; j < W; ++j) x[j] = (alpha * x[j] - dot(sT + j * W, 0, (j + 7) & ~7)) / sD[j];
-    } else if (MODE == kTriSolveL) {  // x T = alpha b: x_j = (alpha b_j - sum_{k>j} x_k T_kj) / T_jj
-      for (int j = W - 1; j >= 0; --j) x[j] = (alpha * x[j] - dot(sT + j * W, j & ~7, W)) / sD[j];
-    } else if (MODE == kTriMulL) {  // y_j = alpha (x_j T_jj + sum_{k>j} x_k T_kj), ascending j
-      for (int j = 0; j < W; ++j) x[j] = alpha * fma(x[j], sD[j], dot(sT + j * W, j & ~7, W));
-    } else {  // kTriMulLT: y_j = alpha (x_j T_jj + sum_{k<j} x_k T_jk), descending j
-      for (int j = W - 1; j >= 0; --j) x[j] = alpha * fma(x[j], sD[j], dot(sT + j * W, 0, (j + 7) & ~7));
+      double xj[8], y[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) xj[jj] = x[8 * J + jj];
+      if (kSolve) {
+        // y_jj = (alpha x_jj - off_jj - sum_{kk before jj} y_kk S[jj][kk]) / D_jj
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int jj = kAsc ? i : 7 - i;
+          double acc = fma(alpha, xj[jj], -off[jj]);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            if (kAsc ? kk < jj : kk > jj) acc = fma(-y[kk], sT[(8 * J + jj) * W + 8 * J + kk], acc);
+          y[jj] = acc / sD[8 * J + jj];
+        }
+      } else {
+        // y_jj = alpha (x_jj D_jj + sum_{kk in the block's part} x_kk S[jj][kk] + off_jj)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          double acc = fma(xj[jj], sD[8 * J + jj], off[jj]);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            if (kRows ? kk < jj : kk > jj) acc = fma(xj[kk], sT[(8 * J + jj) * W + 8 * J + kk], acc);
+          y[jj] = alpha * acc;
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) x[8 * J + jj] = y[jj];
     }
   }
   __syncthreads();
