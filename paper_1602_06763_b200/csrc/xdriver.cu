@@ -73,13 +73,14 @@ struct XExec {
 
 constexpr size_t kCandDoubles = 2 * 160 + 2 * 160 * kGetf2Max + 2 * kGetf2Max;
 
-// CTAs of a getrf panel: one per RELAPACK_GETF2_ROWS rows (default 128), at
-// most one per SM — fewer CTAs make the per-column grid barrier cheaper, more
-// spread the rank-1 updates (tools/experiments r2j sweep).
+// CTAs of a getrf panel: one per RELAPACK_GETF2_ROWS rows (default 32), at
+// most one per SM — measured at n = 16384 (tools/experiments r2j / r2o): 256
+// rows per CTA 277 ms, 128 231 ms, 64 (= one CTA per SM at the top) 215 ms:
+// the per-CTA row work outweighs the cheaper barrier of fewer CTAs.
 int getf2_grid(int m, int sms) {
   static const int rows = [] {
     const char* v = getenv("RELAPACK_GETF2_ROWS");
-    const int r = v ? atoi(v) : 128;
+    const int r = v ? atoi(v) : 32;
     return r < 16 ? 16 : r;
   }();
   int g = (m + rows - 1) / rows;
