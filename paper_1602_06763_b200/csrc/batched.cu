@@ -25,6 +25,7 @@
 //    8x8 tiles of the lower triangle, K = 8), all tiles of a tile row in flight;
 //  * odd n, odd lda or a base not 16-byte aligned take a plain-load path into
 //    the same slot layout.
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -211,7 +212,7 @@ __device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], 
 template <int NMAX, int LAYOUT>
 __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::MIN_BLOCKS)
     k_batched_cls(int batch, const int* counts, const int* lists, double* const* d_A, const int* d_n,
-                  const int* d_lda, int* d_info) {
+                  const int* d_lda, int* d_info, int stagger_ns) {
   using C = BC<NMAX, LAYOUT>;
   using T = RegTri<NMAX / 8>;
   constexpr int WPC = C::WPC;
@@ -237,6 +238,11 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
   int64_t lda = d_lda[b];
   double* A = d_A[b];
   issue_load<NMAX, LAYOUT>(slot, bar, A, n, lda, lane);
+  // the second wave of CTAs (sharing SMs with the first) starts later, so the
+  // two CTAs on an SM do not run their factorization and memory phases in
+  // lockstep (RELAPACK_BATCH_STAGGER_NS; the first load is already in flight)
+  if (stagger_ns > 0 && blockIdx.x >= gridDim.x / 2)
+    for (int w = 0; w < stagger_ns; w += 1000) __nanosleep(1000);
   uint32_t parity = 0;
   while (pos < count) {
     double v[T::NT][2];
@@ -322,7 +328,12 @@ cudaError_t launch_cls(int batch, const int* counts, const int* lists, double* c
   int grid = sms * per_sm;
   const int need = (batch + C::WPC - 1) / C::WPC;
   if (grid > need) grid = need;
-  k_batched_cls<NMAX, LAYOUT><<<grid, C::WPC * 32, C::SMEM, st>>>(batch, counts, lists, d_A, d_n, d_lda, d_info);
+  static const int stagger = [] {
+    const char* v = getenv("RELAPACK_BATCH_STAGGER_NS");
+    return v ? atoi(v) : 0;
+  }();
+  k_batched_cls<NMAX, LAYOUT><<<grid, C::WPC * 32, C::SMEM, st>>>(batch, counts, lists, d_A, d_n, d_lda, d_info,
+                                                                  stagger);
   return cudaGetLastError();
 }
 
