@@ -85,6 +85,13 @@ struct BC {
   }
 };
 
+// x, hidden from loop-invariant code motion
+__device__ __forceinline__ int opaque(int x) {
+  int z;
+  asm volatile("mov.u32 %0, 0;" : "=r"(z));
+  return x + z;
+}
+
 // Pass 1: validate, bucket by size class (list[c * batch + pos]).
 __global__ void k_bucket(int batch, const int* __restrict__ d_n, const int* __restrict__ d_lda, int* d_info,
                          int* counts, int* lists) {
@@ -166,16 +173,28 @@ __device__ __forceinline__ void issue_load(double* s, uint64_t* bar, const doubl
   }
 }
 
-// Registers <- the matrix (from the prefetch slot when it was bulk-loaded,
-// else straight from global memory); identity beyond n, 0 above the diagonal.
+// Plain-load matrices (odd n or lda, unaligned base): the lanes copy the
+// lower triangle into the slot (same layout as the bulk copies), so the
+// register load below has one source.  Not unrolled: a rare path kept small.
 template <int NMAX, int LAYOUT>
-__device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], const double* s, bool from_slot,
-                                          bool square, const double* A, int n, int64_t lda, int lane) {
+__device__ __forceinline__ void plain_to_slot(double* s, const double* A, int n, int64_t lda, int lane) {
+  using C = BC<NMAX, LAYOUT>;
+  __syncwarp();  // every lane has read the previous matrix out of the slot
+#pragma unroll 1
+  for (int c = 0; c < n; ++c)
+    for (int r = c + lane; r < n; r += 32) s[C::off(r, c)] = A[lv_off(LAYOUT, r, c, lda)];
+  __syncwarp();
+}
+
+// Registers <- the matrix from the slot; identity beyond n, 0 above the
+// diagonal.  (One source only: the kernel's code size matters — the fully
+// unrolled 64-class kernel is instruction-cache bound.)
+template <int NMAX, int LAYOUT>
+__device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], const double* s, bool square, int n,
+                                          int lane) {
   using C = BC<NMAX, LAYOUT>;
   using T = RegTri<NMAX / 8>;
   const int g = lane >> 2, t = lane & 3;
-  // separate loops (warp-uniform branches): a select between the shared and
-  // the global load would issue both
   if (C::SQ && square) {
 #pragma unroll
     for (int i = 0; i < C::TN; ++i)
@@ -186,16 +205,6 @@ __device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], 
           const int r = 8 * i + g, c = 8 * k + 2 * t + q;
           v[T::id(i, k)][q] = r >= c ? s[r + c * C::SQ_LD] : (r == c ? 1.0 : 0.0);
         }
-  } else if (from_slot) {
-#pragma unroll
-    for (int i = 0; i < C::TN; ++i)
-#pragma unroll
-      for (int k = 0; k <= i; ++k)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-          v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? s[C::off(r, c)] : (r == c ? 1.0 : 0.0);
-        }
   } else {
 #pragma unroll
     for (int i = 0; i < C::TN; ++i)
@@ -204,7 +213,7 @@ __device__ __forceinline__ void load_regs(double (&v)[RegTri<NMAX / 8>::NT][2], 
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-          v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? A[lv_off(LAYOUT, r, c, lda)] : (r == c ? 1.0 : 0.0);
+          v[T::id(i, k)][q] = (r < n && c < n && r >= c) ? s[C::off(r, c)] : (r == c ? 1.0 : 0.0);
         }
   }
 }
@@ -254,8 +263,13 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
     } else if (bulk) {
       mbar_wait(bar, parity);
       parity ^= 1u;
+    } else {
+      plain_to_slot<NMAX, LAYOUT>(slot, A, n, lda, lane);
     }
-    load_regs<NMAX, LAYOUT>(v, slot, bulk, sq, A, n, lda, lane);
+    // the slot offsets of the 72 (n = 64) register elements depend only on the
+    // lane: computed from an opaque copy of it, so they are not hoisted out of
+    // the matrix loop and held live across it (register spills)
+    load_regs<NMAX, LAYOUT>(v, slot, sq, n, opaque(lane));
     // prefetch this warp's next matrix into the (now consumed) slot
     const int npos = pos + stride;
     int nb = 0, nn = 0;
@@ -268,37 +282,27 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
       nA = d_A[nb];
       issue_load<NMAX, LAYOUT>(slot, bar, nA, nn, nlda, lane);
     }
+    // the lower triangle of L is stored panel by panel as it becomes final
+    // (only the uplo triangle is written)
+    double* const Al = A + lv_off(LAYOUT, g, 2 * t, lda);
+    const int64_t cs = LAYOUT == kLayoutN ? lda : 1, rs = LAYOUT == kLayoutN ? 1 : lda;  // column / row stride
+    auto sink = [&](int k) {
+      double* Ak = Al + 8 * k * cs;
+#pragma unroll
+      for (int i = k; i < C::TN; ++i)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = 8 * i + g, c = 8 * k + 2 * t + q;
+          if (r < n && c < n && r >= c) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q];
+        }
+    };
 #if RELAPACK_BATCH_MODE == 1  // tools/microbench only: memory phases alone
     const int fail = 0;
+#pragma unroll
+    for (int k = 0; k < C::TN; ++k) sink(k);
 #else
-    const int fail = reg_potrf<NMAX / 8>(v, lane);
+    const int fail = reg_potrf<NMAX / 8>(v, lane, sink);
 #endif
-    // store the lower triangle of L (only the uplo triangle is written)
-    if (n == NMAX) {
-      // full class size: only diagonal tiles need a predicate; one lane base
-      // pointer, tile offsets are (i, k) multiples of 8 rows / columns
-      double* Al = A + lv_off(LAYOUT, g, 2 * t, lda);
-      const int64_t cs = LAYOUT == kLayoutN ? lda : 1, rs = LAYOUT == kLayoutN ? 1 : lda;  // column / row stride
-#pragma unroll
-      for (int k = 0; k < C::TN; ++k) {
-        double* Ak = Al + 8 * k * cs;
-#pragma unroll
-        for (int i = k; i < C::TN; ++i)
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            if (i > k || g >= 2 * t + q) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q];
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < C::TN; ++i)
-#pragma unroll
-        for (int k = 0; k <= i; ++k)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-            if (r < n && c < n && r >= c) A[lv_off(LAYOUT, r, c, lda)] = v[T::id(i, k)][q];
-          }
-    }
     if (lane == 0) d_info[b] = fail;
     pos = npos;
     b = nb;

@@ -49,8 +49,15 @@ __device__ __forceinline__ double tile_frag(double x0, double x1, int ks, int g,
 // multiplier l_kc of a finished column is 0.  (Plain substitution, no
 // explicit inverses: exact on integer factors whose pivots are perfect
 // squares, backward stable otherwise.)
-template <int TN>
-__device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lane) {
+// sink(p) is called once panel p's tiles (i, p), i >= p, hold their final
+// values, before the trailing update: a caller that stores them there (the
+// batched kernel) lets them die early, which lowers the register peak.
+struct NoSink {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+
+template <int TN, class Sink = NoSink>
+__device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lane, Sink sink = Sink()) {
   using T = RegTri<TN>;
   const int g = lane >> 2, t = lane & 3;
   // failed pivots as a bit mask (branch-free: every shuffle stays in converged code)
@@ -58,7 +65,9 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
 #pragma unroll
   for (int p = 0; p < TN; ++p) {
     const int D = T::id(p, p);
-    double dv[8], rv[8];
+    // this lane's columns 2t, 2t + 1: their 1/sqrt(d) and d, picked as the
+    // panel's columns go by (no per-panel arrays of all eight)
+    double r0 = 0.0, r1 = 0.0, d0 = 1.0, d1 = 1.0;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int e = c & 1, tc = c >> 1;
@@ -75,8 +84,13 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
       }
       bad |= (uint64_t)(!(d >= kMinPivot)) << (8 * p + c);
       const double r = rsqrt_nr(d);
-      dv[c] = d;
-      rv[c] = r;
+      if (e == 0) {
+        r0 = t == tc ? r : r0;
+        d0 = t == tc ? d : d0;
+      } else {
+        r1 = t == tc ? r : r1;
+        d1 = t == tc ? d : d1;
+      }
       if (c < 7) {
         const double l0 = 2 * t > c ? a0 * r : 0.0;
         const double l1 = 2 * t + 1 > c ? a1 * r : 0.0;
@@ -89,14 +103,6 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
       }
     }
     // scale the panel: column 2t + q by its r; the diagonal gets sqrt(d)
-    double r0 = rv[0], r1 = rv[1], d0 = dv[0], d1 = dv[1];
-#pragma unroll
-    for (int q = 1; q < 4; ++q) {
-      r0 = t == q ? rv[2 * q] : r0;
-      r1 = t == q ? rv[2 * q + 1] : r1;
-      d0 = t == q ? dv[2 * q] : d0;
-      d1 = t == q ? dv[2 * q + 1] : d1;
-    }
 #pragma unroll
     for (int i = p + 1; i < TN; ++i) {
       v[T::id(i, p)][0] *= r0;
@@ -112,6 +118,7 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
         fr[i][0] = tile_frag(v[T::id(i, p)][0], v[T::id(i, p)][1], 0, g, t);
         fr[i][1] = tile_frag(v[T::id(i, p)][0], v[T::id(i, p)][1], 1, g, t);
       }
+      sink(p);
       // trailing update, the next panel's column of tiles first
 #pragma unroll
       for (int k = p + 1; k < TN; ++k)
@@ -120,6 +127,8 @@ __device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lan
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
             dmma_884(v[T::id(i, k)][0], v[T::id(i, k)][1], -fr[i][ks], fr[k][ks]);
+    } else {
+      sink(p);
     }
   }
   return bad ? __ffsll((long long)bad) : 0;
