@@ -39,6 +39,9 @@
 
 namespace relapack {
 
+#ifndef RELAPACK_BATCH_DESC_AHEAD
+#define RELAPACK_BATCH_DESC_AHEAD 1
+#endif
 #ifndef RELAPACK_BATCH_SQUARE
 #define RELAPACK_BATCH_SQUARE 1
 #endif
@@ -54,6 +57,9 @@ struct BC {
   static constexpr int WPC = 4;  // warps (matrices in flight) per CTA
   // CTAs per SM the register budget is sized for: more warps in flight hide
   // the per-matrix column chain (compile-time knobs RELAPACK_BATCH_MINB<NMAX>)
+#ifndef RELAPACK_BATCH_MINB16
+#define RELAPACK_BATCH_MINB16 4
+#endif
 #ifndef RELAPACK_BATCH_MINB32
 #define RELAPACK_BATCH_MINB32 3
 #endif
@@ -64,7 +70,7 @@ struct BC {
 #define RELAPACK_BATCH_MINB64 2
 #endif
   static constexpr int MIN_BLOCKS =
-      NMAX == 64 ? RELAPACK_BATCH_MINB64 : NMAX == 48 ? RELAPACK_BATCH_MINB48 : NMAX == 32 ? RELAPACK_BATCH_MINB32 : 8;
+      NMAX == 64 ? RELAPACK_BATCH_MINB64 : NMAX == 48 ? RELAPACK_BATCH_MINB48 : NMAX == 32 ? RELAPACK_BATCH_MINB32 : RELAPACK_BATCH_MINB16;
   // even-packed lower triangle: NMAX (NMAX/2 + 1) doubles per prefetch slot;
   // n <= 32, uplo L: room for the whole column-major square at stride SQ_LD
   // instead (the square path below)
@@ -253,8 +259,23 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
   if (stagger_ns > 0 && blockIdx.x >= gridDim.x / 2)
     for (int w = 0; w < stagger_ns; w += 1000) __nanosleep(1000);
   uint32_t parity = 0;
+  // the next matrix's list entry, one iteration ahead (RELAPACK_BATCH_DESC_AHEAD):
+  // its descriptor loads then start before this matrix's wait and register load
+  constexpr bool kAhead = RELAPACK_BATCH_DESC_AHEAD && NMAX == 64;  // measured: helps the 64-class only
+  int nb_ahead = (kAhead && pos + stride < count) ? list[pos + stride] : 0;
   while (pos < count) {
     double v[T::NT][2];
+    const int npos = pos + stride;
+    int nb = 0, nn = 0;
+    int64_t nlda = 0;
+    double* nA = nullptr;
+    if (kAhead && npos < count) {
+      nb = nb_ahead;
+      nn = d_n[nb];
+      nlda = d_lda[nb];
+      nA = d_A[nb];
+      nb_ahead = npos + stride < count ? list[npos + stride] : 0;
+    }
     const bool sq = square_ok<NMAX, LAYOUT>(A, n, lda);
     const bool bulk = bulk_ok<NMAX, LAYOUT>(A, n, lda);
     if (sq) {
@@ -271,15 +292,13 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
     // the matrix loop and held live across it (register spills)
     load_regs<NMAX, LAYOUT>(v, slot, sq, n, opaque(lane));
     // prefetch this warp's next matrix into the (now consumed) slot
-    const int npos = pos + stride;
-    int nb = 0, nn = 0;
-    int64_t nlda = 0;
-    double* nA = nullptr;
     if (npos < count) {
-      nb = list[npos];
-      nn = d_n[nb];
-      nlda = d_lda[nb];
-      nA = d_A[nb];
+      if (!kAhead) {
+        nb = list[npos];
+        nn = d_n[nb];
+        nlda = d_lda[nb];
+        nA = d_A[nb];
+      }
       issue_load<NMAX, LAYOUT>(slot, bar, nA, nn, nlda, lane);
     }
     // the lower triangle of L is stored panel by panel as it becomes final

@@ -56,81 +56,116 @@ struct NoSink {
   __device__ __forceinline__ void operator()(int) const {}
 };
 
-template <int TN, class Sink = NoSink>
-__device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lane, Sink sink = Sink()) {
+#ifndef RELAPACK_REG_DEFER
+#define RELAPACK_REG_DEFER 0
+#endif
+
+// Deferred trailing update of panel PP (fragments fp) on the tiles (i, k),
+// PP + 2 <= k <= i: DMMA number [lo, hi) of its list (all k-step 0 DMMAs
+// first, then k-step 1, so a tile's two dependent DMMAs are far apart).
+template <int TN, int PP>
+__device__ __forceinline__ void reg_deferred(double (&v)[RegTri<TN>::NT][2], const double (&fp)[TN][2], int lo, int hi) {
+  using T = RegTri<TN>;
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+    for (int k = PP + 2; k < TN; ++k)
+#pragma unroll
+      for (int i = k; i < TN; ++i) {
+        // position of (ks, k, i) in the list
+        const int idx = ks * ((TN - PP - 2) * (TN - PP - 1) / 2) + ((k - PP - 2) * (2 * TN - PP - k - 1)) / 2 + (i - k);
+        if (idx >= lo && idx < hi) dmma_884(v[T::id(i, k)][0], v[T::id(i, k)][1], -fp[i][ks], fp[k][ks]);
+      }
+}
+
+// Panel P of the register factorization (compile-time P: every register
+// index is static), then panel P + 1.
+template <int TN, int P, class Sink>
+__device__ __forceinline__ void reg_panel(double (&v)[RegTri<TN>::NT][2], double (&fprev)[TN][2], int lane,
+                                          uint64_t& bad, Sink& sink) {
   using T = RegTri<TN>;
   const int g = lane >> 2, t = lane & 3;
-  // failed pivots as a bit mask (branch-free: every shuffle stays in converged code)
-  uint64_t bad = 0;
+  constexpr int D = T::id(P, P);
+  constexpr bool kDefer = RELAPACK_REG_DEFER != 0;
+  constexpr int ndef = (kDefer && P >= 1) ? (TN - P - 1) * (TN - P) : 0;  // panel P-1's deferred DMMAs
+  // this lane's columns 2t, 2t + 1: their 1/sqrt(d) and d, picked as the
+  // panel's columns go by (no per-panel arrays of all eight)
+  double r0 = 0.0, r1 = 0.0, d0 = 1.0, d1 = 1.0;
 #pragma unroll
-  for (int p = 0; p < TN; ++p) {
-    const int D = T::id(p, p);
-    // this lane's columns 2t, 2t + 1: their 1/sqrt(d) and d, picked as the
-    // panel's columns go by (no per-panel arrays of all eight)
-    double r0 = 0.0, r1 = 0.0, d0 = 1.0, d1 = 1.0;
+  for (int c = 0; c < 8; ++c) {
+    const int e = c & 1, tc = c >> 1;
+    const int quad_src = (lane & ~3) | tc;
+    const double d = __shfl_sync(0xffffffffu, v[D][e], 4 * c + tc);
+    // unscaled column values
+    double a0 = 0.0, a1 = 0.0;
+    double xc[TN];
+    if (c < 7) {
+      a0 = __shfl_sync(0xffffffffu, v[D][e], 8 * t + tc);      // a(8P + 2t,     8P + c)
+      a1 = __shfl_sync(0xffffffffu, v[D][e], 8 * t + 4 + tc);  // a(8P + 2t + 1, 8P + c)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int e = c & 1, tc = c >> 1;
-      const int quad_src = (lane & ~3) | tc;
-      const double d = __shfl_sync(0xffffffffu, v[D][e], 4 * c + tc);
-      // unscaled column values
-      double a0 = 0.0, a1 = 0.0;
-      double xc[TN];
-      if (c < 7) {
-        a0 = __shfl_sync(0xffffffffu, v[D][e], 8 * t + tc);      // a(8p + 2t,     8p + c)
-        a1 = __shfl_sync(0xffffffffu, v[D][e], 8 * t + 4 + tc);  // a(8p + 2t + 1, 8p + c)
-#pragma unroll
-        for (int i = p; i < TN; ++i) xc[i] = __shfl_sync(0xffffffffu, v[T::id(i, p)][e], quad_src);
-      }
-      bad |= (uint64_t)(!(d >= kMinPivot)) << (8 * p + c);
-      const double r = rsqrt_nr(d);
-      if (e == 0) {
-        r0 = t == tc ? r : r0;
-        d0 = t == tc ? d : d0;
-      } else {
-        r1 = t == tc ? r : r1;
-        d1 = t == tc ? d : d1;
-      }
-      if (c < 7) {
-        const double l0 = 2 * t > c ? a0 * r : 0.0;
-        const double l1 = 2 * t + 1 > c ? a1 * r : 0.0;
-#pragma unroll
-        for (int i = p; i < TN; ++i) {
-          const double x = xc[i] * r;  // l(8i + g, 8p + c)
-          v[T::id(i, p)][0] = fma(-x, l0, v[T::id(i, p)][0]);
-          v[T::id(i, p)][1] = fma(-x, l1, v[T::id(i, p)][1]);
-        }
-      }
+      for (int i = P; i < TN; ++i) xc[i] = __shfl_sync(0xffffffffu, v[T::id(i, P)][e], quad_src);
     }
-    // scale the panel: column 2t + q by its r; the diagonal gets sqrt(d)
-#pragma unroll
-    for (int i = p + 1; i < TN; ++i) {
-      v[T::id(i, p)][0] *= r0;
-      v[T::id(i, p)][1] *= r1;
-    }
-    v[D][0] = g == 2 * t ? sqrt_from_rsqrt(d0, r0) : v[D][0] * r0;
-    v[D][1] = g == 2 * t + 1 ? sqrt_from_rsqrt(d1, r1) : v[D][1] * r1;
-    if (p + 1 < TN) {
-      // A/B fragments of the panel tiles: fr[i][ks] = L(8i + g, 8p + 4ks + t)
-      double fr[TN][2];
-#pragma unroll
-      for (int i = p + 1; i < TN; ++i) {
-        fr[i][0] = tile_frag(v[T::id(i, p)][0], v[T::id(i, p)][1], 0, g, t);
-        fr[i][1] = tile_frag(v[T::id(i, p)][0], v[T::id(i, p)][1], 1, g, t);
-      }
-      sink(p);
-      // trailing update, the next panel's column of tiles first
-#pragma unroll
-      for (int k = p + 1; k < TN; ++k)
-#pragma unroll
-        for (int i = k; i < TN; ++i)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-            dmma_884(v[T::id(i, k)][0], v[T::id(i, k)][1], -fr[i][ks], fr[k][ks]);
+    bad |= (uint64_t)(!(d >= kMinPivot)) << (8 * P + c);
+    const double r = rsqrt_nr(d);
+    if constexpr (ndef > 0) reg_deferred<TN, (P >= 1 ? P - 1 : 0)>(v, fprev, ndef * c / 8, ndef * (c + 1) / 8);
+    if (e == 0) {
+      r0 = t == tc ? r : r0;
+      d0 = t == tc ? d : d0;
     } else {
-      sink(p);
+      r1 = t == tc ? r : r1;
+      d1 = t == tc ? d : d1;
+    }
+    if (c < 7) {
+      const double l0 = 2 * t > c ? a0 * r : 0.0;
+      const double l1 = 2 * t + 1 > c ? a1 * r : 0.0;
+#pragma unroll
+      for (int i = P; i < TN; ++i) {
+        const double x = xc[i] * r;  // l(8i + g, 8P + c)
+        v[T::id(i, P)][0] = fma(-x, l0, v[T::id(i, P)][0]);
+        v[T::id(i, P)][1] = fma(-x, l1, v[T::id(i, P)][1]);
+      }
     }
   }
+  // scale the panel: column 2t + q by its r; the diagonal gets sqrt(d)
+#pragma unroll
+  for (int i = P + 1; i < TN; ++i) {
+    v[T::id(i, P)][0] *= r0;
+    v[T::id(i, P)][1] *= r1;
+  }
+  v[D][0] = g == 2 * t ? sqrt_from_rsqrt(d0, r0) : v[D][0] * r0;
+  v[D][1] = g == 2 * t + 1 ? sqrt_from_rsqrt(d1, r1) : v[D][1] * r1;
+  if constexpr (P + 1 < TN) {
+    // A/B fragments of the panel tiles: fr[i][ks] = L(8i + g, 8P + 4ks + t)
+#pragma unroll
+    for (int i = P + 1; i < TN; ++i) {
+      fprev[i][0] = tile_frag(v[T::id(i, P)][0], v[T::id(i, P)][1], 0, g, t);
+      fprev[i][1] = tile_frag(v[T::id(i, P)][0], v[T::id(i, P)][1], 1, g, t);
+    }
+    sink(P);
+    // the next panel's column of tiles now; the rest deferred into panel P+1
+    // (or at once without RELAPACK_REG_DEFER)
+#pragma unroll
+    for (int k = P + 1; k < (kDefer ? P + 2 : TN); ++k)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int i = k; i < TN; ++i) dmma_884(v[T::id(i, k)][0], v[T::id(i, k)][1], -fprev[i][ks], fprev[k][ks]);
+    reg_panel<TN, P + 1>(v, fprev, lane, bad, sink);
+  } else {
+    sink(P);
+  }
+}
+
+template <int TN, class Sink = NoSink>
+__device__ __forceinline__ int reg_potrf(double (&v)[RegTri<TN>::NT][2], int lane, Sink sink = Sink()) {
+  // failed pivots as a bit mask (branch-free: every shuffle stays in converged code)
+  uint64_t bad = 0;
+  // Panel P-1's update of the columns k >= P+1 is not issued in one block
+  // after panel P-1 (the warp would stall on the DMMA pipe in front of panel
+  // P's column chain) but spread over panel P's eight column steps, where the
+  // chain leaves issue slots idle (RELAPACK_REG_DEFER).
+  double fprev[TN][2];
+  reg_panel<TN, 0>(v, fprev, lane, bad, sink);
   return bad ? __ffsll((long long)bad) : 0;
 }
 

@@ -34,27 +34,6 @@ int main() {
       cudaEventRecord(e); cudaEventSynchronize(e);
       float ms; cudaEventElapsedTime(&ms, a, e); if (r > 0 && ms < best) best = ms;
     }
-#ifdef RELAPACK_TEAM_PROBE
-    if (n >= 48) {
-      int one = 1;
-      cudaMemcpyToSymbol(g_tprobe_on, &one, 4);
-      cudaMemcpy(d, d0, h.size() * 8, cudaMemcpyDeviceToDevice);
-      launch_potf2_batched(kLayoutN, count, dn, dp, dn, dinfo, 0);
-      cudaDeviceSynchronize();
-      long long pr[2][8][6];
-      cudaMemcpyFromSymbol(pr, g_tprobe, sizeof(pr));
-      const long long t0 = pr[0][0][0];
-      for (int q = 0; q < n / 8; ++q) {
-        const int w = q & 1;
-        printf("n=%d panel %d (warp %d): start %6lld | sync wait %5lld | col update %5lld | factor %5lld | publish %5lld | own updates %5lld | end %6lld\n",
-               n, q, w, pr[w][q][0] - t0, q ? pr[w][q][1] - pr[w][q][0] : 0, q ? pr[w][q][2] - pr[w][q][1] : 0,
-               pr[w][q][3] - pr[w][q][2], q + 1 < n / 8 ? pr[w][q][4] - pr[w][q][3] : 0,
-               q + 1 < n / 8 ? pr[w][q][5] - pr[w][q][4] : 0, pr[w][q][5] - t0);
-      }
-      int zero = 0;
-      cudaMemcpyToSymbol(g_tprobe_on, &zero, 4);
-    }
-#endif
     double tri = 8.0 * n * (n + 1) * (double)count;
     printf("mode %d n=%2d count=%d: %.3f ms  %.0f GB/s (tri r+w)  %.2f us per matrix-slot (%s)\n", RELAPACK_BATCH_MODE, n, count, best,
            tri / best / 1e6, best * 1e3 / count, cudaGetErrorString(cudaGetLastError()));
