@@ -515,7 +515,7 @@ def xplan_count(op: str, n: int, nb: int = 0):
     return cnt, list(kinds)[:cnt], fl.value
 
 
-XKINDS = {"gemm": 0, "tri": 1, "trti2": 2, "lauu2": 3, "potf2": 4, "getf2": 5, "laswp": 6, "check": 7}
+XKINDS = {"gemm": 0, "tri": 1, "trti2": 2, "lauu2": 3, "potf2": 4, "getf2": 5, "laswp": 6, "check": 7, "perm": 8}
 
 
 def xprofile_records(fn, max_records: int = 200000):

@@ -62,6 +62,7 @@ struct XExec {
   double* cand = nullptr;  // per getf2 slot: 2G vals, 2G*kGetf2Max rows, 2*kGetf2Max diag rows
   int* cand_idx = nullptr;
   int sms = 148;
+  int cl_size = 0;  // getrf cluster panels: CTAs per cluster
   bool is_getrf = false, has_check = false;
   cudaGraphExec_t exec = nullptr;
   ~XExec() {
@@ -121,6 +122,20 @@ cudaError_t launch_xop(const XExec& x, size_t i, cudaStream_t st) {
     }
     case XK_GETF2: {
       const XOperand P = resolve(b, o.c);
+      if (o.mode == 1) {
+        XGetf2ClArgs a{};
+        a.P = P.p;
+        a.ld = P.ld;
+        a.m = o.m;
+        a.w = o.n;
+        a.rows_per_cta = (o.m + x.cl_size - 1) / x.cl_size;
+        a.ipiv = b.ipiv + o.c.c0;
+        a.pivot_base = o.c.r0 + 1;
+        a.getrf_info = x.d_info + 1;
+        a.info_base = o.info_base;
+        a.d_info = x.d_info;
+        return launch_getf2_cl(a, x.cl_size, st);
+      }
       const int G = getf2_grid(o.m, x.sms);
       double* c = x.cand + (size_t)x.slot[i] * kCandDoubles;
       XGetf2Args a{};
@@ -143,6 +158,11 @@ cudaError_t launch_xop(const XExec& x, size_t i, cudaStream_t st) {
       a.c0 = o.c.c0;
       a.d_info = x.d_info;
       return launch_getf2(a, G, st);
+    }
+    case XK_PERM: {
+      const XOperand A = resolve(b, o.c);
+      XPermArgs a{A.p, A.ld, o.n, b.ipiv, o.k, o.m, o.c.r0 + 1, x.d_info};
+      return launch_permute(a, st);
     }
     case XK_LASWP: {
       const XOperand A = resolve(b, XView{o.c.buf, 0, o.c.c0, 0});
@@ -172,7 +192,7 @@ cudaError_t setup_exec(XExec& x, const std::vector<uint64_t>& anc) {
   if ((e = cudaMalloc(&x.d_info, 4 * sizeof(int))) != cudaSuccess) return e;  // before the descriptors use it
   for (size_t i = 0; i < n; ++i) {
     const XOp& o = x.ops[i];
-    if (o.kind == XK_GETF2) x.slot[i] = nget++;
+    if (o.kind == XK_GETF2 && o.mode == 0) x.slot[i] = nget++;
     if (o.kind != XK_GEMM) continue;
     const XOperand C = resolve(x.bufs, o.c), A = resolve(x.bufs, o.a), B = resolve(x.bufs, o.b);
     UpdateOp& u = x.upd[i];
@@ -341,6 +361,7 @@ int x_run(const std::string& key, const std::vector<XOp>& ops_in, const XBuffers
     p->bufs = bufs;
     p->is_getrf = is_getrf;
     p->has_check = has_check;
+    p->cl_size = is_getrf ? getf2_cluster_caps() : 0;
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev);
     std::vector<std::vector<int>> deps;
     std::vector<uint64_t> anc;
@@ -410,7 +431,7 @@ XParams x_params() {
 
 std::string params_key(const XParams& p) {
   char b[96];
-  snprintf(b, sizeof(b), " tb%d st%d gb%d", p.tri_base, p.split_tile, p.getrf_base);
+  snprintf(b, sizeof(b), " tb%d st%d gb%d cl%d", p.tri_base, p.split_tile, p.getrf_base, p.getf2_cluster);
   return b;
 }
 
@@ -542,7 +563,9 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
   if (std::min(*m, *n) > 0 && (!ipiv || !device_ptr(ipiv))) { *info = -5; return; }
   *info = 0;
   if (*m == 0 || *n == 0) return;
-  const XParams p = x_params();
+  XParams p = x_params();
+  p.getf2_cluster = getf2_cluster_caps();
+  p.getrf_cols = *n;
   std::vector<XOp> ops;
   xplan_getrf(ops, p, 0, 0, *m, *n, 0);
   XBuffers b;

@@ -22,8 +22,14 @@
 // layout 1 at X[c + r*ld] (common.cuh lv_off).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
+#include "kernels.h"
 #include "xkernels.h"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace relapack {
 
@@ -438,6 +444,294 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
   }
 }
 
+// ---- cluster panel
+// LU with partial pivoting of the m x w panel by one cluster of C CTAs, the
+// panel held in REGISTERS: CTA g owns rows [g R, g R + R), thread t its rows
+// t + T s (s < S), all W columns (W, S, T compile-time: every register index
+// static, runtime column j by predicates).  Per column j (the same
+// arithmetic as k_getf2):
+//   (a) the first maximum |a(i, j)|, i >= j, of the thread's rows — tracked
+//       while column j was updated (step f of column j-1) — reduced over the
+//       warp (shuffles) and the CTA;
+//   (b) published with the whole candidate row in this CTA's shared memory;
+//       the owner of row j publishes row j too (slots by column parity: a CTA
+//       is at most one barrier ahead);
+//   (c) cluster barrier (barrier.cluster arrive.release / wait.acquire);
+//   (d) every CTA reads the C candidates through DSMEM, picks the global first
+//       maximum p and reads the pivot row and row j from their publishers;
+//   (e) the owners of rows j and p interchange them in their registers;
+//   (f) multipliers l = a(i, j) / a(p, j) (true division, as the oracle) and
+//       the rank-1 update of the rows below j (a zero pivot records info and
+//       skips the division).
+// No global-memory round trip and no shared-memory traffic proportional to
+// the panel inside the column loop.
+#ifdef RELAPACK_GETF2_PROBE  // tools/microbench/getf2_probe.cu only: phase cycles accumulated in registers
+__device__ long long g_gprobe[8];
+#define GPROBE(k)                    \
+  {                                  \
+    const long long now = clock64(); \
+    pacc[k] += now - t_last;         \
+    t_last = now;                    \
+  }
+#else
+#define GPROBE(k)
+#endif
+
+template <int T, int S, int W>
+__global__ void __launch_bounds__(T) k_getf2_clr(XGetf2ClArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  if (ld_info(a.d_info) != 0) return;  // the same flag for every CTA of the cluster
+#ifdef RELAPACK_GETF2_PROBE
+  long long t_last = clock64(), pacc[8] = {};
+#endif
+  constexpr int NW = T / 32;
+  const int rank = (int)cl.block_rank(), C = (int)cl.num_blocks();
+  const int w = a.w, R = a.rows_per_cta, m = a.m;
+  const int r0 = rank * R;
+  const int rows = max(0, min(R, m - r0));
+  __shared__ double pub[2][2][W];  // [parity][candidate row | row j]
+  __shared__ double cand_v[2];
+  __shared__ int cand_i[2];
+  __shared__ double sPiv[W], sDiag[W];
+  __shared__ double red_v[NW];
+  __shared__ int red_i[NW];
+  __shared__ int s_bi, s_p;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double x[S][W];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int r = tid + T * s;
+#pragma unroll
+    for (int c = 0; c < W; ++c) x[s][c] = (r < rows && c < w) ? a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld] : 0.0;
+  }
+  // column 0's candidates
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (tid + T * s < rows && fabs(x[s][0]) > bv) {  // rows ascend: the first maximum wins ties
+      bv = fabs(x[s][0]);
+      bi = r0 + tid + T * s;
+    }
+  cl.sync();
+  GPROBE(6);
+  const int jmax = min(m, w);
+  for (int j = 0; j < jmax; ++j) {
+    const int buf = j & 1;
+    // (a)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      red_v[warp] = bv;
+      red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      bv = lane < NW ? red_v[lane] : -1.0;
+      bi = lane < NW ? red_i[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        cand_v[buf] = bv;
+        cand_i[buf] = bi;
+        s_bi = bi;
+      }
+    }
+    __syncthreads();
+    // (b) the owners of the candidate row and of row j publish them
+    {
+      const int cr = s_bi - r0, jr = j - r0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (cr == tid + T * s)
+#pragma unroll
+          for (int c = 0; c < W; ++c) pub[buf][0][c] = x[s][c];
+        if (jr == tid + T * s)
+#pragma unroll
+          for (int c = 0; c < W; ++c) pub[buf][1][c] = x[s][c];
+      }
+    }
+    GPROBE(0);
+    // (c)
+    cl.sync();
+    GPROBE(1);
+    // (d)
+    if (warp == 0) {
+      double v = -1.0;
+      int i = 0x7fffffff, who = 0;
+      if (lane < C) {
+        v = *cl.map_shared_rank(&cand_v[buf], lane);
+        i = *cl.map_shared_rank(&cand_i[buf], lane);
+        who = lane;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+        if (ov > v || (ov == v && oi < i)) {
+          v = ov;
+          i = oi;
+          who = ow;
+        }
+      }
+      if (lane == 0) s_p = i;
+      if (lane < W) {
+        sPiv[lane] = cl.map_shared_rank(&pub[buf][0][0], who)[lane];
+        sDiag[lane] = cl.map_shared_rank(&pub[buf][1][0], j / R)[lane];
+      }
+    }
+    __syncthreads();
+    GPROBE(2);
+    // (e)
+    const int p = s_p;
+    if (p != j) {
+      const int jr = j - r0, pr = p - r0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (jr == tid + T * s)
+#pragma unroll
+          for (int c = 0; c < W; ++c) x[s][c] = sPiv[c];
+        if (pr == tid + T * s)
+#pragma unroll
+          for (int c = 0; c < W; ++c) x[s][c] = sDiag[c];
+      }
+    }
+    if (rank == 0 && tid == 0) {
+      a.ipiv[j] = a.pivot_base + p;
+      if (sPiv[j] == 0.0) atomicMin(a.getrf_info, a.info_base + j + 1);
+    }
+    GPROBE(4);
+    // (f) rows below j; the next column's candidates on the way.  Column j
+    // and j + 1 are picked by select chains, so the division and the compare
+    // appear once in the code, not once per column.
+    const double piv = sPiv[j];
+    double pv[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) pv[c] = sPiv[c];
+    bv = -1.0;
+    bi = 0x7fffffff;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int r = tid + T * s;
+      if (r < rows && r0 + r > j) {
+        double xj = x[s][0];
+#pragma unroll
+        for (int c = 1; c < W; ++c) xj = c == j ? x[s][c] : xj;
+        const double l = piv != 0.0 ? xj / piv : xj;
+        double xn = 0.0;
+        // branch-free per column (selects, not W reconvergence regions)
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+          const double nv = fma(-l, pv[c], x[s][c]);
+          x[s][c] = c == j ? l : ((c > j && c < w) ? nv : x[s][c]);
+          xn = c == j + 1 ? x[s][c] : xn;
+        }
+        if (j + 1 < w && fabs(xn) > bv) {
+          bv = fabs(xn);
+          bi = r0 + r;
+        }
+      }
+    }
+    GPROBE(5);
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int r = tid + T * s;
+#pragma unroll
+    for (int c = 0; c < W; ++c)
+      if (r < rows && c < w) a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld] = x[s][c];
+  }
+  cl.sync();  // no CTA leaves while another may still read its published slots
+  GPROBE(7);
+#ifdef RELAPACK_GETF2_PROBE
+  if (threadIdx.x == 0 && cl.block_rank() == 0)
+    for (int k = 0; k < 8; ++k) g_gprobe[k] = pacc[k];
+#endif
+}
+
+// One panel's interchanges as a permutation.  Warp 0 composes the
+// transpositions (row k <-> p_k, k ascending, p_k >= k) on the affected rows:
+// lane l tracks row l < npiv (cont_lo: the row whose value ends there) and
+// extra slot l a pivot row >= npiv; then every warp moves whole columns.
+__global__ void __launch_bounds__(256) k_permute(XPermArgs a) {
+  if (ld_info(a.d_info) != 0) return;
+  __shared__ int s_row[2 * kGetf2Max], s_src[2 * kGetf2Max];
+  __shared__ int s_cnt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    int cont_lo = lane, xrow = -1, xcont = -1, ne = 0;
+    const int mypiv = lane < a.npiv ? a.ipiv[a.k0 + lane] - a.base : lane;  // all pivots in one load
+    for (int k = 0; k < a.npiv; ++k) {
+      const int p = __shfl_sync(0xffffffffu, mypiv, k);
+      if (p == k) continue;
+      const int ck = __shfl_sync(0xffffffffu, cont_lo, k);
+      if (p < a.npiv) {
+        const int cp = __shfl_sync(0xffffffffu, cont_lo, p);
+        if (lane == k) cont_lo = cp;
+        if (lane == p) cont_lo = ck;
+      } else {
+        const unsigned mk = __ballot_sync(0xffffffffu, xrow == p);
+        int slot;
+        if (mk) {
+          slot = __ffs(mk) - 1;
+        } else {
+          slot = ne++;
+          if (lane == slot) {
+            xrow = p;
+            xcont = p;
+          }
+        }
+        const int cp = __shfl_sync(0xffffffffu, xcont, slot);
+        if (lane == k) cont_lo = cp;
+        if (lane == slot) xcont = ck;
+      }
+    }
+    // the moved rows, compacted
+    const bool mv_lo = lane < a.npiv && cont_lo != lane, mv_x = xrow >= 0 && xcont != xrow;
+    const unsigned b_lo = __ballot_sync(0xffffffffu, mv_lo), b_x = __ballot_sync(0xffffffffu, mv_x);
+    const int n_lo = __popc(b_lo);
+    if (mv_lo) {
+      const int at = __popc(b_lo & ((1u << lane) - 1));
+      s_row[at] = lane;
+      s_src[at] = cont_lo;
+    }
+    if (mv_x) {
+      const int at = n_lo + __popc(b_x & ((1u << lane) - 1));
+      s_row[at] = xrow;
+      s_src[at] = xcont;
+    }
+    if (lane == 0) s_cnt = n_lo + __popc(b_x);
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  if (cnt == 0) return;
+  const int r0 = lane < cnt ? s_row[lane] : 0, q0 = lane < cnt ? s_src[lane] : 0;
+  const int r1 = lane + 32 < cnt ? s_row[lane + 32] : 0, q1 = lane + 32 < cnt ? s_src[lane + 32] : 0;
+  const int wpb = blockDim.x >> 5;
+  for (int col = blockIdx.x * wpb + warp; col < a.ncols; col += gridDim.x * wpb) {
+    double* c = a.A + (int64_t)col * a.ld;
+    const double v0 = lane < cnt ? c[q0] : 0.0, v1 = lane + 32 < cnt ? c[q1] : 0.0;
+    __syncwarp();
+    if (lane < cnt) c[r0] = v0;
+    if (lane + 32 < cnt) c[r1] = v1;
+  }
+}
+
 // Row interchanges: for k = k0 .. k1-1 (in order) swap rows k and ipiv[k] - base
 // of the columns [0, ncols) of A (layout 0).  One thread per column.
 __global__ void k_laswp(XLaswpArgs a) {
@@ -521,6 +815,77 @@ cudaError_t launch_getf2(const XGetf2Args& a, int grid, cudaStream_t st) {
 cudaError_t launch_laswp(const XLaswpArgs& a, cudaStream_t st) {
   if (a.ncols <= 0 || a.k1 <= a.k0) return cudaSuccess;
   k_laswp<<<(a.ncols + 127) / 128, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// (threads, rows per thread, width) of the register panel for a CTA row count
+template <class F>
+cudaError_t getf2_clr_dispatch(int rows_per_cta, F&& f) {
+  if (rows_per_cta <= kGetf2ClRows32) return f(k_getf2_clr<256, 2, 32>, 256);
+  if (rows_per_cta <= kGetf2ClRows16) return f(k_getf2_clr<512, 2, 16>, 512);
+  if (rows_per_cta <= kGetf2ClRows8) return f(k_getf2_clr<512, 4, 8>, 512);
+  return cudaErrorInvalidValue;
+}
+
+int getf2_cluster_caps() {
+  static int csz[kMaxDevices] = {}, done[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return 0;
+  if (!done[dev]) {
+    done[dev] = 1;
+    // opt-in (RELAPACK_GETF2_CLUSTER=16|8): measured slower end to end than the
+    // cooperative grid kernel at n = 16384 (225 vs 208 ms, tools/experiments r3q)
+    const char* v = getenv("RELAPACK_GETF2_CLUSTER");
+    const int want = v ? atoi(v) : 0;
+    for (auto k : {k_getf2_clr<256, 2, 32>, k_getf2_clr<512, 2, 16>, k_getf2_clr<512, 4, 8>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c : {16, 8}) {
+      if (c > want) continue;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(512);
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = c;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, k_getf2_clr<512, 2, 16>, &cfg) == cudaSuccess && nc > 0) {
+        csz[dev] = c;
+        break;
+      }
+      cudaGetLastError();
+    }
+  }
+  return csz[dev];
+}
+
+cudaError_t launch_getf2_cl(const XGetf2ClArgs& a, int csize, cudaStream_t st) {
+  if (a.m <= 0 || a.w <= 0) return cudaSuccess;
+  return getf2_clr_dispatch(a.rows_per_cta, [&](auto kern, int threads) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+  });
+}
+
+cudaError_t launch_permute(const XPermArgs& a, cudaStream_t st) {
+  if (a.ncols <= 0 || a.npiv <= 0) return cudaSuccess;
+  int grid = (a.ncols + 7) / 8;
+  if (grid > 148 * 8) grid = 148 * 8;
+  k_permute<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,8 @@ constexpr int kTriMax = 64;        // widest triangular block of k_tri_rows / k_
 constexpr int kGetf2Max = 32;      // widest getrf panel of k_getf2
 constexpr int kGetf2Threads = 256;
 constexpr int kGetf2RowThreads = 128;  // threads on the panel rows; the rest swap rows outside the panel
+// register panels of k_getf2_clr: rows per CTA for panel widths 32 / 16 / 8
+constexpr int kGetf2ClRows32 = 512, kGetf2ClRows16 = 1024, kGetf2ClRows8 = 2048;
 
 enum XTriMode : int {
   kTriSolveLT = 0,  // x := alpha x T^{-T}   (x T^T = alpha b, forward)
@@ -56,6 +58,34 @@ struct XGetf2Args {
   const int* d_info;
 };
 
+// Cluster panel (k_getf2_clr): the same LU with partial pivoting of an m x w
+// panel held by ONE thread-block cluster (C CTAs, rows split evenly), the
+// per-column exchange through distributed shared memory and the hardware
+// cluster barrier; interchanges outside the panel are left to k_permute.
+struct XGetf2ClArgs {
+  double* P;  // m x w panel, layout 0
+  int64_t ld;
+  int m, w, rows_per_cta;
+  int* ipiv;
+  int pivot_base;
+  int* getrf_info;
+  int info_base;
+  const int* d_info;
+};
+
+// Row interchanges of one panel (pivots ipiv[k0 .. k0 + npiv), panel-relative
+// row = ipiv - base) applied as one permutation to columns [0, ncols) of A
+// (A = element (panel row 0, first column), layout 0): a warp per column
+// gathers the at most 2 npiv affected rows and scatters them permuted.
+struct XPermArgs {
+  double* A;
+  int64_t ld;
+  int ncols;
+  const int* ipiv;
+  int k0, npiv, base;
+  const int* d_info;
+};
+
 struct XLaswpArgs {
   double* A;      // columns [0, ncols) of the matrix, layout 0
   int64_t ld;
@@ -72,6 +102,11 @@ cudaError_t launch_diag_check(const double* A, int64_t ld, int layout, int n, in
 size_t getf2_smem(int rows_per_cta);
 cudaError_t launch_getf2(const XGetf2Args& a, int grid, cudaStream_t st);
 cudaError_t launch_laswp(const XLaswpArgs& a, cudaStream_t st);
+// cluster size C (16 or 8; 0: no cluster can be scheduled); configures the
+// cluster panel kernels once per device
+int getf2_cluster_caps();
+cudaError_t launch_getf2_cl(const XGetf2ClArgs& a, int csize, cudaStream_t st);
+cudaError_t launch_permute(const XPermArgs& a, cudaStream_t st);
 cudaError_t configure_xkernels();
 
 }  // namespace relapack

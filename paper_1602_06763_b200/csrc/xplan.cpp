@@ -159,30 +159,59 @@ void xplan_potrs(std::vector<XOp>& ops, const XParams& p, int n, int nrhs) {
   xplan_tri(ops, p, kTriSolveL, L, Bt, nrhs, n, 1.0, 0, 1);   // L^T X = Y  <=> X^T L = Y^T
 }
 
+// Panel width of a getrf leaf with m rows on a cluster: the configured width,
+// narrowed to what the register panels hold (rows per CTA: <= 512 at 32
+// columns, <= 1024 at 16, <= 2048 at 8); 0: the cooperative grid kernel.
+static int cluster_leaf_width(const XParams& p, int m) {
+  if (p.getf2_cluster <= 0) return 0;
+  const int rows = (m + p.getf2_cluster - 1) / p.getf2_cluster;
+  const int cap = rows <= kGetf2ClRows32 ? 32 : rows <= kGetf2ClRows16 ? 16 : rows <= kGetf2ClRows8 ? 8 : 0;
+  return std::min(cap, p.getrf_base);
+}
+
 void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, int n, int level) {
   if (m <= 0 || n <= 0) return;
   const int mn = std::min(m, n);
-  if (n <= p.getrf_base) {
+  const int wcl = cluster_leaf_width(p, m);
+  const int base = wcl > 0 ? wcl : p.getrf_base;
+  if (n <= base) {
     XOp o;
     o.kind = XK_GETF2;
     o.level = level;
     o.c = XView{0, r0, c0, 0};
     o.m = m;
     o.n = n;
+    o.mode = wcl > 0 ? 1 : 0;  // 1: cluster panel (panel columns only)
     o.info_base = c0;
     o.flops = (double)m * n * n - (double)n * n * n / 3.0;
     ops.push_back(o);
+    if (o.mode == 1) {
+      // the panel's interchanges in the other columns: the right part first
+      // (its solve and update read those rows), the left part off the path
+      const int npiv = std::min(m, n);
+      for (int side = 0; side < 2; ++side) {
+        XOp q;
+        q.kind = XK_PERM;
+        q.level = level;
+        q.c = side == 0 ? XView{0, r0, c0 + n, 0} : XView{0, r0, 0, 0};
+        q.n = side == 0 ? p.getrf_cols - (c0 + n) : c0;
+        q.m = npiv;
+        q.k = c0;
+        if (q.n > 0) ops.push_back(q);
+      }
+    }
     return;
   }
   // split the columns at n1; getrf(left panel) -> P1; laswp P1 on
   // the right panel; A12 := L11^{-1} A12 (unit); A22 -= A21 A12; getrf(A22)
   // -> P2; laswp P2 on the left panel's lower rows.
-  // The interchanges of a panel are applied by the panel kernel itself to every
-  // column of the matrix (k_getf2 step e'), which is what the two laswp calls
-  // of the recursion do (P1 on the right part before its solve and update, P2
-  // on the left part's lower rows after the right recursion): nothing reads
-  // those rows of the other columns in between, so the order does not matter.
-  const int n1 = mn <= p.getrf_base ? mn : xsplit(mn, p.getrf_base);
+  // The interchanges of a panel are applied to every other column of the
+  // matrix right after the panel (k_permute; the cooperative kernel k_getf2
+  // does it itself), which is what the two laswp calls of the recursion do (P1
+  // on the right part before its solve and update, P2 on the left part's
+  // lower rows after the right recursion): nothing reads those rows of the
+  // other columns in between, so the order does not matter.
+  const int n1 = mn <= base ? mn : xsplit(mn, base);
   xplan_getrf(ops, p, r0, c0, m, n1, level + 1);
   const XView L11{0, r0, c0, 0}, A12{0, r0, c0 + n1, 0}, A21{0, r0 + n1, c0, 0}, A22{0, r0 + n1, c0 + n1, 0};
   xplan_tri(ops, p, kTriSolveLT, L11, tr(A12), n - n1, n1, 1.0, 1, level + 1);
@@ -226,9 +255,14 @@ void footprint(const XOp& o, int total_rows, XRect* w, XRect* r) {
     case XK_POTF2:
       w[0] = rect(o.c, o.n, o.n);
       break;
-    case XK_GETF2:  // the panel, and its interchanges in every other column: rows [r0, m) of the matrix
-      w[0] = XRect{o.c.buf, o.c.r0, total_rows, 0, 1 << 30};
-      w[1] = XRect{2, 0, 1, o.c.r0, o.c.r0 + std::min(o.m, o.n)};  // its pivots
+    case XK_GETF2:  // the panel (mode 1) or also its interchanges in every other column: rows [r0, m) of the matrix
+      w[0] = o.mode == 1 ? XRect{o.c.buf, o.c.r0, total_rows, o.c.c0, o.c.c0 + o.n}
+                         : XRect{o.c.buf, o.c.r0, total_rows, 0, 1 << 30};
+      w[1] = XRect{2, 0, 1, o.c.c0, o.c.c0 + std::min(o.m, o.n)};  // its pivots
+      break;
+    case XK_PERM:
+      w[0] = XRect{o.c.buf, o.c.r0, total_rows, o.c.c0, o.c.c0 + o.n};
+      r[0] = XRect{2, 0, 1, o.k, o.k + o.m};
       break;
     case XK_LASWP:
       // interchanges rows >= m among the columns; reads the pivots [m, k)

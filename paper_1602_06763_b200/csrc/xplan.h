@@ -31,7 +31,8 @@ enum XKind : int {
   XK_POTF2 = 4,  // Cholesky of the n x n block (n <= 128)                        [potf2.cu]
   XK_GETF2 = 5,  // LU with partial pivoting of the m x n panel at c (n <= 32)    [k_getf2]
   XK_LASWP = 6,  // row interchanges ipiv[m .. k) on columns [c.c0, c.c0 + n)      [k_laswp]
-  XK_CHECK = 7   // info := first zero diagonal of the n x n L-view (trtri)      [k_diag_check]
+  XK_CHECK = 7,  // info := first zero diagonal of the n x n L-view (trtri)      [k_diag_check]
+  XK_PERM = 8    // pivots [k, k + m) of the panel at row c.r0 applied to columns [c.c0, c.c0 + n) [k_permute]
 };
 
 struct XOp {
@@ -52,6 +53,10 @@ struct XParams {
   int split_tile = 64;  // n1 = T floor(n / 2T)
   int getrf_base = 32;  // panel width of the getrf leaves
   int potrf_base = 128; // Cholesky leaves (blocked dpotrf's diagonal blocks)
+  // getrf panels on one thread-block cluster (k_getf2_clr): cluster size (0:
+  // the cooperative grid kernel k_getf2)
+  int getf2_cluster = 0;
+  int getrf_cols = 0;   // columns of the whole matrix (the interchanges' extent)
 };
 
 // Recursive TRSM / TRMM on rows: B(m x k) := op(B, T) with T (k x k) lower,

@@ -189,7 +189,7 @@ def apply_ipiv(A, ipiv):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 5), (32, 32), (33, 33), (100, 100), (300, 300), (1031, 1031),
-                                 (2048, 2048), (1500, 700), (700, 1500), (4096, 64)])
+                                 (2048, 2048), (1500, 700), (700, 1500), (4096, 64), (16384, 48)])
 def test_getrf(m, n):
     A = np.asfortranarray(np.random.default_rng(m * 7 + n).uniform(-1, 1, size=(m, n)))
     dA = to_dev(A)
@@ -226,6 +226,27 @@ def test_getrf_singular_and_identity():
     assert rl.dgetrf(dI, ip) == 0
     assert torch.equal(dI.cpu(), torch.eye(77, dtype=torch.float64))
     assert ip.cpu().tolist() == list(range(1, 78))
+
+
+@pytest.mark.parametrize("cluster", ["16", "8"])
+def test_getrf_panel_variants(cluster):
+    """The getrf panels on one thread-block cluster of 16 / 8 CTAs (opt-in
+    RELAPACK_GETF2_CLUSTER; narrower leaves for tall panels, interchanges by
+    k_permute) — the knob is read once per process, so each variant runs in a
+    subprocess."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = ("from tests.test_gpu_next import test_getrf, test_getrf_singular_and_identity\n"
+            "for mn in [(33, 33), (300, 300), (1031, 1031), (1500, 700), (700, 1500), (4096, 64), (16384, 48)]:\n"
+            "    test_getrf(*mn)\n"
+            "test_getrf_singular_and_identity()\nprint('variant ok')\n")
+    env = dict(os.environ, RELAPACK_GETF2_CLUSTER=cluster)
+    r = subprocess.run([sys.executable, "-c", code], cwd=Path(__file__).resolve().parents[1], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
 # ------------------------------------------------------------------ N2 blocked dpotrf
