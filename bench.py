@@ -422,6 +422,20 @@ def _in_graph_update_rate(rl, W, P, d_info, uplo, st, dev, upd_fl):
                     "graph (%globaltimer, RELAPACK_TRACE=1 replay of the same plan)"}
 
 
+def _committed_batch_traffic(count):
+    """DRAM bytes per CFG[4] step (the four class kernels) from the committed ncu capture, or None."""
+    import glob
+
+    if count != 131072:
+        return None
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                          "ncu_dram_batch_*.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        return int(json.load(f)["total_bytes"])
+
+
 def _committed_traffic(n):
     """DRAM bytes per k_update launch from the committed ncu capture of this
     workload (profiles/ncu_update_traffic_n<n>_*.json), or (None, why)."""
@@ -579,8 +593,10 @@ def run_batch(args, rank, world, dev):
         "config": {"workload": f"batched dpotrf, {count} matrices n~U{{16,32,48,64}} (BASELINE.json configs[4])",
                    "count": count, "l2": "2 GB batch > 126 MB L2; restored from a pristine copy between steps"},
         "roofline": {"kernel": "k_potf2_batched", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
-                     "note": "algorithmic bytes = lower triangles read + written once (8 n(n+1) per matrix)"},
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": _committed_batch_traffic(count),
+                     "note": "algorithmic bytes = lower triangles read + written once (8 n(n+1) per matrix); traffic = "
+                             "DRAM bytes of the four class kernels per step from the committed ncu capture "
+                             "(profiles/ncu_dram_batch_*.json)"},
         "gb_per_s": round(tot_bytes / (ms_max / 1e3) / 1e9, 1),
         "gpu_launches": 5 * args.steps, "step_times_ms": [round(t, 4) for t in times], "clocks": clk.summary(),
         "e2e": ({"value": round(tot_flops / (e2e_ms / 1e3) / 1e9, 2), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
