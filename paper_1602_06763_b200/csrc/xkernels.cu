@@ -24,6 +24,7 @@
 
 #include <cstdlib>
 
+#include "chol_regs.cuh"
 #include "common.cuh"
 #include "kernels.h"
 #include "xkernels.h"
@@ -175,6 +176,148 @@ __global__ void __launch_bounds__(kTriRows) k_tri_rows(XTriArgs a) {
     if (a.lb == 0) { rr = e % rows; c = e / rows; } else { c = e % t; rr = e / t; }
     a.B[lv_off(a.lb, row0 + rr, c, a.ldb)] = sB[rr * (W + 1) + c];
   }
+}
+
+// ---- DMMA form of the triangular-rows leaf (the same four operations)
+// A warp owns 8 rows of B, all t <= 64 columns in registers as eight 8 x 8
+// DMMA accumulator tiles (lane (g, q4) holds x(g, 8J + 2 q4 + e)); T sits in
+// shared memory as a dense 64 x 64 lower block (zero above the diagonal, 1 on
+// a unit diagonal, identity beyond t).  With 8-column blocks J:
+//   MulL   x := alpha x T      out_J = sum_{K >= J} x_K T_KJ         (DMMA)
+//   MulLT  x := alpha x T^T    out_J = sum_{K <= J} x_K T_JK^T       (DMMA)
+//   SolveLT x T^T = b (fwd)    per J ascending: the in-block substitution
+//                              (quad shuffles, x_c = y_c * (1 / T_cc)), then
+//                              y_J' -= x_J T_J'J^T for J' > J        (DMMA)
+//   SolveL  x T = b (bwd)      per J descending: in-block substitution, then
+//                              y_J' -= x_J T_JJ' for J' < J          (DMMA)
+// (the factorization's register TRSM applied to the other operations: the
+// row-per-thread kernel above runs one dependent FMA chain per row).
+constexpr int kTriMmaWarps = 8;
+constexpr int kTriMmaRows = 8 * kTriMmaWarps;
+constexpr int kTriMmaLd = kTriMax + 4;  // column stride: fragment reads at most 2-way conflicted
+
+template <int MODE, int UNIT>
+__global__ void __launch_bounds__(32 * kTriMmaWarps) k_tri_mma(XTriArgs a) {
+  if (ld_info(a.d_info) != 0) return;
+  constexpr int W = kTriMax, LD = kTriMmaLd, NB = W / 8;
+  extern __shared__ double sm[];
+  double* sT = sm;              // T(i, j) at sT[i + j * LD]
+  double* sR = sm + W * LD;     // 1 / T(i, i)
+  const int t = a.t;
+  for (int e = threadIdx.x; e < W * LD; e += blockDim.x) {
+    const int i = e % LD, j = e / LD;
+    sT[e] = (i == j && (UNIT || j >= t)) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  stage_in<8>(sT, a.T, t * t, [&](int e, int64_t& so, int& dof) {
+    int i, j;
+    if (a.lt == 0) { i = e % t; j = e / t; } else { j = e % t; i = e / t; }
+    so = lv_off(a.lt, i, j, a.ldt);
+    dof = i + j * LD;
+    return i > j || (i == j && !UNIT);
+  });
+  __syncthreads();
+  if (MODE == kTriSolveLT || MODE == kTriSolveL)
+    for (int i = threadIdx.x; i < W; i += blockDim.x) sR[i] = 1.0 / sT[i + i * LD];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q4 = lane & 3;
+  const int row = blockIdx.x * kTriMmaRows + 8 * warp + g;
+  if (blockIdx.x * kTriMmaRows + 8 * warp >= a.m) return;  // whole warp past the end
+  const bool rok = row < a.m;
+  double v[NB][2];
+#pragma unroll
+  for (int J = 0; J < NB; ++J)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 8 * J + 2 * q4 + e;
+      v[J][e] = (rok && c < t) ? a.B[lv_off(a.lb, row, c, a.ldb)] : 0.0;
+    }
+  const int nb = (t + 7) / 8;  // blocks holding columns < t (the rest stay 0)
+  if (MODE == kTriMulL || MODE == kTriMulLT) {
+    double fr[NB][2];
+#pragma unroll
+    for (int K = 0; K < NB; ++K) {
+      fr[K][0] = tile_frag(v[K][0], v[K][1], 0, g, q4);
+      fr[K][1] = tile_frag(v[K][0], v[K][1], 1, g, q4);
+    }
+#pragma unroll
+    for (int J = 0; J < NB; ++J) {
+      if (J >= nb) break;
+      double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int K = 0; K < NB; ++K) {
+        if (MODE == kTriMulL ? (K < J || K >= nb) : K > J) continue;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          // B(kk, n): (T_KJ)(4ks + kk, n) for MulL, (T_JK^T)(4ks + kk, n) = T(8J + n, 8K + 4ks + kk) for MulLT
+          const double b = MODE == kTriMulL ? sT[(8 * K + 4 * ks + q4) + (8 * J + g) * LD]
+                                            : sT[(8 * J + g) + (8 * K + 4 * ks + q4) * LD];
+          dmma_884(o0, o1, fr[K][ks], b);
+        }
+      }
+      v[J][0] = a.alpha * o0;
+      v[J][1] = a.alpha * o1;
+    }
+  } else {
+    constexpr bool kFwd = MODE == kTriSolveLT;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int J = kFwd ? i : NB - 1 - i;
+      if (J >= nb) continue;
+      // in-block substitution: column c of block J final at its owner lane
+      // (q4 == c / 2), broadcast in the quad, applied to the lane's columns
+      // still to come (c2 = 2 q4 + e after c in the sweep order)
+      double tc[8][2];  // T(8J + c2, 8J + c) (fwd: T^T(c, c2)) or T(8J + c, 8J + c2) (bwd)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c2 = 2 * q4 + e;
+          tc[c][e] = kFwd ? sT[(8 * J + c2) + (8 * J + c) * LD] : sT[(8 * J + c) + (8 * J + c2) * LD];
+        }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int c = kFwd ? s : 7 - s;
+        const int co = c >> 1, ce = c & 1;
+        double own = ce ? v[J][1] : v[J][0];
+        if (!UNIT) own *= sR[8 * J + c];
+        if (q4 == co) {
+          if (ce)
+            v[J][1] = own;
+          else
+            v[J][0] = own;
+        }
+        const double xc = __shfl_sync(0xffffffffu, own, (lane & ~3) | co);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c2 = 2 * q4 + e;
+          const double nv = fma(-xc, tc[c][e], v[J][e]);
+          v[J][e] = (kFwd ? c2 > c : c2 < c) ? nv : v[J][e];
+        }
+      }
+      // the other blocks still to solve: y_J' -= x_J * (T_J'J^T | T_JJ')
+      double fr0 = tile_frag(v[J][0], v[J][1], 0, g, q4), fr1 = tile_frag(v[J][0], v[J][1], 1, g, q4);
+#pragma unroll
+      for (int i2 = i + 1; i2 < NB; ++i2) {
+        const int J2 = kFwd ? i2 : NB - 1 - i2;
+        if (J2 >= nb) continue;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          // fwd: B(kk, n) = T^T(8J + 4ks + kk, 8J2 + n) = T(8J2 + n, 8J + 4ks + kk); bwd: T(8J + 4ks + kk, 8J2 + n)
+          const double b = kFwd ? sT[(8 * J2 + g) + (8 * J + 4 * ks + q4) * LD]
+                                : sT[(8 * J + 4 * ks + q4) + (8 * J2 + g) * LD];
+          dmma_884(v[J2][0], v[J2][1], -(ks ? fr1 : fr0), b);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int J = 0; J < NB; ++J)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 8 * J + 2 * q4 + e;
+      if (rok && c < t) a.B[lv_off(a.lb, row, c, a.ldb)] = v[J][e];
+    }
 }
 
 // Inverse of the t x t lower-triangular block in place.  Column j of X = T^{-1}
@@ -763,9 +906,42 @@ cudaError_t configure_tri_mode() {
   return cudaFuncSetAttribute(k_tri_rows<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
 }
 
+constexpr size_t kTriMmaSmem = sizeof(double) * ((size_t)kTriMax * kTriMmaLd + kTriMax);
+
+template <int MODE, int UNIT>
+cudaError_t launch_tri_mma(const XTriArgs& a, cudaStream_t st) {
+  k_tri_mma<MODE, UNIT><<<(a.m + kTriMmaRows - 1) / kTriMmaRows, 32 * kTriMmaWarps, kTriMmaSmem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t configure_tri_mma() {
+  cudaError_t e = cudaFuncSetAttribute(k_tri_mma<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriMmaSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_tri_mma<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriMmaSmem);
+}
+
+// RELAPACK_TRI_MMA=0: the row-per-thread kernel instead of the DMMA one
+static bool tri_mma() {
+  static const bool v = [] {
+    const char* e = getenv("RELAPACK_TRI_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 cudaError_t launch_tri_rows(const XTriArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.t <= 0) return cudaSuccess;
   if (a.t > kTriMax) return cudaErrorInvalidValue;
+  if (tri_mma()) {
+    const bool u = a.unit != 0;
+    switch (a.mode) {
+      case kTriSolveLT: return u ? launch_tri_mma<kTriSolveLT, 1>(a, st) : launch_tri_mma<kTriSolveLT, 0>(a, st);
+      case kTriSolveL: return u ? launch_tri_mma<kTriSolveL, 1>(a, st) : launch_tri_mma<kTriSolveL, 0>(a, st);
+      case kTriMulL: return u ? launch_tri_mma<kTriMulL, 1>(a, st) : launch_tri_mma<kTriMulL, 0>(a, st);
+      default: return u ? launch_tri_mma<kTriMulLT, 1>(a, st) : launch_tri_mma<kTriMulLT, 0>(a, st);
+    }
+  }
   switch (a.mode) {
     case kTriSolveLT: return launch_tri_mode<kTriSolveLT>(a, st);
     case kTriSolveL: return launch_tri_mode<kTriSolveL>(a, st);
@@ -895,6 +1071,10 @@ cudaError_t configure_xkernels() {
   if ((e = configure_tri_mode<kTriSolveL>()) != cudaSuccess) return e;
   if ((e = configure_tri_mode<kTriMulL>()) != cudaSuccess) return e;
   if ((e = configure_tri_mode<kTriMulLT>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mma<kTriSolveLT>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mma<kTriSolveL>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mma<kTriMulL>()) != cudaSuccess) return e;
+  if ((e = configure_tri_mma<kTriMulLT>()) != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_trti2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(2 * sizeof(double) * kTriMax * kTriLd));
   if (e != cudaSuccess) return e;

@@ -249,6 +249,29 @@ def test_getrf_panel_variants(cluster):
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
+def test_tri_leaf_row_kernel_variant():
+    """The triangular leaves on the row-per-thread kernel (RELAPACK_TRI_MMA=0)
+    instead of the DMMA one: the same parity checks of every operation that
+    uses them (trtri L/U and unit, lauum, potri, potrs, getrf), in a subprocess
+    (the knob is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = ("import tests.test_gpu_next as t\n"
+            "for n in (65, 300, 1031):\n"
+            "    for u in 'LU':\n"
+            "        t.test_trtri(n, u); t.test_lauum(n, u)\n"
+            "t.test_trtri_unit_and_integer('L'); t.test_trtri_unit_and_integer('U')\n"
+            "t.test_getrf(300, 300); t.test_getrf(1500, 700)\n"
+            "print('variant ok')\n")
+    env = dict(os.environ, RELAPACK_TRI_MMA="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=Path(__file__).resolve().parents[1], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 # ------------------------------------------------------------------ N2 blocked dpotrf
 @pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("nb", [64, 128, 256])
