@@ -196,7 +196,12 @@ constexpr int kTriMmaWarps = 8;
 constexpr int kTriMmaRows = 8 * kTriMmaWarps;
 constexpr int kTriMmaLd = kTriMax + 4;  // column stride: fragment reads at most 2-way conflicted
 
-template <int MODE, int UNIT>
+// BSRC 1 (trti2): B is the identity and the result X^T = T^{-T} (i.e. X =
+// T^{-1}, lower) is written over T's strictly lower part (and its diagonal
+// unless unit): T X = I solved as rows of X^T T^T = I.
+// BSRC 2 (lauu2): B is the transposed view of T (row r = column r of L, only
+// its entries c >= r read), MulL gives L^T L, stored as its lower part.
+template <int MODE, int UNIT, int BSRC = 0>
 __global__ void __launch_bounds__(32 * kTriMmaWarps) k_tri_mma(XTriArgs a) {
   if (ld_info(a.d_info) != 0) return;
   constexpr int W = kTriMax, LD = kTriMmaLd, NB = W / 8;
@@ -230,7 +235,10 @@ __global__ void __launch_bounds__(32 * kTriMmaWarps) k_tri_mma(XTriArgs a) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int c = 8 * J + 2 * q4 + e;
-      v[J][e] = (rok && c < t) ? a.B[lv_off(a.lb, row, c, a.ldb)] : 0.0;
+      if (BSRC == 1)
+        v[J][e] = (rok && c < t && c == row) ? 1.0 : 0.0;
+      else
+        v[J][e] = (rok && c < t && (BSRC == 0 || c >= row)) ? a.B[lv_off(a.lb, row, c, a.ldb)] : 0.0;
     }
   const int nb = (t + 7) / 8;  // blocks holding columns < t (the rest stay 0)
   if (MODE == kTriMulL || MODE == kTriMulLT) {
@@ -316,7 +324,8 @@ __global__ void __launch_bounds__(32 * kTriMmaWarps) k_tri_mma(XTriArgs a) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int c = 8 * J + 2 * q4 + e;
-      if (rok && c < t) a.B[lv_off(a.lb, row, c, a.ldb)] = v[J][e];
+      const bool keep = BSRC == 0 || c > row || (c == row && !UNIT);  // X(c, row) / C(c, row): lower part only
+      if (rok && c < t && keep) a.B[lv_off(a.lb, row, c, a.ldb)] = v[J][e];
     }
 }
 
@@ -953,6 +962,16 @@ cudaError_t launch_tri_rows(const XTriArgs& a, cudaStream_t st) {
 cudaError_t launch_trti2(const XBlockArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
   if (a.n > kTriMax) return cudaErrorInvalidValue;
+  if (tri_mma()) {
+    // T^{-1} as the rows of X^T T^T = I (the DMMA triangular kernel on the
+    // identity), written back through the transposed view of T's storage
+    XTriArgs t{a.A, a.ld, a.layout, a.A, a.ld, a.layout ^ 1, a.n, a.n, kTriSolveLT, a.unit, 1.0, a.d_info};
+    if (a.unit)
+      k_tri_mma<kTriSolveLT, 1, 1><<<1, 32 * kTriMmaWarps, kTriMmaSmem, st>>>(t);
+    else
+      k_tri_mma<kTriSolveLT, 0, 1><<<1, 32 * kTriMmaWarps, kTriMmaSmem, st>>>(t);
+    return cudaGetLastError();
+  }
   k_trti2<<<1, kTriMax, 2 * sizeof(double) * kTriMax * kTriLd, st>>>(a);
   return cudaGetLastError();
 }
@@ -960,6 +979,12 @@ cudaError_t launch_trti2(const XBlockArgs& a, cudaStream_t st) {
 cudaError_t launch_lauu2(const XBlockArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
   if (a.n > kTriMax) return cudaErrorInvalidValue;
+  if (tri_mma()) {
+    // L^T L = (rows of L^T) times L: MulL on the transposed view of the block
+    XTriArgs t{a.A, a.ld, a.layout, a.A, a.ld, a.layout ^ 1, a.n, a.n, kTriMulL, 0, 1.0, a.d_info};
+    k_tri_mma<kTriMulL, 0, 2><<<1, 32 * kTriMmaWarps, kTriMmaSmem, st>>>(t);
+    return cudaGetLastError();
+  }
   k_lauu2<<<1, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
@@ -1075,6 +1100,9 @@ cudaError_t configure_xkernels() {
   if ((e = configure_tri_mma<kTriSolveL>()) != cudaSuccess) return e;
   if ((e = configure_tri_mma<kTriMulL>()) != cudaSuccess) return e;
   if ((e = configure_tri_mma<kTriMulLT>()) != cudaSuccess) return e;
+  for (auto k : {k_tri_mma<kTriSolveLT, 0, 1>, k_tri_mma<kTriSolveLT, 1, 1>, k_tri_mma<kTriMulL, 0, 2>})
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriMmaSmem)) != cudaSuccess)
+      return e;
   e = cudaFuncSetAttribute(k_trti2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(2 * sizeof(double) * kTriMax * kTriLd));
   if (e != cudaSuccess) return e;
