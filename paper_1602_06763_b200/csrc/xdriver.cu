@@ -61,13 +61,15 @@ struct XExec {
   size_t nbars = 0;
   double* cand = nullptr;  // per getf2 slot: 2G vals, 2G*kGetf2Max rows, 2*kGetf2Max diag rows
   int* cand_idx = nullptr;
+  void* poll_ws = nullptr;  // epoch-stamped exchange records (shared by the panels)
   int sms = 148;
   int cl_size = 0;  // getrf cluster panels: CTAs per cluster
   bool is_getrf = false, has_check = false;
   cudaGraphExec_t exec = nullptr;
   ~XExec() {
     if (exec) cudaGraphExecDestroy(exec);
-    for (void* p : {(void*)d_info, (void*)splitk_ws, (void*)splitk_cnt, (void*)bars, (void*)cand, (void*)cand_idx})
+    for (void* p : {(void*)d_info, (void*)splitk_ws, (void*)splitk_cnt, (void*)bars, (void*)cand, (void*)cand_idx,
+                    poll_ws})
       if (p) cudaFree(p);
   }
 };
@@ -90,9 +92,27 @@ int getf2_grid(int m, int sms) {
   return std::max(1, std::min(g, sms));
 }
 
+// Epoch-stamped panel exchange (RELAPACK_GETF2_POLL=1, opt-in): no grid
+// barrier, every CTA polls the others' 16-byte records.  Measured alone
+// (tools/experiments r4d): faster with few CTAs (G = 2: 104 vs 122 us per
+// 32-column panel) but the G x G polling contends at G >= 128 (205 vs 149 us);
+// getrf n = 16384 225 vs 195 ms.
+bool getf2_poll() {
+  static const bool v = [] {
+    const char* e = getenv("RELAPACK_GETF2_POLL");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+// one workspace for all panels of a plan (they run one after another):
+// records for up to 160 CTAs
+constexpr size_t kPollRecBytes = 2 * 160 * 16, kPollRowBytes = 2 * 160 * kGetf2Max * 16,
+                 kPollDiagBytes = 2 * kGetf2Max * 16;
+
 __global__ void k_xprologue(int* d_info, int check) {
   if (!check) d_info[0] = 0;
   d_info[1] = kIntMax;
+  d_info[2] += 1;  // replay counter: the panels' exchange epochs are unique per replay
 }
 
 __global__ void k_xepilogue(int* d_info) {
@@ -157,6 +177,14 @@ cudaError_t launch_xop(const XExec& x, size_t i, cudaStream_t st) {
       a.ncols = b.total_cols;
       a.c0 = o.c.c0;
       a.d_info = x.d_info;
+      if (getf2_poll()) {
+        a.poll = 1;
+        a.epoch_base = (unsigned)(x.slot[i] & 1023) << 6;
+        a.replay = reinterpret_cast<const unsigned*>(x.d_info + 2);
+        a.prec = x.poll_ws;
+        a.prow = static_cast<char*>(x.poll_ws) + kPollRecBytes;
+        a.pdiag = static_cast<char*>(x.poll_ws) + kPollRecBytes + kPollRowBytes;
+      }
       return launch_getf2(a, G, st);
     }
     case XK_PERM: {
@@ -190,6 +218,7 @@ cudaError_t setup_exec(XExec& x, const std::vector<uint64_t>& anc) {
   int nget = 0;
   cudaError_t e;
   if ((e = cudaMalloc(&x.d_info, 4 * sizeof(int))) != cudaSuccess) return e;  // before the descriptors use it
+  if ((e = cudaMemset(x.d_info, 0, 4 * sizeof(int))) != cudaSuccess) return e;   // [2]: the replay counter
   for (size_t i = 0; i < n; ++i) {
     const XOp& o = x.ops[i];
     if (o.kind == XK_GETF2 && o.mode == 0) x.slot[i] = nget++;
@@ -232,6 +261,9 @@ cudaError_t setup_exec(XExec& x, const std::vector<uint64_t>& anc) {
     if ((e = cudaMalloc(&x.bars, nget * sizeof(unsigned))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&x.cand, nget * kCandDoubles * sizeof(double))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&x.cand_idx, nget * 2 * 160 * sizeof(int))) != cudaSuccess) return e;
+    const size_t pb = kPollRecBytes + kPollRowBytes + kPollDiagBytes;
+    if ((e = cudaMalloc(&x.poll_ws, pb)) != cudaSuccess) return e;
+    if ((e = cudaMemset(x.poll_ws, 0, pb)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

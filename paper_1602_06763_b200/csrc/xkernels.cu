@@ -409,6 +409,24 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+// One 16-byte access each, memory-model strong (relaxed.gpu): a record and its
+// epoch are read or written whole, and a spin on it is not hoisted (a weak
+// load in a loop is; __ldcg on a longlong2 may also be split in two).
+__device__ __forceinline__ longlong2 ld16_cg(const longlong2* p) {
+  longlong2 v;
+  asm volatile(
+      "{\n .reg .b128 t;\n ld.relaxed.gpu.global.b128 t, [%2];\n mov.b128 {%0, %1}, t;\n}\n"
+      : "=l"(v.x), "=l"(v.y)
+      : "l"(p)
+      : "memory");
+  return v;
+}
+__device__ __forceinline__ void st16_cg(longlong2* p, longlong2 v) {
+  asm volatile("{\n .reg .b128 t;\n mov.b128 t, {%1, %2};\n st.relaxed.gpu.global.b128 [%0], t;\n}\n" ::"l"(p), "l"(v.x),
+               "l"(v.y)
+               : "memory");
+}
+
 // Barrier of the panel warps only (named barrier 1, kGetf2RowThreads threads):
 // the interchange warps run decoupled (k_getf2).
 __device__ __forceinline__ void panel_sync() {
@@ -447,8 +465,23 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& phase) {
 // each interchange to this CTA's slice of every column outside the panel (the
 // recursion's laswp calls, folded in), following the pivots through a
 // shared-memory list at their own pace, off the panel's chain.
+#ifdef RELAPACK_GETF2_PROBE  // tools/microbench/getf2_probe.cu only: phase cycles accumulated in registers
+__device__ long long g_gprobe[8];
+#define GPROBE(k)                    \
+  {                                  \
+    const long long now = clock64(); \
+    pacc[k] += now - t_last;         \
+    t_last = now;                    \
+  }
+#else
+#define GPROBE(k)
+#endif
+
 __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
   if (ld_info(a.d_info) != 0) return;
+#ifdef RELAPACK_GETF2_PROBE
+  long long t_last = clock64(), pacc[8] = {};
+#endif
   extern __shared__ double sm[];
   const int w = a.w, R = a.rows_per_cta;
   const int g = blockIdx.x, G = gridDim.x;
@@ -490,6 +523,7 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
   } else {
     // ---- panel warps
     unsigned phase = 0;
+    const unsigned epoch = a.poll ? ((*a.replay) << 16) + a.epoch_base : 0u;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int j = 0; j < jmax; ++j) {
       // (a) local first maximum of |a(i, j)| over owned rows i >= j
@@ -521,6 +555,68 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
       }
       // (b) publish: value, index and the candidate row; the owner of row j publishes it too
       const int buf = j & 1;
+      if (a.poll) {
+        // epoch-stamped 16-byte records, one store each: a reader takes a
+        // record once its epoch is this column's (old or new, never torn)
+        const unsigned E = epoch + (unsigned)j + 1u;
+        longlong2* rec = reinterpret_cast<longlong2*>(a.prec);
+        longlong2* rrow = reinterpret_cast<longlong2*>(a.prow);
+        longlong2* rdiag = reinterpret_cast<longlong2*>(a.pdiag);
+        if (warp == 0) {
+          const bool ok = bi != 0x7fffffff;
+          for (int c = lane; c < w; c += 32)
+            st16_cg(rrow + ((int64_t)buf * G + g) * kGetf2Max + c,
+                   make_longlong2(__double_as_longlong(ok ? sP[(bi - r0) * sld + c] : 0.0), (long long)E));
+          if (lane == 0)
+            st16_cg(rec + buf * G + g, make_longlong2(__double_as_longlong(bv),
+                                                     (long long)(((unsigned long long)E << 32) | (unsigned)bi)));
+        } else if (warp == 1 && j >= r0 && j < r0 + rows) {
+          for (int c = lane; c < w; c += 32)
+            st16_cg(rdiag + buf * kGetf2Max + c, make_longlong2(__double_as_longlong(sP[(j - r0) * sld + c]), (long long)E));
+        }
+        GPROBE(0);
+        GPROBE(1);
+        if (warp == 0) {
+          double v = -1.0;
+          int i = 0x7fffffff, who = -1;
+          for (int q = lane; q < G; q += 32) {
+            longlong2 x;
+            do {
+              x = ld16_cg(rec + buf * G + q);
+            } while ((unsigned)((unsigned long long)x.y >> 32) != E);
+            const double qv = __longlong_as_double(x.x);
+            const int qi = (int)(unsigned)(x.y & 0xffffffffull);
+            if (qi != 0x7fffffff && (qv > v || (qv == v && qi < i))) { v = qv; i = qi; who = q; }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+            if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; who = ow; }
+          }
+          if (who < 0) i = j;  // no comparable candidate (a NaN column): row j stays, no interchange
+          if (lane == 0) {
+            s_p = i;
+            s_pivots[j] = i;
+            __threadfence_block();
+            s_ready = j + 1;  // the interchange warps may apply it
+          }
+          for (int c = lane; c < w; c += 32) {
+            longlong2 x;
+            do {
+              x = ld16_cg(rdiag + buf * kGetf2Max + c);
+            } while ((unsigned)x.y != E);
+            sDiag[c] = __longlong_as_double(x.x);
+            if (who >= 0) {
+              do {
+                x = ld16_cg(rrow + ((int64_t)buf * G + who) * kGetf2Max + c);
+              } while ((unsigned)x.y != E);
+            }
+            sPiv[c] = __longlong_as_double(x.x);
+          }
+        }
+      } else {
       double* slot_row = a.cand_rows + ((int64_t)buf * G + g) * kGetf2Max;
       if (threadIdx.x == 0) {
         a.cand_val[buf * G + g] = bv;
@@ -532,8 +628,10 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
       }
       if (j >= r0 && j < r0 + rows)
         for (int c = threadIdx.x; c < w; c += kGetf2RowThreads) a.diag_row[buf * kGetf2Max + c] = sP[(j - r0) * sld + c];
+      GPROBE(0);
       // (c) barrier
       grid_sync(a.bar, phase);
+      GPROBE(1);
       // (d) global first maximum
       if (warp == 0) {
         double v = -1.0;
@@ -562,8 +660,10 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
           sDiag[c] = __ldcg(a.diag_row + buf * kGetf2Max + c);
         }
       }
+      }  // !poll
       panel_sync();
       const int p = s_p;
+      GPROBE(2);
       // (e) interchange rows j and p among the owned rows
       if (p != j) {
         if (j >= r0 && j < r0 + rows)
@@ -576,6 +676,7 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
         if (sPiv[j] == 0.0) atomicMin(a.getrf_info, a.info_base + j + 1);
       }
       panel_sync();
+      GPROBE(4);
       // (f) multipliers and the rank-1 update of the owned rows below row j
       const double piv = sPiv[j];
       for (int r = threadIdx.x; r < rows; r += kGetf2RowThreads) {
@@ -587,6 +688,7 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
         for (int c = j + 1; c < w; ++c) sP[r * sld + c] -= l * sPiv[c];
       }
       panel_sync();
+      GPROBE(5);
     }
   }
   __syncthreads();
@@ -594,6 +696,10 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
     const int r = e % rows, c = e / rows;
     a.P[(int64_t)(r0 + r) + (int64_t)c * a.ld] = sP[r * sld + c];
   }
+#ifdef RELAPACK_GETF2_PROBE
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int k = 0; k < 8; ++k) g_gprobe[k] = pacc[k];
+#endif
 }
 
 // ---- cluster panel
@@ -617,17 +723,6 @@ __global__ void __launch_bounds__(kGetf2Threads) k_getf2(XGetf2Args a) {
 //       skips the division).
 // No global-memory round trip and no shared-memory traffic proportional to
 // the panel inside the column loop.
-#ifdef RELAPACK_GETF2_PROBE  // tools/microbench/getf2_probe.cu only: phase cycles accumulated in registers
-__device__ long long g_gprobe[8];
-#define GPROBE(k)                    \
-  {                                  \
-    const long long now = clock64(); \
-    pacc[k] += now - t_last;         \
-    t_last = now;                    \
-  }
-#else
-#define GPROBE(k)
-#endif
 
 template <int T, int S, int W>
 __global__ void __launch_bounds__(T) k_getf2_clr(XGetf2ClArgs a) {

@@ -56,6 +56,14 @@ struct XGetf2Args {
   double* A0;         // element (panel row 0, column 0) of the matrix: the interchanges apply to every column
   int ncols, c0;      // the matrix's columns; the panel's first column
   const int* d_info;
+  // epoch-stamped exchange (poll != 0): 16-byte records {value, epoch} read
+  // until their epoch is this column's — no grid barrier, no fence
+  int poll;
+  unsigned epoch_base;       // (replay << 16) | (op << 6) is added on the device (replay: *replay)
+  const unsigned* replay;    // the plan's replay counter (incremented by its prologue)
+  void* prec;                // [2][grid] candidate records {|a|, (epoch << 32) | row}
+  void* prow;                // [2][grid][kGetf2Max] candidate-row records {a, epoch}
+  void* pdiag;               // [2][kGetf2Max] row-j records {a, epoch}
 };
 
 // Cluster panel (k_getf2_clr): the same LU with partial pivoting of an m x w

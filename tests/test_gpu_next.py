@@ -228,12 +228,13 @@ def test_getrf_singular_and_identity():
     assert ip.cpu().tolist() == list(range(1, 78))
 
 
-@pytest.mark.parametrize("cluster", ["16", "8"])
+@pytest.mark.parametrize("cluster", ["16", "8", "poll"])
 def test_getrf_panel_variants(cluster):
     """The getrf panels on one thread-block cluster of 16 / 8 CTAs (opt-in
     RELAPACK_GETF2_CLUSTER; narrower leaves for tall panels, interchanges by
-    k_permute) — the knob is read once per process, so each variant runs in a
-    subprocess."""
+    k_permute) and the cooperative panels with the epoch-stamped exchange
+    (opt-in RELAPACK_GETF2_POLL) — the knobs are read once per process, so each
+    variant runs in a subprocess."""
     import os
     import subprocess
     import sys
@@ -243,7 +244,7 @@ def test_getrf_panel_variants(cluster):
             "for mn in [(33, 33), (300, 300), (1031, 1031), (1500, 700), (700, 1500), (4096, 64), (16384, 48)]:\n"
             "    test_getrf(*mn)\n"
             "test_getrf_singular_and_identity()\nprint('variant ok')\n")
-    env = dict(os.environ, RELAPACK_GETF2_CLUSTER=cluster)
+    env = dict(os.environ, **({"RELAPACK_GETF2_POLL": "1"} if cluster == "poll" else {"RELAPACK_GETF2_CLUSTER": cluster}))
     r = subprocess.run([sys.executable, "-c", code], cwd=Path(__file__).resolve().parents[1], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

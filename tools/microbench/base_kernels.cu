@@ -41,13 +41,20 @@ int main() {
     printf("potf2 n=64 phases (cycles from start): stage-in %lld |", pr[1] - pr[0]);
     for (int p = 0; p < 8; ++p) printf(" P%d %lld |", p, pr[2 + p] - pr[0]);
     printf(" factor-end %lld end %lld\n", pr[62] - pr[0], pr[63] - pr[0]);
-    printf("potf2 n=64 panel j0=16 (warp 0): strip_update %lld | factor_panel %lld | barrier wait %lld\n",
-           pr[41] - pr[40], pr[42] - pr[41], pr[43] - pr[42]);
+    auto loops = [&](const char* what) {
+      for (int p = 0; p < 7; ++p)
+        printf("%s loop j0=%2d: warp0 strip_update %5lld factor_panel %5lld | warp1 trail %5lld | barrier end %5lld\n", what, 8 * p,
+               pr[12 + p] - (p ? pr[1 + p] : pr[11]), pr[22 + p] - pr[12 + p], pr[32 + p] - (p ? pr[1 + p] : pr[11]),
+               pr[2 + p] - (p ? pr[1 + p] : pr[11]));
+    };
+    loops("potf2 n=64");
     launch_potf2(d, n, kLayoutN, 128, info, 0, 0);
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
     printf("node128 phases (cycles): load %lld | potf2(A11) %lld | trsm %lld | syrk %lld | potf2(A22) %lld | store %lld\n",
            pr[51] - pr[50], pr[52] - pr[51], pr[53] - pr[52], pr[54] - pr[53], pr[55] - pr[54], pr[56] - pr[55]);
+    printf("node128 potf2(A22): first panel %lld\n", pr[11] - pr[54]);
+    loops("node128 A22");
     setenv("RELAPACK_NODE128", "0", 1);
     launch_potf2(d, n, kLayoutN, 128, info, 0, 0);
     cudaDeviceSynchronize();
