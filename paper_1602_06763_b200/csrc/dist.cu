@@ -232,7 +232,6 @@ int build_exec(DistPlan& dp, int n, int layout, const PlanParams& pp, const Dist
   }
   dp.send_elems = send_elems;
   if (send_elems > 0) {
-    if ((e = cudaMalloc(&dp.send, send_elems * sizeof(double))) != cudaSuccess) return cuda_fail(e, "send buffer");
     if ((e = cudaMalloc(&dp.recv, send_elems * d.nranks * sizeof(double))) != cudaSuccess)
       return cuda_fail(e, "recv buffer");
   }
@@ -242,6 +241,13 @@ int build_exec(DistPlan& dp, int n, int layout, const PlanParams& pp, const Dist
 }  // namespace
 
 void destroy_dist_plan(DistPlan* p) { delete p; }
+
+// This rank's packed chunk of op i: its slot inside the receive buffer, so the
+// all-gather runs in place (NCCL: sendbuff == recvbuff + rank * count) and the
+// own rows are never copied send -> recv.
+static inline double* send_ptr(const DistPlan& dp, size_t i, int rank, int ncols) {
+  return dp.recv + (size_t)rank * (size_t)dp.rows_pad[i] * (size_t)ncols;
+}
 
 // Pointer + ld of an op operand (matrix or the current packed send chunk).
 static inline double* operand(int buf, int ri, int ci, int layout, double* A, int64_t lda, double* send, int rows_pad,
@@ -267,7 +273,7 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
         e = launch_potf2(A + lv_off(layout, op.c_i, op.c_j, lda), lda, layout, op.n, d_info, op.info_base, st);
         break;
       case OP_TRSM: {
-        double* B = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
+        double* B = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, send_ptr(dp, i, rank, nc), pad, nc, &ldc);
         e = launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, lda), lda, B, ldc, layout, op.m, op.k, d_info, st);
         break;
       }
@@ -275,9 +281,10 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
       case OP_SYRK: {
         UpdateOp& u = dp.upd[i];
         const bool syrk = op.kind == OP_SYRK;
-        double* C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
-        const double* Ap = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, dp.send, pad, nc, &lda_);
-        const double* Bp = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, dp.send, pad, nc, &ldb);
+        double* sp = send_ptr(dp, i, rank, nc);
+        double* C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, sp, pad, nc, &ldc);
+        const double* Ap = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, sp, pad, nc, &lda_);
+        const double* Bp = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, sp, pad, nc, &ldb);
         init_update(u, C, ldc, layout, Ap, lda_, layout, Bp, ldb, layout, syrk ? op.n : op.m, op.n, op.k, -1.0,
                     syrk ? 1 : 0);
         u.args.d_info = d_info;
@@ -287,7 +294,7 @@ static int run_local(DistPlan& dp, size_t beg, size_t end, int layout, double* A
       case OP_PACK: {
         const int64_t total = (int64_t)pad * op.k;
         k_pack_rows<<<grid_for(total), 256, 0, st>>>(A, lda, layout, dp.d_rows[i] + (size_t)rank * pad, pad, op.c_j,
-                                                     op.k, dp.send, d_info);
+                                                     op.k, send_ptr(dp, i, rank, op.k), d_info);
         e = cudaGetLastError();
         break;
       }
@@ -317,7 +324,7 @@ static cudaError_t launch_dist_op(DistPlan& dp, size_t i, int layout, double* A,
     case OP_POTF2:
       return launch_potf2(A + lv_off(layout, op.c_i, op.c_j, lda), lda, layout, op.n, d_info, op.info_base, st);
     case OP_TRSM: {
-      double* B = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
+      double* B = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, send_ptr(dp, i, d.rank, nc), pad, nc, &ldc);
       return launch_trsm_any(A + lv_off(layout, op.a_i, op.a_j, lda), lda, B, ldc, layout, op.m, op.k, d_info, st);
     }
     case OP_GEMM:
@@ -326,7 +333,7 @@ static cudaError_t launch_dist_op(DistPlan& dp, size_t i, int layout, double* A,
     case OP_PACK: {
       const int64_t total = (int64_t)pad * op.k;
       k_pack_rows<<<grid_for(total), 256, 0, st>>>(A, lda, layout, dp.d_rows[i] + (size_t)d.rank * pad, pad, op.c_j,
-                                                   op.k, dp.send, d_info);
+                                                   op.k, send_ptr(dp, i, d.rank, op.k), d_info);
       return cudaGetLastError();
     }
     case OP_UNPACK: {
@@ -337,7 +344,8 @@ static cudaError_t launch_dist_op(DistPlan& dp, size_t i, int layout, double* A,
     }
     case OP_ALLGATHER: {
       const size_t cnt = (size_t)pad * op.k;
-      const ncclResult_t r = nccl().AllGather(dp.send, dp.recv, cnt, ncclDouble_, comm->nccl, st);
+      // in place: this rank's chunk already sits at recv + rank * cnt
+      const ncclResult_t r = nccl().AllGather(send_ptr(dp, i, d.rank, op.k), dp.recv, cnt, ncclDouble_, comm->nccl, st);
       if (r != 0) {
         set_error(std::string("ncclAllGather: ") + (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
         return cudaErrorUnknown;
@@ -514,9 +522,10 @@ void relapack_dpotrf_dist(const char* uplo, const int* n_, double* A, const int*
         if (op.kind != OP_GEMM && op.kind != OP_SYRK) continue;
         int64_t ldc = 0, lda_ = 0, ldb = 0;
         const int pad = dp.rows_pad[i], nc = dp.ncols[i];
-        double* C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, dp.send, pad, nc, &ldc);
-        const double* Ap = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, dp.send, pad, nc, &lda_);
-        const double* Bp = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, dp.send, pad, nc, &ldb);
+        double* sp = send_ptr(dp, i, d.rank, nc);
+        double* C = operand(op.c_buf, op.c_i, op.c_j, layout, A, lda, sp, pad, nc, &ldc);
+        const double* Ap = operand(op.a_buf, op.a_i, op.a_j, layout, A, lda, sp, pad, nc, &lda_);
+        const double* Bp = operand(op.b_buf, op.b_i, op.b_j, layout, A, lda, sp, pad, nc, &ldb);
         const bool syrk = op.kind == OP_SYRK;
         init_update(dp.upd[i], C, ldc, layout, Ap, lda_, layout, Bp, ldb, layout, syrk ? op.n : op.m, op.n, op.k,
                     -1.0, syrk ? 1 : 0);
@@ -669,8 +678,9 @@ int relapack_dpotrf_dist_loopback(const char* uplo, int n, double* const* A_rank
       const size_t i = stop[dst];
       const size_t cnt = (size_t)plans[dst]->rows_pad[i] * plans[dst]->ops[i].k;
       for (int src = 0; src < nranks; ++src)
-        cudaMemcpyAsync(plans[dst]->recv + (size_t)src * cnt, plans[src]->send, cnt * sizeof(double),
-                        cudaMemcpyDeviceToDevice, st);
+        if (src != dst)  // in place: the own chunk is already there
+          cudaMemcpyAsync(plans[dst]->recv + (size_t)src * cnt, plans[src]->recv + (size_t)src * cnt,
+                          cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
     }
     for (int s = 0; s < nranks; ++s) beg[s] = stop[s] + 1;
   }

@@ -248,8 +248,13 @@ void compute_deps(const std::vector<PlanOp>& ops, std::vector<std::vector<int>>&
     uint64_t* aj = &anc[j * words];
     for (size_t ii = j; ii-- > 0;) {
       if (aj[ii / 64] >> (ii % 64) & 1) continue;  // already implied
+      // the packed send chunk is this rank's slot of the receive buffer (the
+      // all-gather runs in place): a write to BUF_SEND also touches BUF_RECV
+      auto recv_hit = [](const Rect& w, const Rect& x) { return w.buf == BUF_SEND && x.buf == BUF_RECV; };
       const bool conflict = overlap(W[ii], W[j]) || overlap(W[ii], R1[j]) || overlap(W[ii], R2[j]) ||
-                            overlap(R1[ii], W[j]) || overlap(R2[ii], W[j]);
+                            overlap(R1[ii], W[j]) || overlap(R2[ii], W[j]) || recv_hit(W[ii], W[j]) ||
+                            recv_hit(W[ii], R1[j]) || recv_hit(W[ii], R2[j]) || recv_hit(W[j], W[ii]) ||
+                            recv_hit(W[j], R1[ii]) || recv_hit(W[j], R2[ii]);
       if (!conflict) continue;
       deps[j].push_back((int)ii);
       const uint64_t* ai = &anc[ii * words];

@@ -753,6 +753,16 @@ static bool copy_pairs() {
   return r;
 }
 
+// Shared memory requested per node-128 launch: RELAPACK_NODE_EXCLUSIVE=1 asks
+// for (nearly) the whole SM so no other CTA (an update tile) shares it.
+static int node128_smem() {
+  static const int v = [] {
+    const char* e = getenv("RELAPACK_NODE_EXCLUSIVE");
+    return (e && e[0] == '0') ? (int)P2<kBaseMax>::SMEM : 220 * 1024;
+  }();
+  return v;
+}
+
 static bool potf2_node128() {
   static const bool r = [] {
     const char* v = getenv("RELAPACK_NODE128");
@@ -767,7 +777,7 @@ cudaError_t configure_potf2() {
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
   cudaError_t e = cudaFuncSetAttribute(k_potf2_base, attr, (int)P2<kBaseMax>::SMEM);
   if (e != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_potf2_node128, attr, (int)P2<kBaseMax>::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_potf2_node128, attr, node128_smem())) != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_potf2_base64, attr, (int)P2<64>::SMEM);
 }
 
@@ -788,7 +798,7 @@ cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, 
   } else if (n <= 64)
     k_potf2_base64<<<1, P2<64>::THREADS, P2<64>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
   else if (potf2_node128())
-    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout | (copy_pairs() ? 0x100 : 0), n,
+    k_potf2_node128<<<1, P2<kBaseMax>::THREADS, node128_smem(), st>>>(A, ld, layout | (copy_pairs() ? 0x100 : 0), n,
                                                                           d_info, info_base, g_launch_trace);
   else
     k_potf2_base<<<1, P2<kBaseMax>::THREADS, P2<kBaseMax>::SMEM, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace);
