@@ -68,6 +68,7 @@ VARIANTS = {
     "prio_two_levels": {"RELAPACK_PRIO_MODE": "0"},
     "chain_split_as_others": {"RELAPACK_SPLITK_CHAIN_KT": "0"},
     "no_defer_cap": {"RELAPACK_BULK_CTAS": "0"},
+    "node_shared_sm": {"RELAPACK_NODE_EXCLUSIVE": "0"},
 }
 
 
