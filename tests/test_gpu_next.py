@@ -180,6 +180,56 @@ def test_potrs(n, nrhs, uplo):
     assert np.isnan(dT.cpu().numpy()[other_mask(n, uplo)]).all()
 
 
+def padded_dev(A, extra):
+    """Column-major device view of A inside a (n + extra)-row buffer whose
+    padding rows hold NaN (an odd lda: no 16-byte-aligned columns, the plain-load
+    paths of the kernels)."""
+    m, n = A.shape
+    buf = np.full((m + extra, n), np.nan)
+    buf[:m] = A
+    d = torch.from_numpy(np.ascontiguousarray(buf.T)).cuda().t()
+    return d[:m], d
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_next_ops_padded_lda(uplo):
+    """trtri, lauum, potrs and getrf on a matrix with lda = n + 3: the same
+    parity, and the lda padding (NaN) bitwise untouched."""
+    n = 301
+    T, A = chol_factor(n, 31, uplo)
+    for op in ("trtri", "lauum"):
+        dT, full = padded_dev(T, 3)
+        assert (rl.dtrtri(dT, uplo, "N") if op == "trtri" else rl.dlauum(dT, uplo)) == 0
+        G = dT.cpu().numpy()
+        R = np.array(T, order="F")
+        if op == "trtri":
+            assert oracle.dtrtri(R, uplo, "N") == 0
+            assert colnorm_err(tri_part(G, uplo), tri_part(R, uplo)) <= 1e-11
+        else:
+            oracle.dlauum(R, uplo)
+            assert colnorm_err(tri_part(G, uplo), tri_part(R, uplo)) <= 1e-11
+        assert np.isnan(full.cpu().numpy()[n:]).all()
+        assert np.isnan(G[other_mask(n, uplo)]).all()
+    B0 = np.asfortranarray(np.random.default_rng(5).uniform(-1, 1, size=(n, 37)))
+    dT, _ = padded_dev(T, 3)
+    dB, fullB = padded_dev(B0, 5)
+    assert rl.dpotrs(dT, dB, uplo) == 0
+    R = np.array(B0, order="F")
+    oracle.dpotrs(np.nan_to_num(T), R, uplo)
+    assert colnorm_err(dB.cpu().numpy(), R) <= 1e-11
+    assert np.isnan(fullB.cpu().numpy()[n:]).all()
+    if uplo == "L":
+        M = np.asfortranarray(np.random.default_rng(9).uniform(-1, 1, size=(n, n)))
+        dM, fullM = padded_dev(M, 3)
+        ipiv = torch.zeros(n, dtype=torch.int32, device="cuda")
+        assert rl.dgetrf(dM, ipiv) == 0
+        R = np.array(M, order="F")
+        rinfo, rpiv = oracle.dgetrf(R)
+        assert rinfo == 0 and np.array_equal(ipiv.cpu().numpy(), rpiv)
+        assert colnorm_err(dM.cpu().numpy(), R) <= 1e-9
+        assert np.isnan(fullM.cpu().numpy()[n:]).all()
+
+
 # ------------------------------------------------------------------ N4 getrf
 def apply_ipiv(A, ipiv):
     A = A.copy()
