@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--nb", type=int, default=512, help="multi-GPU row block")
     ap.add_argument("--dist-min", type=int, default=8192, help="multi-GPU replicated-leaf threshold")
     ap.add_argument("--batch-count", type=int, default=131072)
+    ap.add_argument("--dist", action="store_true",
+                    help="the multi-GPU executor even at one GPU (NCCL world size 1; exercises the N > 1 path)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -216,14 +218,19 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist_
 
-        dist_.init_process_group("nccl", device_id=dev)
+        if world == 1:  # --dist on one GPU: a world-size-1 group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29513")
+            dist_.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        else:
+            dist_.init_process_group("nccl", device_id=dev)
     if args.config == "batch":
         return run_batch(args, rank, world, dev)
 
-    if world > 1:
+    if world > 1 or args.dist:
         return run_dist(args, rank, world, dev, n, uplo, dist)
 
     # ------------------------------------------------------------------ N = 1
@@ -864,9 +871,28 @@ def run_dist(args, rank, world, dev, n, uplo, dist):
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         times = [step() for _ in range(args.steps)]
     ms = _max_over_ranks(sum(times) / len(times), world, dev)
+    # end to end: every rank's replica comes from pinned host memory, the
+    # factorization runs, the info word goes back (the factor stays on the
+    # device: SPMD, one replica per rank)
+    H = P.cpu().pin_memory() if args.e2e_steps > 0 else None
+    e2e_t = []
+    for i in range(args.e2e_steps + 1 if H is not None else 0):
+        torch.cuda.synchronize(dev)
+        tdist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        W.copy_(H, non_blocking=True)
+        info = rl.dpotrf_dist(W, comm, uplo, nb=nb, dist_min=dmin, stream=st)  # reads info back (4 bytes)
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        assert info == 0, info
+        if i > 0:
+            e2e_t.append(e0.elapsed_time(e1))
+    e2e_ms = _max_over_ranks(sum(e2e_t) / len(e2e_t), world, dev) if e2e_t else None
     sched = rl.dist_schedule(n, rank, world, nb=nb, dist_min=dmin)
     launches = sum(1 for o in sched if o["kind"] != "allgather")
     comm.close()
+    tdist.destroy_process_group()
     if rank != 0:
         return 0
     gflops = n ** 3 / 3.0 / (ms / 1e3) / 1e9
@@ -875,15 +901,23 @@ def run_dist(args, rank, world, dev, n, uplo, dist):
         "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Philox B, A = B B^T + n I)",
-        "config": {"workload": f"single dpotrf n={n} uplo={uplo} sharded over {world} GPUs",
+        "config": {"workload": f"single dpotrf n={n} uplo={uplo} sharded over {world} GPU(s) (multi-GPU executor)",
                    "n": n, "uplo": uplo, "nb": nb, "dist_min": dmin, "parallelism": f"rowblock-cyclic x{world}",
                    "l2": "input > L2; restored from a pristine copy between steps (untimed)"},
         "pct_fp64_peak_per_gpu": round(100 * gflops / 1e3 / FP64_PEAK_TFLOPS_DATASHEET / world, 2),
         "gpu_launches": launches * args.steps, "step_times_ms": [round(t, 4) for t in times],
         "clocks": clk.summary(),
-        "roofline": None,
-        "e2e": None,
-        "e2e_note": "relapack_dpotrf_dist takes device buffers (SPMD, one replica per rank); no host-matrix path",
+        "roofline": {"kernel": "whole distributed step per GPU (DMMA update kernels + NCCL all-gathers)",
+                     "bound": "tensor", "achieved": round(gflops / 1e3 / world, 3), "peak": FP64_PEAK_TFLOPS_DATASHEET,
+                     "unit": "TFLOP/s", "frac": round(gflops / 1e3 / world / FP64_PEAK_TFLOPS_DATASHEET, 4),
+                     "traffic": None,
+                     "note": "step-level: n^3/3 over the max-over-ranks step time, per GPU (no per-kernel trace in "
+                             "the SPMD executor)"},
+        "e2e": ({"value": round(n ** 3 / 3.0 / (e2e_ms / 1e3) / 1e9, 2), "unit": "GFLOP/s",
+                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(n) * n * 8 * world,
+                 "d2h_bytes_per_step": 4 * world, "steps": len(e2e_t),
+                 "api": "relapack_dpotrf_dist; every rank's replica copied from pinned host memory inside the "
+                        "timed region, the info word read back"} if e2e_ms else None),
     }
     print(json.dumps(out))
     return 0
