@@ -161,7 +161,7 @@ def finalize() -> None:
 
 def set_crossover(c: int) -> None:
     if lib().relapack_set_crossover(int(c)) != 0:
-        raise ValueError(f"crossover {c} out of range [16, 128]")
+        raise ValueError(f"crossover {c} out of range [16, 256]")
 
 
 def set_split_tile(t: int) -> None:

@@ -74,10 +74,10 @@ int trsm_base_cols() {
 PlanParams current_params() {
   PlanParams p;
   int c = g_crossover.load();
-  if (c < 0) c = env_int("RELAPACK_CROSSOVER", 128);
+  if (c < 0) c = env_int("RELAPACK_CROSSOVER", kCrossoverDefault);
   int t = g_split_tile.load();
   if (t < 0) t = env_int("RELAPACK_SPLIT_TILE", 64);
-  if (c < 16 || c > kPotf2Max) c = 128;
+  if (c < 16 || c > kPotf2Max) c = kCrossoverDefault;
   if (t != 8 && t != 16 && t != 32 && t != 64 && t != 128) t = 64;
   p.crossover = c;
   p.split_tile = t;

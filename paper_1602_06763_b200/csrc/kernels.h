@@ -72,7 +72,15 @@ int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit);
 // ---- K1 base-case potf2 (potf2.cu) ----
 // Factor the n x n L-view block at A (n <= kPotf2Max) in shared memory; on a
 // non-positive pivot at local column j write d_info = info_base + j + 1.
-constexpr int kPotf2Max = 128;
+// n <= 128: one CTA holds the block (register / shared-memory kernels, the
+// 128-node); 128 < n <= 256: the 256-node kernel (split at 128, TRSM and SYRK
+// inside the CTA).
+constexpr int kPotf2Max = 256;
+// default crossover c of the recursion (RELAPACK_CROSSOVER / relapack_set_crossover
+// override): 128 — the 256-node kernel measured slower on the chain (one SM
+// does the TRSM and SYRK the separate launches spread over 4-10 SMs: n = 4096
+// 2.82 vs 2.09 ms, n = 256 0.117 vs 0.105 ms; tools/experiments/exp_node256.sh)
+constexpr int kCrossoverDefault = 128;
 cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, int info_base, cudaStream_t st);
 
 // ---- K5 base TRSM (trsm.cu): B(m x t) := B * L^{-T}, L t x t lower (t <= kTrsmMax)

@@ -1,5 +1,6 @@
-// potf2.cu — K1 (base case of the recursion, order n <= 128): Cholesky of a
-// block held entirely in one SM's shared memory (north_star subsystem (2); P:301-307 crossover to the
+// potf2.cu — K1 (base case of the recursion, order n <= 128; the opt-in
+// 256-node kernel for 128 < n <= 256): Cholesky of a block held entirely in
+// one SM's shared memory (north_star subsystem (2); P:301-307 crossover to the
 // unblocked kernel; "the unblocked kernel is slightly faster ...
 // within the processor's L1 cache" -> on the GPU: within shared memory).
 //
@@ -22,6 +23,7 @@
 #include "chol_regs.cuh"
 #include "common.cuh"
 #include "kernels.h"
+#include "trsm_regs.cuh"
 
 namespace relapack {
 
@@ -307,7 +309,7 @@ __device__ __forceinline__ void copy_lower(double* s, double* __restrict__ A, in
   }
 }
 
-constexpr int kBaseMax = kPotf2Max;  // 128
+constexpr int kBaseMax = 128;  // the square of the 128-node kernels
 
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_base(double* A, int64_t ld, int layout, int n,
                                                                        int* d_info, int info_base, TraceRec* tr) {
@@ -631,6 +633,48 @@ __device__ __forceinline__ void syrk_in_smem(double* s, int n2) {
   }
 }
 
+// The 128-node's four phases on the block already in shared memory (A11's
+// 64 x 64 block loaded, the rest possibly still in flight by cp.async): factor
+// A11, A21 := A21 L11^{-T}, A22 -= A21 A21^T, factor A22.  n <= 128; for
+// n <= 64 only the first factorization runs.  Returns 0 or the 1-based local
+// column of the first failed pivot (the block then holds the factor up to it).
+template <int LDS, int NW>
+__device__ __forceinline__ int node128_factor(double* s, int n, int* fail_flag, double* rinv) {
+  int fail = potf2_smem<kN1, LDS, NW>(s, n < kN1 ? n : kN1, fail_flag);
+  PROBE(52);
+  if (fail == 0 && n > kN1) {
+    const int n2 = n - kN1;
+    if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    trsm_in_smem<LDS>(s, rinv, n2);
+    __syncthreads();
+    PROBE(53);
+    syrk_in_smem<LDS, NW>(s, n2);
+    __syncthreads();
+    PROBE(54);
+    fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, fail_flag);
+    if (fail) fail += kN1;
+  } else {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+  PROBE(55);
+  return fail;
+}
+
+// Store the factored 128-node (the lower triangle of its n x n block) from
+// shared memory; after a failure in the first 64 columns only A11's block.
+template <int LDS, int TH>
+__device__ __forceinline__ void node128_store(double* s, double* A, int64_t ld, int layout, int n, int fail,
+                                              bool pairs) {
+  if (fail == 0 || fail > kN1) {
+    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
+    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
+  } else {
+    copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
+  }
+}
+
 __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double* A, int64_t ld, int layout, int n,
                                                                           int* d_info, int info_base, TraceRec* tr) {
   const bool pairs = (layout & 0x100) != 0;  // 16-byte copies (host knob RELAPACK_COPY_PAIRS)
@@ -653,38 +697,175 @@ __global__ void __launch_bounds__(P2<kBaseMax>::THREADS) k_potf2_node128(double*
   copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, n, kN1, 0, pairs);
   __syncthreads();
   PROBE(51);
-  int fail = potf2_smem<kN1, LDS, NW>(s, kN1, &fail_flag);
-  PROBE(52);
-  if (fail == 0) {
-    const int n2 = n - kN1;
-    if (threadIdx.x < kN1) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-    trsm_in_smem<LDS>(s, rinv, n2);
-    __syncthreads();
-    PROBE(53);
-#if RELAPACK_NODE_EARLY_STORE
-    // L11 and L21 are final: write them back while A22 is finished
-    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
-#endif
-    syrk_in_smem<LDS, NW>(s, n2);
-    __syncthreads();
-    PROBE(54);
-    fail = potf2_smem<kN1, LDS, NW>(s + kN1 + kN1 * LDS, n2, &fail_flag);
-    if (fail) fail += kN1;
-    PROBE(55);
-    pdl_trigger();
-#if !RELAPACK_NODE_EARLY_STORE
-    copy_rect<kBaseMax, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
-#endif
-    copy_rect<kBaseMax - kN1, kBaseMax - kN1, LDS, TH, 2>(s, A, ld, layout, n, kN1, kN1, pairs);
-  } else {
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    PROBE(55);
-    copy_rect<kN1, kN1, LDS, TH, 2>(s, A, ld, layout, n, 0, 0, pairs);
-  }
+  const int fail = node128_factor<LDS, NW>(s, n, &fail_flag, rinv);
+  pdl_trigger();
+  node128_store<LDS, TH>(s, A, ld, layout, n, fail, pairs);
   PROBE(56);
   if (fail && threadIdx.x == 0) *untag(d_info) = info_base + fail;
+  trace_end(tr);
+}
+
+// ---- K1'' base case for 128 < n <= 256: the recursion's 256-node in ONE CTA
+// (P:286-295 split at n1 = 128): the 128-node phases on A11, then
+//   A21 := A21 L11^{-T}   rows in registers (RG = 2 groups of 8 rows per
+//                          warp, trsm_regs.cuh), L11 read in place from the
+//                          node's shared-memory square;
+//   A22 -= A21 A21^T      DMMA on the lower 8x8 tiles, K = 128 in two halves
+//                          of 64 staged through shared memory (warp w owns
+//                          tile rows w and 15 - w: 17 tiles each), while A22
+//                          streams into the square (cp.async);
+// then the 128-node phases on A22.  One launch instead of the four of the
+// plan's 256-node (node-128, TRSM, SYRK, node-128): no launch gaps and no
+// global round trip of L11 / L21 between them on the base-case chain.
+constexpr int kN2 = 128;             // the 256-node's split
+constexpr int kHLd = 68;             // L21 half row stride (== 4 mod 16: conflict-free fragments)
+
+struct Node256 {
+  static constexpr int LDS = P2<kBaseMax>::LDS, NW = P2<kBaseMax>::NW, TH = P2<kBaseMax>::THREADS;
+  static constexpr size_t SQ = sizeof(double) * (size_t)kBaseMax * LDS;         // the 128 x 128 square
+  static constexpr size_t HALF = sizeof(double) * (size_t)kN2 * kHLd;          // L21[:, half] staging
+  static constexpr size_t SMEM = SQ + HALF;                                     // 204.8 KB
+};
+
+__global__ void __launch_bounds__(Node256::TH, 1) k_potf2_node256(double* A, int64_t ld, int layout, int n,
+                                                                   int* d_info, int info_base, TraceRec* tr) {
+  const bool pairs = (layout & 0x100) != 0;
+  layout &= 0xff;
+  constexpr int LDS = Node256::LDS, NW = Node256::NW, TH = Node256::TH;
+  PROBE(50);
+  {
+    const KState ks = ld_state(d_info);
+    if (ks.info != 0) return;
+    A = rebase(A, ks.base);
+  }
+  trace_begin(tr);
+  extern __shared__ double s[];  // the 128 x 128 square (A11, then L21 rows for nothing, then A22)
+  double* H = s + kBaseMax * LDS; // L21(r, k), k in one 64-column half: H[r * kHLd + k]
+  __shared__ int fail_flag;
+  __shared__ double rinv[kN2];
+  if (threadIdx.x == 0) fail_flag = 0;
+  const int n2 = n - kN2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  double* const A21 = A + lv_off(layout, kN2, 0, ld);
+  double* const A22 = A + lv_off(layout, kN2, kN2, ld);
+  // A21 and A22 towards L2 now (their first reads come after A11's factorization)
+  {
+    constexpr int kLine = 16;  // doubles per 128-byte line
+    for (int e = threadIdx.x; e < 2 * kN2 * (kN2 / kLine); e += TH) {
+      const int blk = e / (kN2 * (kN2 / kLine)), x = e % (kN2 * (kN2 / kLine));
+      const int slow = x / (kN2 / kLine), fast = (x % (kN2 / kLine)) * kLine;  // fast: contiguous index
+      const int i = layout == kLayoutN ? fast : slow, j = layout == kLayoutN ? slow : fast;
+      if (i < n2 && (blk == 0 || j <= i + kLine))
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((blk ? A22 : A21) + lv_off(layout, i, j, ld)));
+    }
+  }
+  copy_rect<kN1, kN1, LDS, TH, 0>(s, A, ld, layout, kN2, 0, 0, pairs);
+  copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A, ld, layout, kN2, kN1, 0, pairs);
+  __syncthreads();
+  PROBE(51);
+  // one call site of the 128-node phases (code size): half 0 factors A11,
+  // half 1 factors A22 after the TRSM and the SYRK below
+  for (int half = 0;; ++half) {
+    double* const Ah = half ? A22 : A;
+    const int nh = half ? n2 : kN2;
+    const int fail = node128_factor<LDS, NW>(s, nh, &fail_flag, rinv);
+    if (half == 1 || fail) {
+      pdl_trigger();
+      node128_store<LDS, TH>(s, Ah, ld, layout, nh, fail, pairs);
+      if (fail && threadIdx.x == 0) *untag(d_info) = info_base + half * kN2 + fail;
+      break;
+    }
+  PROBE(62);
+  // L11 is final: store it (the values leave shared memory before the next
+  // barrier) and form 1 / L_jj of all 128 columns
+  node128_store<LDS, TH>(s, A, ld, layout, kN2, 0, pairs);
+  if (threadIdx.x < kN2) rinv[threadIdx.x] = 1.0 / s[threadIdx.x * (LDS + 1)];
+  // this warp's 16 rows of A21 (two groups of 8) as DMMA accumulator tiles
+  constexpr int RG = 2, NT = 16;
+  double xs[RG][NT][2];
+  const int row_base = warp * 8 * RG;
+  const bool tpairs = layout == kLayoutT && (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(A21) & 15) == 0;
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int sb = 0; sb < NT; ++sb) {
+      const int row = row_base + 8 * r + g, col = 8 * sb + 2 * tq;
+      if (tpairs && row < n2) {
+        const double2 v = *reinterpret_cast<const double2*>(A21 + lv_off(kLayoutT, row, col, ld));
+        xs[r][sb][0] = v.x;
+        xs[r][sb][1] = v.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) xs[r][sb][q] = row < n2 ? A21[lv_off(layout, row, col + q, ld)] : 0.0;
+      }
+    }
+  __syncthreads();
+  PROBE(57);
+  // A21 := A21 L11^{-T}, L11(r, c) = s[r + c * LDS]
+  solve_chunk_regs<RG, 0, NT, 1, LDS>(xs, s, rinv, lane, g, tq);
+  update_chunk1_regs<RG, NT, 1, LDS>(xs, s + kN1, g, tq);
+  solve_chunk_regs<RG, 1, NT, 1, LDS>(xs, s + kN1 + kN1 * LDS, rinv + kN1, lane, g, tq);
+  PROBE(58);
+  // L21 to global
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int sb = 0; sb < NT; ++sb) {
+      const int row = row_base + 8 * r + g, col = 8 * sb + 2 * tq;
+      if (tpairs && row < n2) {
+        *reinterpret_cast<double2*>(A21 + lv_off(kLayoutT, row, col, ld)) = make_double2(xs[r][sb][0], xs[r][sb][1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (row < n2) A21[lv_off(layout, row, col + q, ld)] = xs[r][sb][q];
+      }
+    }
+  __syncthreads();  // every warp is done with L11 in the square: A22 streams in
+  copy_rect<kN1, kN1, LDS, TH, 1>(s, A22, ld, layout, n2, 0, 0, pairs);
+  copy_rect<kBaseMax - kN1, kBaseMax, LDS, TH, 1>(s, A22, ld, layout, n2, kN1, 0, pairs);
+  // A22 -= L21 L21^T: warp w owns tile rows ra = w and rb = 15 - w (17 tiles:
+  // slot j <= ra is tile (ra, j), slot j > ra is tile (rb, j - ra - 1))
+  const int ra = warp, rb = 15 - warp;
+  double acc[17][2];
+  int boff[17];
+#pragma unroll
+  for (int j = 0; j < 17; ++j) {
+    acc[j][0] = acc[j][1] = 0.0;
+    boff[j] = (8 * (j <= ra ? j : j - ra - 1) + g) * kHLd + tq;
+  }
+  const int aoff = (8 * ra + g) * kHLd + tq, boff_b = (8 * rb + g) * kHLd + tq;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    // stage L21[:, 64h .. 64h + 63]
+#pragma unroll
+    for (int r = 0; r < RG; ++r)
+#pragma unroll
+      for (int sb = 0; sb < 8; ++sb)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) H[(row_base + 8 * r + g) * kHLd + 8 * sb + 2 * tq + q] = xs[r][8 * h + sb][q];
+    __syncthreads();
+#pragma unroll 4
+    for (int k0 = 0; k0 < kN1; k0 += 4) {
+      const double a0 = -H[aoff + k0], a1 = -H[boff_b + k0];
+#pragma unroll
+      for (int j = 0; j < 17; ++j) dmma_884(acc[j][0], acc[j][1], j <= ra ? a0 : a1, H[boff[j] + k0]);
+    }
+    __syncthreads();  // H free for the next half
+  }
+  PROBE(59);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 17; ++j) {
+    const int ti = j <= ra ? ra : rb, tk = j <= ra ? j : j - ra - 1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) s[(8 * ti + g) + (8 * tk + 2 * tq + q) * LDS] += acc[j][q];
+  }
+  __syncthreads();
+  PROBE(60);
+  }
+  PROBE(61);
   trace_end(tr);
 }
 
@@ -778,13 +959,17 @@ cudaError_t configure_potf2() {
   cudaError_t e = cudaFuncSetAttribute(k_potf2_base, attr, (int)P2<kBaseMax>::SMEM);
   if (e != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_potf2_node128, attr, node128_smem())) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_potf2_node256, attr, (int)Node256::SMEM)) != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_potf2_base64, attr, (int)P2<64>::SMEM);
 }
 
 cudaError_t launch_potf2(double* A, int64_t ld, int layout, int n, int* d_info, int info_base, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (n > kPotf2Max) return cudaErrorInvalidValue;
-  if (potf2_use_regs(n)) {
+  if (n > kBaseMax) {
+    k_potf2_node256<<<1, Node256::TH, Node256::SMEM, st>>>(A, ld, layout | (copy_pairs() ? 0x100 : 0), n, d_info,
+                                                            info_base, g_launch_trace);
+  } else if (potf2_use_regs(n)) {
     switch ((n + 7) / 8) {
       case 1: k_potf2_reg<1><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;
       case 2: k_potf2_reg<2><<<1, 32, 0, st>>>(A, ld, layout, n, d_info, info_base, g_launch_trace); break;

@@ -25,6 +25,7 @@
 #include "chol_regs.cuh"
 #include "common.cuh"
 #include "kernels.h"
+#include "trsm_regs.cuh"
 
 namespace relapack {
 
@@ -312,93 +313,11 @@ __global__ void __launch_bounds__(TF<NW>::THREADS, 8 / NW)
 // holds only the three L blocks (104 KB) and a CTA covers 8 * RG * NW rows —
 // twice the rows per SM of the shared-memory slab at the same per-warp chain
 // (the RG groups' substitution chains interleave in one instruction stream).
-#ifndef RELAPACK_TRSM_MASKL
-#define RELAPACK_TRSM_MASKL 1
-#endif
-#ifndef RELAPACK_TRSM_SPLITACC
-#define RELAPACK_TRSM_SPLITACC 1
-#endif
-
 template <int NW, int RG>
 struct TRG {
   static constexpr int ROWS = 8 * RG * NW, THREADS = 32 * NW;
   static constexpr size_t SMEM = sizeof(double) * (3 * (size_t)kFC * kFLdL + 2 * kFC);
 };
-
-// Solve the 64 columns of chunk cb (tiles 8cb .. 8cb+7) against its diagonal
-// block sLd (1/L_jj in sRd), sub-block by sub-block, for every row group.
-template <int RG, int CB, int NT>
-__device__ __forceinline__ void solve_chunk_reg(double (&xs)[RG][NT][2], const double* sLd, const double* sRd,
-                                                int lane, int g, int tq) {
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    double l0[8], l1[8], rc[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-#if RELAPACK_TRSM_MASKL
-      // L(8s+2t, 8s+c), L(8s+2t+1, 8s+c): zero above the diagonal, not loaded
-      l0[c] = 2 * tq > c ? sLd[(8 * s + 2 * tq) * kFLdL + 8 * s + c] : 0.0;
-      l1[c] = 2 * tq + 1 > c ? sLd[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c] : 0.0;
-#else
-      l0[c] = sLd[(8 * s + 2 * tq) * kFLdL + 8 * s + c];      // L(8s+2t,   8s+c), 0 unless 2t > c
-      l1[c] = sLd[(8 * s + 2 * tq + 1) * kFLdL + 8 * s + c];  // L(8s+2t+1, 8s+c)
-#endif
-      rc[c] = sRd[8 * s + c];
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-#pragma unroll
-      for (int r = 0; r < RG; ++r) {
-        double& x0 = xs[r][8 * CB + s][0];
-        double& x1 = xs[r][8 * CB + s][1];
-        const double xj = __shfl_sync(0xffffffffu, (c & 1) ? x1 : x0, (lane & ~3) | (c >> 1)) * rc[c];
-        x0 -= xj * l0[c];
-        x1 -= xj * l1[c];
-        if (tq == (c >> 1)) {
-          if (c & 1)
-            x1 = xj;
-          else
-            x0 = xj;
-        }
-      }
-    }
-#if RELAPACK_TRSM_SPLITACC
-    // the next sub-block's tile first, its two k-halves into separate
-    // accumulators (two independent DMMAs instead of a dependent pair: the
-    // next substitution waits ~one DMMA latency less)
-    if (s + 1 < 8) {
-#pragma unroll
-      for (int r = 0; r < RG; ++r) {
-        double a[2];
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) a[ks] = -tile_frag(xs[r][8 * CB + s][0], xs[r][8 * CB + s][1], ks, g, tq);
-        double h0 = 0.0, h1 = 0.0;
-        dmma_884(xs[r][8 * CB + s + 1][0], xs[r][8 * CB + s + 1][1], a[0], sLd[(8 * (s + 1) + g) * kFLdL + 8 * s + tq]);
-        dmma_884(h0, h1, a[1], sLd[(8 * (s + 1) + g) * kFLdL + 8 * s + 4 + tq]);
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-          for (int s2 = s + 2; s2 < 8; ++s2)
-            dmma_884(xs[r][8 * CB + s2][0], xs[r][8 * CB + s2][1], a[ks],
-                     sLd[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
-        xs[r][8 * CB + s + 1][0] += h0;
-        xs[r][8 * CB + s + 1][1] += h1;
-      }
-    }
-#else
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-#pragma unroll
-      for (int r = 0; r < RG; ++r) {
-        const double a = -tile_frag(xs[r][8 * CB + s][0], xs[r][8 * CB + s][1], ks, g, tq);  // -X_s[g][4ks + tq]
-#pragma unroll
-        for (int s2 = s + 1; s2 < 8; ++s2)
-          dmma_884(xs[r][8 * CB + s2][0], xs[r][8 * CB + s2][1], a, sLd[(8 * s2 + g) * kFLdL + 8 * s + 4 * ks + tq]);
-      }
-    }
-#endif
-  }
-}
 
 template <int NW, int RG, int NC>
 __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
@@ -442,23 +361,13 @@ __global__ void __launch_bounds__(TRG<NW, RG>::THREADS, 1)
   finish_L_all<NW>(sL, sRinv, t);
   __syncthreads();
   TPROBE(1);
-  solve_chunk_reg<RG, 0, NT>(xs, sL, sRinv, lane, g, tq);
+  solve_chunk_regs<RG, 0, NT, kFLdL, 1>(xs, sL, sRinv, lane, g, tq);
   TPROBE(2);
   if (NC == 2 && t > kFC) {  // (NC == 1 instances never get here: t <= 64)
     // X_1 -= X_0 L_{1,0}^T (A fragments of X_0 from the quads, B from block 2)
-    const double* sLb = sL + 2 * kFC * kFLdL;
-#pragma unroll
-    for (int k0 = 0; k0 < kFC; k0 += 4) {
-#pragma unroll
-      for (int r = 0; r < RG; ++r) {
-        const double a = -tile_frag(xs[r][k0 >> 3][0], xs[r][k0 >> 3][1], (k0 >> 2) & 1, g, tq);
-#pragma unroll
-        for (int sb = 0; sb < 8; ++sb)
-          dmma_884(xs[r][(8 + sb) % NT][0], xs[r][(8 + sb) % NT][1], a, sLb[(8 * sb + g) * kFLdL + k0 + tq]);
-      }
-    }
+    update_chunk1_regs<RG, NT, kFLdL, 1>(xs, sL + 2 * kFC * kFLdL, g, tq);
     TPROBE(3);
-    if constexpr (NC == 2) solve_chunk_reg<RG, 1, NT>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
+    if constexpr (NC == 2) solve_chunk_regs<RG, 1, NT, kFLdL, 1>(xs, sL + kFC * kFLdL, sRinv + kFC, lane, g, tq);
     TPROBE(4);
   }
   pdl_trigger();

@@ -111,13 +111,13 @@ def test_argument_errors_without_gpu():
 
 def test_knobs():
     old = rl.get_crossover()
-    assert old == 128  # default: the in-CTA 128-node base case
+    assert old == 128  # default: the in-CTA 128-node base case (256-node kernel opt-in)
     with pytest.raises(ValueError):
         rl.set_crossover(8)
     with pytest.raises(ValueError):
         rl.set_split_tile(48)
     with pytest.raises(ValueError):
-        rl.set_crossover(160)  # the base case lives in one SM's shared memory: c <= 128
+        rl.set_crossover(300)  # the base case lives in one SM's shared memory: c <= 256
     rl.set_crossover(48)
     assert rl.get_crossover() == 48
     rl.set_crossover(old)

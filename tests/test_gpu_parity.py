@@ -516,6 +516,70 @@ def test_node128_info(k):
     assert info == rinfo == k + 1
 
 
+# ---------------------------------------------------------------- 128 < n <= 256 base case (in-CTA 256-node)
+@pytest.mark.parametrize("n", [129, 136, 160, 191, 192, 200, 255, 256])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_node256_base_case(n, uplo):
+    """The 256-node kernel (A11 node, register TRSM, K-halved SYRK, A22 node in one CTA)."""
+    old = rl.get_crossover()
+    rl.set_crossover(256)
+    try:
+        check_spd(gen.spd(n, 70 + n), uplo)
+        A, L = gen.integer_L(n, 5 + n)
+        G, info, _, _ = run_both(A, uplo)
+        assert info == 0
+        assert np.array_equal(lower_of(G, uplo), L)  # exact: integer factor, perfect-square pivots
+    finally:
+        rl.set_crossover(old)
+
+
+@pytest.mark.parametrize("n,lda", [(256, 259), (200, 203), (250, 256), (129, 130)])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_node256_lda(n, lda, uplo):
+    """Odd / padded lda (element copies instead of 16-byte pairs); padding untouched."""
+    old = rl.get_crossover()
+    rl.set_crossover(256)
+    try:
+        check_spd(gen.spd(n, 17, lda=lda), uplo)
+    finally:
+        rl.set_crossover(old)
+
+
+@pytest.mark.parametrize("k", [0, 5, 64, 127, 128, 129, 191, 200, 255])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_node256_info(k, uplo):
+    """A negated diagonal at k is the first failed pivot (closed form R11), in A11's
+    or in A22's half of the node."""
+    n = 256
+    A = np.array(gen.spd(n, 9), order="F")
+    A[k, k] = -A[k, k]
+    old = rl.get_crossover()
+    rl.set_crossover(256)
+    try:
+        _, info, _, rinfo = run_both(A, uplo)
+    finally:
+        rl.set_crossover(old)
+    assert info == rinfo == k + 1
+
+
+@pytest.mark.parametrize("n", [256, 1000, 2048])
+def test_node256_vs_node128_plans(n):
+    """Crossover 256 (one launch per 256-node) and 128 (node-128, TRSM, SYRK,
+    node-128) factor the same matrix to within the parity tolerance of each other."""
+    A = gen.spd(n, 77)
+    old = rl.get_crossover()
+    try:
+        out = []
+        for c in (128, 256):
+            rl.set_crossover(c)
+            dA = to_dev(A)
+            assert rl.dpotrf(dA, "L") == 0
+            out.append(np.tril(dA.cpu().numpy()))
+    finally:
+        rl.set_crossover(old)
+    assert floored_rel_err(out[1], out[0], A) <= TOL
+
+
 # ---------------------------------------------------------------- extreme exponents
 @pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("n", [100, 300, 1031])
