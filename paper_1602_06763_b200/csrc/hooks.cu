@@ -38,12 +38,12 @@ extern "C" {
 
 int relapack_update_test(int la, int lb, int lc, int tri, int M, int N, int K, double alpha, double* C, int64_t ldc,
                          const double* A, int64_t lda, const double* B, int64_t ldb, int tile, int ksplit,
-                         int allow_tma, relapack_stream_t stream, int* chosen) {
+                         int allow_tma, int max_ctas, relapack_stream_t stream, int* chosen) {
   if (la < 0 || la > 1 || lb < 0 || lb > 1 || lc < 0 || lc > 1 || tri < 0 || tri > 2 || M < 0 || N < 0 || K < 0)
     return -1;
   if (tri && M != N) return -1;
   if (tile != 0 && tile != 32 && tile != 64 && tile != 128) return -1;
-  if (ksplit < 0 || ksplit > 16) return -1;
+  if (ksplit < 0 || ksplit > 16 || max_ctas < 0) return -1;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = configure_kernels();
   if (e != cudaSuccess) return cuda_fail(e, "configure");
@@ -53,6 +53,7 @@ int relapack_update_test(int la, int lb, int lc, int tri, int M, int N, int K, d
   UpdateOp u{};
   init_update(u, C, ldc, lc, A, lda, la, B, ldb, lb, M, N, K, alpha, tri, tile, allow_tma != 0);
   u.args.d_info = s.d_info;
+  u.max_ctas = max_ctas;
   int ks = ksplit;
   if (ks == 0) ks = update_ksplit_for(u.args.M, u.args.N, K, u.args.tri != 0, u.tile);
   if (ks > 1) {

@@ -388,10 +388,20 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
   __shared__ uintptr_t s_base;
   if (threadIdx.x == 0) s_base = ks.base;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms) by an integer offset from the
+  // __shared__ array, so the compiler keeps the shared address space: the
+  // fragment reads are LDS with 32-bit addresses (rounding the pointer through
+  // uintptr_t made them generic LD.E with 64-bit address arithmetic per load)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nwork = args.ntiles * args.ksplit;
   for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
-    if (work != (int)blockIdx.x) __syncthreads();  // previous item fully drained (smem, barriers)
+    if (work != (int)blockIdx.x) {
+      // previous item fully drained (smem, barriers); its generic-proxy
+      // accesses of the ring (fragment reads, the epilogue's staging tile)
+      // are ordered before this item's TMA writes into the same bytes
+      fence_proxy_async_smem();
+      __syncthreads();
+    }
     update_item<LA, LB, LAYOUT, USE_TMA, TBM, GM>(&tmA, &tmB, args, smem, work, work + (int)gridDim.x >= nwork,
                                                   &s_base);
   }

@@ -53,7 +53,7 @@ def _rand(shape, seed, stream):
     return g.uniform(-1.0, 1.0, size=shape)
 
 
-def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, odd=False, seed=7):
+def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, odd=False, seed=7, ctas=0):
     A = _rand((M, K), seed, 1)
     B = A.copy() if (tri and seed % 2 == 0 and M == N) else _rand((N, K), seed, 2)
     C0 = _rand((M, N), seed, 3) * 4.0
@@ -61,7 +61,7 @@ def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, 
     tB, _ = _operand(B, lb, pad)
     tC, bufC = _operand(C0, lc, pad)
     before = bufC.clone()
-    chosen = rl.update_test(tC, tA, tB, alpha=alpha, tri=tri, tile=tile, ksplit=ksplit, tma=tma)
+    chosen = rl.update_test(tC, tA, tB, alpha=alpha, tri=tri, tile=tile, ksplit=ksplit, tma=tma, ctas=ctas)
     torch.cuda.synchronize()
     Cg = tC.cpu().numpy()
     # oracle: C -= A' B^T with A' = -alpha A (alpha a power of two: exact scaling)
@@ -89,6 +89,22 @@ def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, 
 
 SIZES = (1, 7, 63, 65, 129)
 HOT = ((0, 0, 0), (1, 1, 1))  # the factorization's (la, lb, lc) for uplo L / U
+
+
+@pytest.mark.parametrize("lay", HOT)
+@pytest.mark.parametrize("tile", (64, 128))
+@pytest.mark.parametrize("tma", (True, False))
+@pytest.mark.parametrize("ctas,ksplit", [(3, 1), (7, 1), (5, 3)])
+def test_update_persistent_ctas(lay, tile, tma, ctas, ksplit):
+    """Persistent CTAs (the plan's CTA-capped deferred updates): each CTA runs
+    several (tile, split) items through the same shared-memory ring, the TMA of
+    an item writing the bytes the previous item's fragment reads and epilogue
+    staging used (generic -> async proxy, fenced).  GEMM and SYRK."""
+    la, lb, lc = lay
+    for tri in (0, 1):
+        M = N = 3 * tile + 17
+        chosen = _run_update(M, N, 200, la, lb, lc, tri, tile, tma, ksplit, ctas=ctas, seed=11 + tri)
+        assert chosen[0] == tile and chosen[2] == ksplit
 
 
 @pytest.mark.parametrize("lay", HOT)
