@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(BC<NMAX, LAYOUT>::WPC * 32, BC<NMAX, LAYOUT>::
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int r = 8 * i + g, c = 8 * k + 2 * t + q;
-          if (r < n && c < n && r >= c) Ak[8 * i * rs + q * cs] = v[T::id(i, k)][q];
+          if (r < n && c < n && r >= c) __stcs(Ak + 8 * i * rs + q * cs, v[T::id(i, k)][q]);  // st.global.cs: streamed out, not re-read
         }
     };
 #if RELAPACK_BATCH_MODE == 1  // tools/microbench only: memory phases alone
