@@ -347,7 +347,10 @@ RELAPACK_API int relapack_xprofile_records(int max, double* out);
  *   operand path (it is also taken when a base is not 16-byte aligned or an ld
  *   is odd).  max_ctas > 0 caps the grid: each CTA then processes several
  *   (tile, split) work items in turn (the persistent launch the plan uses for
- *   its deferred updates).  chosen (host, 3 ints, may be NULL) receives (tile, used TMA,
+ *   its deferred updates).  full_items > 0 with a forced ksplit > 1 splits
+ *   only the tiles [full_items, ntiles) (the plan's tail split of a big
+ *   grid's last partial wave); with ksplit 0 the size rule may choose a tail
+ *   split itself.  chosen (host, 3 ints, may be NULL) receives (tile, used TMA,
  *   ksplit).  Returns 0, -1 (bad argument) or <= -1000 (CUDA error).
  * relapack_trsm_test — K5 (§8a a3 base): B(m x t) := B L^{-T} (L the t x t lower
  *   L-view block at L, both in `layout`).  variant 0 = the plan's dispatch,
@@ -359,8 +362,8 @@ RELAPACK_API int relapack_xprofile_records(int max, double* out);
  */
 RELAPACK_API int relapack_update_test(int la, int lb, int lc, int tri, int M, int N, int K, double alpha, double* C,
                                       int64_t ldc, const double* A, int64_t lda, const double* B, int64_t ldb, int tile,
-                                      int ksplit, int allow_tma, int max_ctas, relapack_stream_t stream,
-                                      int* chosen);
+                                      int ksplit, int allow_tma, int max_ctas, int full_items,
+                                      relapack_stream_t stream, int* chosen);
 RELAPACK_API int relapack_trsm_test(int layout, int m, int t, const double* L, int64_t ldl, double* B, int64_t ldb,
                                     int variant, relapack_stream_t stream);
 RELAPACK_API int relapack_potf2_test(int layout, int n, double* A, int64_t lda, int* info, relapack_stream_t stream);

@@ -107,7 +107,8 @@ def lib():
         L.relapack_plan_schedule.restype = c_int
         i64 = ctypes.c_int64
         L.relapack_update_test.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_double, c_void_p, i64,
-                                           c_void_p, i64, c_void_p, i64, c_int, c_int, c_int, c_int, c_void_p, ip]
+                                           c_void_p, i64, c_void_p, i64, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                           ip]
         L.relapack_update_test.restype = c_int
         L.relapack_trsm_test.argtypes = [c_int, c_int, c_int, c_void_p, i64, c_void_p, i64, c_int, c_void_p]
         L.relapack_trsm_test.restype = c_int
@@ -355,10 +356,11 @@ def _block_args(X):
 
 
 def update_test(C, A, B, alpha: float = -1.0, tri: int = 0, tile: int = 0, ksplit: int = 0, tma: bool = True,
-                ctas: int = 0, stream=None):
+                ctas: int = 0, full: int = 0, stream=None):
     """Kernel test hook (K3/K4): C += alpha A B^T on the tri part of C (0 all, 1 lower, 2 upper).
     C: (M, N), A: (M, K), B: (N, K) float64 CUDA tensors, each column- or row-major (its layout).
-    ctas > 0 caps the grid (persistent CTAs, several work items each).
+    ctas > 0 caps the grid (persistent CTAs, several work items each); full > 0 with
+    ksplit > 1 splits only the tiles [full, ntiles) (tail split).
     Returns (tile, used_tma, ksplit) the launch used."""
     import torch
 
@@ -373,7 +375,7 @@ def update_test(C, A, B, alpha: float = -1.0, tri: int = 0, tile: int = 0, kspli
     chosen = (ctypes.c_int * 3)()
     r = lib().relapack_update_test(la, lb, lc, tri, M, N, K, float(alpha), ctypes.c_void_p(pc), ldc,
                                    ctypes.c_void_p(pa), lda, ctypes.c_void_p(pb), ldb, tile, ksplit, int(tma),
-                                   int(ctas), ctypes.c_void_p(st.cuda_stream), chosen)
+                                   int(ctas), int(full), ctypes.c_void_p(st.cuda_stream), chosen)
     if r != 0:
         raise RelapackError(f"relapack_update_test failed ({r}): {last_error()}")
     return tuple(chosen)

@@ -304,10 +304,13 @@ cudaError_t setup_splitk_ops(const std::vector<PlanOp>& ops, std::vector<UpdateO
   for (size_t i = 0; i < nops; ++i) {
     if (ops[i].kind != OP_GEMM && ops[i].kind != OP_SYRK) continue;
     UpdateArgs& a = upd[i].args;
-    const int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, upd[i].tile, ops[i].kind == OP_SYRK && !ops[i].deferred);
+    int ks = update_ksplit_for(a.M, a.N, a.K, a.tri, upd[i].tile, ops[i].kind == OP_SYRK && !ops[i].deferred);
+    int full = 0;
+    if (ks <= 1) ks = update_tail_split(a.ntiles, a.K, upd[i].tile, upd[i].max_ctas, &full);
     if (ks <= 1) continue;
     a.ksplit = ks;
-    const int64_t e = update_ws_elems(a.M, a.N, a.tri, upd[i].tile, ks);
+    a.full_items = full;
+    const int64_t e = update_ws_elems(a.M, a.N, a.tri, upd[i].tile, ks, full);
     ws = e > ws ? e : ws;
     cnt = a.ntiles > cnt ? a.ntiles : cnt;
     int s = -1;

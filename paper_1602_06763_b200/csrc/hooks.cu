@@ -38,12 +38,12 @@ extern "C" {
 
 int relapack_update_test(int la, int lb, int lc, int tri, int M, int N, int K, double alpha, double* C, int64_t ldc,
                          const double* A, int64_t lda, const double* B, int64_t ldb, int tile, int ksplit,
-                         int allow_tma, int max_ctas, relapack_stream_t stream, int* chosen) {
+                         int allow_tma, int max_ctas, int full_items, relapack_stream_t stream, int* chosen) {
   if (la < 0 || la > 1 || lb < 0 || lb > 1 || lc < 0 || lc > 1 || tri < 0 || tri > 2 || M < 0 || N < 0 || K < 0)
     return -1;
   if (tri && M != N) return -1;
   if (tile != 0 && tile != 32 && tile != 64 && tile != 128) return -1;
-  if (ksplit < 0 || ksplit > 16 || max_ctas < 0) return -1;
+  if (ksplit < 0 || ksplit > 16 || max_ctas < 0 || full_items < 0) return -1;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = configure_kernels();
   if (e != cudaSuccess) return cuda_fail(e, "configure");
@@ -55,10 +55,16 @@ int relapack_update_test(int la, int lb, int lc, int tri, int M, int N, int K, d
   u.args.d_info = s.d_info;
   u.max_ctas = max_ctas;
   int ks = ksplit;
-  if (ks == 0) ks = update_ksplit_for(u.args.M, u.args.N, K, u.args.tri != 0, u.tile);
+  int full = full_items;
+  if (ks == 0) {
+    ks = update_ksplit_for(u.args.M, u.args.N, K, u.args.tri != 0, u.tile);
+    if (ks <= 1) ks = update_tail_split(u.args.ntiles, K, u.tile, max_ctas, &full, true);
+  }
+  if (ks > 1 && full >= u.args.ntiles) return -1;
   if (ks > 1) {
     u.args.ksplit = ks;
-    const int64_t wse = update_ws_elems(u.args.M, u.args.N, u.args.tri != 0, u.tile, ks);
+    u.args.full_items = full;
+    const int64_t wse = update_ws_elems(u.args.M, u.args.N, u.args.tri != 0, u.tile, ks, full);
     if ((e = cudaMalloc(&s.ws, wse * sizeof(double))) != cudaSuccess) return cuda_fail(e, "hook ws");
     if ((e = cudaMalloc(&s.cnt, u.args.ntiles * sizeof(int))) != cudaSuccess) return cuda_fail(e, "hook cnt");
     if ((e = cudaMemsetAsync(s.cnt, 0, u.args.ntiles * sizeof(int), st)) != cudaSuccess) return cuda_fail(e, "cnt");

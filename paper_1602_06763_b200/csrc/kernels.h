@@ -35,7 +35,13 @@ struct UpdateArgs {
   // counters[tile], self-resetting) sums them in split order and applies C -=.
   int ksplit;         // 1 = no split
   int ntiles;
-  double* ws;         // ksplit * ntiles * tile^2 doubles
+  // tail split (ksplit > 1 and full_items > 0): tiles [0, full_items) run
+  // whole, one work item each; only the last partial wave's tiles
+  // [full_items, ntiles) are split ksplit ways (update_tail_split).  Work
+  // items: full_items + (ntiles - full_items) * ksplit; the partials of tail
+  // tile t at ws + (split * (ntiles - full_items) + t - full_items) * tile^2
+  int full_items;
+  double* ws;         // ksplit * (ntiles - full_items) * tile^2 doubles
   int* counters;      // ntiles ints, zero between launches
   // pointer-independent plan graph: the A / B descriptors in global memory
   // (rebased per run by the plan's first node); C / A / B above are then byte
@@ -67,7 +73,14 @@ int update_tile_for(int M, int N, int K, int tri);
 // chain: the update sits on the base-case chain (non-deferred SYRK): latency
 // over efficiency, down to 2 k-tiles per split
 int update_ksplit_for(int M, int N, int K, int tri, int tile, bool chain = false);
-int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit);
+int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit, int full_items = 0);
+// Tail split of a big-grid update (tile 128, ntiles over several waves of
+// `slots` concurrent CTAs: 148, or the launch's CTA cap): returns the split
+// factor s (2..4) for the last partial wave's r tiles when r * s fits one wave
+// and every piece keeps >= 8 k-tiles, with *full_items = ntiles - r; else 1.
+// Plans apply it only with RELAPACK_TAIL_SPLIT=1 (measured neutral in the DAG);
+// always = true ignores the knob (kernel test hook).
+int update_tail_split(int ntiles, int K, int tile, int max_ctas, int* full_items, bool always = false);
 
 // ---- K1 base-case potf2 (potf2.cu) ----
 // Factor the n x n L-view block at A (n <= kPotf2Max) in shared memory; on a

@@ -182,7 +182,15 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
 
-  const int tile = work % args.ntiles, split = work / args.ntiles;
+  // work item -> (tile, split): uniform split-K (full_items = 0) is
+  // split-major over all tiles; a tail split runs tiles [0, full_items) whole
+  // and splits only the rest
+  const int ntail = args.ntiles - args.full_items;
+  const bool whole = work < args.full_items;
+  const int tail_j = work - args.full_items;
+  const int tile = whole ? work : args.full_items + tail_j % ntail;
+  const int split = whole ? 0 : tail_j / ntail;
+  const int ksplit = whole ? 1 : args.ksplit;
   int tm, tn;
   if (args.tri) {
     tri_index(tile, tm, tn);  // tm >= tn: lower tile
@@ -209,7 +217,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
   const int wm = warp % C::WGM, wn = warp / C::WGM;
   const int g = lane >> 2, t = lane & 3;
   const int KT_all = (args.K + BK - 1) / BK;
-  const int kt_per = (KT_all + args.ksplit - 1) / args.ksplit;
+  const int kt_per = (KT_all + ksplit - 1) / ksplit;
   const int kt0 = split * kt_per;
   const int KT = max(0, min(KT_all, kt0 + kt_per) - kt0);  // k-tiles of this split, from kt0
 
@@ -294,23 +302,23 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
         sC[LAYOUT == kLayoutN ? jl * C::CPAD + il : il * C::CPAD + jl] = acc[mt][nt][c];
       }
   __syncthreads();
-  if (args.ksplit > 1) {
+  if (ksplit > 1) {
     // deterministic split-K reduction: publish this split's partial tile; the
     // last CTA of the tile sums all partials in split order 0..ksplit-1.
     constexpr int T2 = TBM * TBM;
-    double* wsl = args.ws + ((int64_t)split * args.ntiles + tile) * T2;
+    double* wsl = args.ws + ((int64_t)split * ntail + (tile - args.full_items)) * T2;
     for (int e = threadIdx.x; e < T2; e += C::THREADS) wsl[e] = sC[(e / TBM) * C::CPAD + (e % TBM)];
     __threadfence();
     __syncthreads();
     __shared__ int s_last;
-    if (threadIdx.x == 0) s_last = atomicAdd(&args.counters[tile], 1) == args.ksplit - 1;
+    if (threadIdx.x == 0) s_last = atomicAdd(&args.counters[tile], 1) == ksplit - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
     // 4 elements x all splits in flight per thread, summed in split order
     constexpr int KSMAX = 16, EB = 4;
-    const int64_t sstride = (int64_t)args.ntiles * T2;
-    const double* wt = args.ws + (int64_t)tile * T2;
+    const int64_t sstride = (int64_t)ntail * T2;
+    const double* wt = args.ws + (int64_t)(tile - args.full_items) * T2;
     for (int e0 = threadIdx.x; e0 < T2; e0 += C::THREADS * EB) {
       double v[EB][KSMAX];
 #pragma unroll
@@ -318,7 +326,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
 #pragma unroll
         for (int sp = 0; sp < KSMAX; ++sp) {
           const int e = e0 + q * C::THREADS;
-          v[q][sp] = (sp < args.ksplit && e < T2) ? __ldcg(wt + sp * sstride + e) : 0.0;
+          v[q][sp] = (sp < ksplit && e < T2) ? __ldcg(wt + sp * sstride + e) : 0.0;
         }
 #pragma unroll
       for (int q = 0; q < EB; ++q) {
@@ -326,7 +334,7 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
         double sum = 0.0;
 #pragma unroll
         for (int sp = 0; sp < KSMAX; ++sp)
-          if (sp < args.ksplit) sum += v[q][sp];
+          if (sp < ksplit) sum += v[q][sp];
         if (e < T2) sC[(e / TBM) * C::CPAD + (e % TBM)] = sum;
       }
     }
@@ -393,7 +401,7 @@ __global__ void __launch_bounds__(Cfg<TBM>::THREADS, Cfg<TBM>::MIN_BLOCKS)
   // fragment reads are LDS with 32-bit addresses (rounding the pointer through
   // uintptr_t made them generic LD.E with 64-bit address arithmetic per load)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int nwork = args.ntiles * args.ksplit;
+  const int nwork = args.full_items + (args.ntiles - args.full_items) * args.ksplit;
   for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
     if (work != (int)blockIdx.x) {
       // previous item fully drained (smem, barriers); its generic-proxy
@@ -428,7 +436,7 @@ cudaError_t launch_combo(const UpdateOp& op, int grid, cudaStream_t st) {
 template <int TBM>
 cudaError_t launch_tbm(const UpdateOp& op, cudaStream_t st) {
   const UpdateArgs& a = op.args;
-  int grid = a.ntiles * a.ksplit;
+  int grid = a.full_items + (a.ntiles - a.full_items) * a.ksplit;
   if (op.max_ctas > 0 && grid > op.max_ctas) grid = op.max_ctas;  // persistent, leaves SMs to other streams
   const int combo = a.la * 4 + a.lb * 2 + a.layout;
   switch (combo) {
@@ -587,8 +595,37 @@ int update_ksplit_for(int M, int N, int K, int tri, int tile, bool chain) {
   return ks >= 2 ? ks : 1;
 }
 
-int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit) {
-  return ksplit > 1 ? (int64_t)ksplit * ntiles_of(M, N, tri, tile) * tile * tile : 0;
+int64_t update_ws_elems(int M, int N, int tri, int tile, int ksplit, int full_items) {
+  return ksplit > 1 ? (int64_t)ksplit * (ntiles_of(M, N, tri, tile) - full_items) * tile * tile : 0;
+}
+
+// RELAPACK_TAIL_SPLIT=1 turns the tail split on in the plans (off by
+// default: measured neutral inside the DAG, where concurrent launches already
+// fill the last wave's idle SMs — n = 16384 46.78-46.81 vs 46.76-46.77 ms,
+// n = 65536 2795-2796 vs 2793-2794 ms, tools/experiments/exp_tail.sh); the
+// kernel tests force it through the hook either way
+static bool tail_split_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("RELAPACK_TAIL_SPLIT");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+int update_tail_split(int ntiles, int K, int tile, int max_ctas, int* full_items, bool always) {
+  *full_items = 0;
+  if (!(always || tail_split_enabled()) || tile != 128) return 1;
+  const int slots = max_ctas > 0 && max_ctas < 148 ? max_ctas : 148;  // 128-tile CTAs: one per SM
+  if (ntiles <= slots) return 1;
+  const int r = ntiles % slots;
+  if (r == 0) return 1;
+  const int KT = (K + BK - 1) / BK;
+  int s = slots / r;
+  s = s < 4 ? s : 4;
+  while (s >= 2 && KT / s < 8) --s;
+  if (s < 2) return 1;
+  *full_items = ntiles - r;
+  return s;
 }
 
 void init_update(UpdateOp& u, double* C, int64_t ldc, int lc, const double* A, int64_t lda, int la, const double* B,
@@ -627,6 +664,7 @@ void init_update(UpdateOp& u, double* C, int64_t ldc, int lc, const double* A, i
   a.B = B;
   a.ldb = ldb;
   a.ksplit = 1;
+  a.full_items = 0;
   u.tile = tile > 0 ? tile : update_tile_for(M, N, K, tri != 0);
   a.tiles_m = (M + u.tile - 1) / u.tile;
   const int tiles_n = (N + u.tile - 1) / u.tile;

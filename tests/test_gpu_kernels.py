@@ -53,7 +53,7 @@ def _rand(shape, seed, stream):
     return g.uniform(-1.0, 1.0, size=shape)
 
 
-def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, odd=False, seed=7, ctas=0):
+def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, odd=False, seed=7, ctas=0, full=0):
     A = _rand((M, K), seed, 1)
     B = A.copy() if (tri and seed % 2 == 0 and M == N) else _rand((N, K), seed, 2)
     C0 = _rand((M, N), seed, 3) * 4.0
@@ -61,7 +61,7 @@ def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, 
     tB, _ = _operand(B, lb, pad)
     tC, bufC = _operand(C0, lc, pad)
     before = bufC.clone()
-    chosen = rl.update_test(tC, tA, tB, alpha=alpha, tri=tri, tile=tile, ksplit=ksplit, tma=tma, ctas=ctas)
+    chosen = rl.update_test(tC, tA, tB, alpha=alpha, tri=tri, tile=tile, ksplit=ksplit, tma=tma, ctas=ctas, full=full)
     torch.cuda.synchronize()
     Cg = tC.cpu().numpy()
     # oracle: C -= A' B^T with A' = -alpha A (alpha a power of two: exact scaling)
@@ -89,6 +89,30 @@ def _run_update(M, N, K, la, lb, lc, tri, tile, tma, ksplit, alpha=-1.0, pad=0, 
 
 SIZES = (1, 7, 63, 65, 129)
 HOT = ((0, 0, 0), (1, 1, 1))  # the factorization's (la, lb, lc) for uplo L / U
+
+
+@pytest.mark.parametrize("lay", HOT)
+@pytest.mark.parametrize("tma", (True, False))
+@pytest.mark.parametrize("full,ksplit,ctas", [(10, 2, 0), (13, 3, 0), (1, 4, 0), (9, 2, 4)])
+def test_update_tail_split(lay, tma, full, ksplit, ctas):
+    """Tail split: tiles [0, full) whole, the rest split ksplit ways (the plan's
+    last-partial-wave split), also under a CTA cap; GEMM (16 tiles) and SYRK
+    (10 lower tiles) on ragged 128-tiles."""
+    la, lb, lc = lay
+    for tri in (0, 1):
+        M = N = 3 * 128 + 17
+        f = full if tri == 0 else min(full, 9)  # 16 GEMM tiles, 10 SYRK tiles
+        chosen = _run_update(M, N, 300, la, lb, lc, tri, 128, tma, ksplit, ctas=ctas, full=f, seed=21 + tri)
+        assert chosen[0] == 128 and chosen[2] == ksplit
+
+
+@pytest.mark.parametrize("lay", HOT)
+def test_update_tail_split_size_rule(lay):
+    """The size rule's own tail split: 169 tiles of 128 = one wave of 148 plus
+    21, split 4 ways (K = 512: 8 k-tiles a piece)."""
+    la, lb, lc = lay
+    chosen = _run_update(13 * 128, 13 * 128, 512, la, lb, lc, 0, 128, True, 0, seed=5)
+    assert chosen[0] == 128 and chosen[2] == 4
 
 
 @pytest.mark.parametrize("lay", HOT)
