@@ -270,6 +270,13 @@ __device__ __forceinline__ void update_item(const CUtensorMap* tmA_p, const CUte
       mbar_wait(&full[s], (kt / STAGES) & 1);
       const uint8_t* sa = smem + s * C::STAGE_BYTES;
       mma_stage<LA, LB, TBM>(acc, sa, sa + C::TILE_BYTES, wm, wn, g, t);
+      // release the stage to the producer's next TMA: the fragment reads are
+      // generic-proxy LDS and the refill an async-proxy write of the same
+      // bytes, so each lane fences the proxies first (which also waits for its
+      // reads to be performed: the scheduler otherwise issues the arrive right
+      // behind the last LDS, before its data is back — a WAR race that
+      // corrupted ~half of the n = 16384 replays, tools/race_check.py)
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
