@@ -25,6 +25,11 @@ import sys
 import threading
 import time
 
+# NCCL writes its version banner (NCCL_DEBUG=VERSION and above) to stdout, which
+# would put a non-JSON line before the one JSON line rank 0 prints: route NCCL's
+# debug output to a file unless the caller chose one
+os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/relapack_nccl_debug.%h.%p.log")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
