@@ -305,8 +305,10 @@ RELAPACK_API int relapack_trace_read(int max, double* out);
  *   2 n, 3 A, 4 lda, 5 nb.  DEVICE A.
  * relapack_xplan_count — host-only: the launch count of one of these plans
  *   (op 0 trtri, 1 trtri_blocked (nb), 2 lauum, 3 potri, 4 potrs (nrhs = nb),
- *   5 getrf (n x n)), their kinds (0 gemm, 1 tri, 2 trti2, 3 lauu2, 4 potf2,
- *   5 getf2, 6 laswp, 7 check) and the summed leading-term flops.
+ *   5 getrf (n x n), 6 getrf with lookahead (n x n, 16-CTA cluster panels,
+ *   window nb; -1 if n exceeds the cluster panel's rows)), their kinds (0 gemm,
+ *   1 tri, 2 trti2, 3 lauu2, 4 potf2, 5 getf2, 6 laswp, 7 check, 8 perm) and
+ *   the summed leading-term flops.
  */
 RELAPACK_API void relapack_dtrtri(const char* uplo, const char* diag, const int* n, double* A, const int* lda,
                                   int* info);

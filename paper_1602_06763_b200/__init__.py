@@ -507,8 +507,9 @@ def dpotrf_blocked(A, nb: int, uplo: str = "L", stream=None) -> int:
 
 
 def xplan_count(op: str, n: int, nb: int = 0):
-    """Host-only: (launches, kinds, flops) of a §8(f) plan (op in trtri, trtri_blocked, lauum, potri, potrs, getrf)."""
-    code = {"trtri": 0, "trtri_blocked": 1, "lauum": 2, "potri": 3, "potrs": 4, "getrf": 5}[op]
+    """Host-only: (launches, kinds, flops) of a §8(f) plan (op in trtri, trtri_blocked, lauum, potri, potrs, getrf,
+    getrf_la — the lookahead getrf plan with window nb)."""
+    code = {"trtri": 0, "trtri_blocked": 1, "lauum": 2, "potri": 3, "potrs": 4, "getrf": 5, "getrf_la": 6}[op]
     fl = ctypes.c_double(0)
     cnt = lib().relapack_xplan_count(code, n, nb, None, 0, ctypes.byref(fl))
     if cnt < 0:

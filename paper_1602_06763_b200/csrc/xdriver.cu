@@ -35,6 +35,7 @@ struct XBuffers {
   int layout[2] = {kLayoutN, kLayoutN};  // logical -> memory layout of each buffer
   int* ipiv = nullptr;                   // buffer 2 (1-based pivots, indexed by row / column)
   int total_rows = 0, total_cols = 0;
+  int cl_size = 0;  // getrf: CTAs per cluster of the panel-only leaves (0: cooperative leaves)
 };
 
 struct XOperand {
@@ -64,6 +65,7 @@ struct XExec {
   void* poll_ws = nullptr;  // epoch-stamped exchange records (shared by the panels)
   int sms = 148;
   int cl_size = 0;  // getrf cluster panels: CTAs per cluster
+  int defer_ctas = 0;  // getrf lookahead: CTA cap of the deferred updates
   bool is_getrf = false, has_check = false;
   cudaGraphExec_t exec = nullptr;
   ~XExec() {
@@ -119,9 +121,18 @@ __global__ void k_xepilogue(int* d_info) {
   if (d_info[0] == 0 && d_info[1] != kIntMax) d_info[0] = d_info[1];
 }
 
+__global__ void k_xnop() {}
+
 cudaError_t launch_xop(const XExec& x, size_t i, cudaStream_t st) {
   const XOp& o = x.ops[i];
   const XBuffers& b = x.bufs;
+  // measurement only (wrong results): RELAPACK_GETRF_SKIP_DEFER=1 replaces the
+  // deferred lookahead pieces by empty kernels — the time of the chain alone
+  static const int skip_defer = getenv("RELAPACK_GETRF_SKIP_DEFER") ? atoi(getenv("RELAPACK_GETRF_SKIP_DEFER")) : 0;
+  if (o.defer && skip_defer) {
+    k_xnop<<<1, 32, 0, st>>>();
+    return cudaGetLastError();
+  }
   switch (o.kind) {
     case XK_GEMM:
       return launch_update(x.upd[i], st);
@@ -205,6 +216,29 @@ cudaError_t launch_xop(const XExec& x, size_t i, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+int env_int_x(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// getrf lookahead: the deferred updates (each a persistent grid capped below
+// the SM count) one at a time, in the order the chain first needs them, so
+// the SMs they leave free stay free for the windows.  An edge is only added
+// forwards in plan order (the capture creates nodes in that order).
+void serialize_deferred(const std::vector<XOp>& ops, std::vector<std::vector<int>>& deps) {
+  const size_t n = ops.size();
+  std::vector<int> first_use(n, kIntMax);
+  for (size_t j = 0; j < n; ++j)
+    for (int d : deps[j]) first_use[d] = std::min(first_use[d], (int)j);
+  std::vector<int> dg;
+  for (size_t i = 0; i < n; ++i)
+    if (ops[i].defer && ops[i].kind == XK_GEMM) dg.push_back((int)i);
+  std::stable_sort(dg.begin(), dg.end(), [&](int a, int b) { return first_use[a] < first_use[b]; });
+  if (env_int_x("RELAPACK_GETRF_SERIAL", 1) == 0) return;
+  for (size_t q = 1; q < dg.size(); ++q)
+    if (dg[q - 1] < dg[q]) deps[dg[q]].push_back(dg[q - 1]);
+}
+
 // Update descriptors, split-K slots (as the factorization's: two split-K
 // updates share a slot only if one is an ancestor of the other) and the
 // getf2 workspaces.
@@ -227,7 +261,8 @@ cudaError_t setup_exec(XExec& x, const std::vector<uint64_t>& anc) {
     UpdateOp& u = x.upd[i];
     init_update(u, C.p, C.ld, C.layout, A.p, A.ld, A.layout, B.p, B.ld, B.layout, o.m, o.n, o.k, o.alpha, o.tri);
     u.args.d_info = x.d_info;
-    const int ks = update_ksplit_for(u.args.M, u.args.N, u.args.K, u.args.tri != 0, u.tile);
+    if (o.defer) u.max_ctas = x.defer_ctas;  // persistent, leaves the window's SMs free
+    const int ks = o.defer ? 1 : update_ksplit_for(u.args.M, u.args.N, u.args.K, u.args.tri != 0, u.tile);
     if (ks <= 1) continue;
     u.args.ksplit = ks;
     ws = std::max(ws, update_ws_elems(u.args.M, u.args.N, u.args.tri != 0, u.tile, ks));
@@ -301,6 +336,13 @@ cudaError_t capture(const XExec& x, const std::vector<std::vector<int>>& deps, c
     if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &cur, &ncur)) != cudaSuccess) return e;
     if (ncur != 1) return cudaErrorStreamCaptureInvalidated;
     nodes[i] = cur[0];
+  }
+  bool any_defer = false;
+  for (const XOp& o : x.ops) any_defer |= o.defer != 0;
+  if (any_defer) {  // deferred pieces lowest, everything else (the windows' chain) highest
+    std::vector<char> cls(x.ops.size(), 0);
+    for (size_t i = 0; i < x.ops.size(); ++i) cls[i] = x.ops[i].defer ? 2 : 0;
+    if ((e = set_node_priorities(nodes, cls)) != cudaSuccess) return e;
   }
   want.clear();
   for (size_t i = 0; i < x.ops.size(); ++i)
@@ -393,11 +435,16 @@ int x_run(const std::string& key, const std::vector<XOp>& ops_in, const XBuffers
     p->bufs = bufs;
     p->is_getrf = is_getrf;
     p->has_check = has_check;
-    p->cl_size = is_getrf ? getf2_cluster_caps() : 0;
+    p->cl_size = is_getrf ? bufs.cl_size : 0;
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev);
     std::vector<std::vector<int>> deps;
     std::vector<uint64_t> anc;
     xplan_deps(p->ops, bufs.total_rows, deps, &anc);
+    {  // RELAPACK_GETRF_RESERVE < 0: deferred updates one tile per CTA (no cap; yield SMs tile by tile)
+      const int rs = env_int_x("RELAPACK_GETRF_RESERVE", 16);
+      p->defer_ctas = rs < 0 ? 0 : std::max(1, p->sms - std::max(p->cl_size, rs));
+    }
+    serialize_deferred(p->ops, deps);
     if ((e = setup_exec(*p, anc)) != cudaSuccess) return cuda_fail(e, "x workspace");
     if (graphs) {
       cudaGraph_t g = nullptr;
@@ -596,10 +643,20 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
   *info = 0;
   if (*m == 0 || *n == 0) return;
   XParams p = x_params();
-  p.getf2_cluster = getf2_cluster_caps();
   p.getrf_cols = *n;
   std::vector<XOp> ops;
-  xplan_getrf(ops, p, 0, 0, *m, *n, 0);
+  // lookahead plan (RELAPACK_GETRF_LA, window RELAPACK_GETRF_WINDOW): panel-only
+  // cluster leaves for every panel height, else the plain recursion
+  const int la = env_int_x("RELAPACK_GETRF_LA", 0);
+  const int cl = la ? getf2_cluster_size(env_int_x("RELAPACK_GETF2_CLUSTER", 16)) : 0;
+  if (la && cl > 0 && (*m + cl - 1) / cl <= kGetf2ClRows8) {
+    p.getf2_cluster = cl;
+    p.getrf_window = std::max(8, env_int_x("RELAPACK_GETRF_WINDOW", 256));
+    xplan_getrf_la(ops, p, *m, *n);
+  } else {
+    p.getf2_cluster = getf2_cluster_caps();
+    xplan_getrf(ops, p, 0, 0, *m, *n, 0);
+  }
   XBuffers b;
   b.base[0] = A;
   b.ld[0] = *lda;
@@ -607,8 +664,12 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
   b.ipiv = ipiv;
   b.total_rows = *m;
   b.total_cols = *n;
+  b.cl_size = p.getf2_cluster;
   const std::string key = "getrf m" + std::to_string(*m) + " n" + std::to_string(*n) + " ld" + std::to_string(*lda) +
-                          " A" + ptr_key(A) + " P" + ptr_key(ipiv) + params_key(p);
+                          " A" + ptr_key(A) + " P" + ptr_key(ipiv) + params_key(p) + " la" + std::to_string(la) +
+                          " w" + std::to_string(p.getrf_window) + " rs" +
+                          std::to_string(env_int_x("RELAPACK_GETRF_RESERVE", 16)) + " se" +
+                          std::to_string(env_int_x("RELAPACK_GETRF_SERIAL", 1));
   int r = x_run(key, ops, b, true, false, current_stream_or(nullptr), info);
   if (r != 0) *info = r;
 }
@@ -667,7 +728,7 @@ void relapack_xprofile_reset(void) {
 
 int relapack_xplan_count(int op, int n, int nb, int* kinds_out, int max_kinds, double* flops_out) {
   // host-only introspection of the §8(f) plans: op 0 trtri, 1 trtri_blocked,
-  // 2 lauum, 3 potri, 4 potrs (nrhs = nb), 5 getrf (square)
+  // 2 lauum, 3 potri, 4 potrs (nrhs = nb), 5 getrf (square), 6 getrf with lookahead (window nb)
   if (n < 0) return -1;
   XParams p;
   std::vector<XOp> ops;
@@ -678,6 +739,13 @@ int relapack_xplan_count(int op, int n, int nb, int* kinds_out, int max_kinds, d
     case 3: xplan_trtri(ops, p, 0, n, 0, 0); xplan_lauum(ops, p, 0, n, 0); break;
     case 4: xplan_potrs(ops, p, n, nb); break;
     case 5: xplan_getrf(ops, p, 0, 0, n, n, 0); break;
+    case 6:  // getrf lookahead plan, 16-CTA cluster leaves, window nb (0: 256)
+      p.getf2_cluster = 16;
+      p.getrf_cols = n;
+      if (nb > 0) p.getrf_window = nb;
+      if ((n + 15) / 16 > kGetf2ClRows8) return -1;
+      xplan_getrf_la(ops, p, n, n);
+      break;
     default: return -1;
   }
   double fl = 0.0;

@@ -911,58 +911,66 @@ __global__ void __launch_bounds__(T) k_getf2_clr(XGetf2ClArgs a) {
 #endif
 }
 
-// One panel's interchanges as a permutation.  Warp 0 composes the
-// transpositions (row k <-> p_k, k ascending, p_k >= k) on the affected rows:
-// lane l tracks row l < npiv (cont_lo: the row whose value ends there) and
-// extra slot l a pivot row >= npiv; then every warp moves whole columns.
+// The interchanges of up to 32 consecutive pivots (row k <-> p_k, k ascending,
+// p_k >= k, rows relative to the first pivot's row) as one permutation,
+// composed by one warp: lane l tracks row l < npiv (cont_lo: the row whose
+// value ends there) and extra slot l a pivot row >= npiv.  The moved rows go
+// to s_row / s_src (compacted); returns their count (all lanes).
+__device__ __forceinline__ int compose_pivots(const int* ipiv, int npiv, int base, int* s_row, int* s_src) {
+  const int lane = threadIdx.x & 31;
+  int cont_lo = lane, xrow = -1, xcont = -1, ne = 0;
+  const int mypiv = lane < npiv ? ipiv[lane] - base : lane;  // all pivots in one load
+  for (int k = 0; k < npiv; ++k) {
+    const int p = __shfl_sync(0xffffffffu, mypiv, k);
+    if (p == k) continue;
+    const int ck = __shfl_sync(0xffffffffu, cont_lo, k);
+    if (p < npiv) {
+      const int cp = __shfl_sync(0xffffffffu, cont_lo, p);
+      if (lane == k) cont_lo = cp;
+      if (lane == p) cont_lo = ck;
+    } else {
+      const unsigned mk = __ballot_sync(0xffffffffu, xrow == p);
+      int slot;
+      if (mk) {
+        slot = __ffs(mk) - 1;
+      } else {
+        slot = ne++;
+        if (lane == slot) {
+          xrow = p;
+          xcont = p;
+        }
+      }
+      const int cp = __shfl_sync(0xffffffffu, xcont, slot);
+      if (lane == k) cont_lo = cp;
+      if (lane == slot) xcont = ck;
+    }
+  }
+  const bool mv_lo = lane < npiv && cont_lo != lane, mv_x = xrow >= 0 && xcont != xrow;
+  const unsigned b_lo = __ballot_sync(0xffffffffu, mv_lo), b_x = __ballot_sync(0xffffffffu, mv_x);
+  const int n_lo = __popc(b_lo);
+  if (mv_lo) {
+    const int at = __popc(b_lo & ((1u << lane) - 1));
+    s_row[at] = lane;
+    s_src[at] = cont_lo;
+  }
+  if (mv_x) {
+    const int at = n_lo + __popc(b_x & ((1u << lane) - 1));
+    s_row[at] = xrow;
+    s_src[at] = xcont;
+  }
+  return n_lo + __popc(b_x);
+}
+
+// One panel's interchanges as a permutation: warp 0 composes them
+// (compose_pivots), then every warp moves whole columns.
 __global__ void __launch_bounds__(256) k_permute(XPermArgs a) {
   if (ld_info(a.d_info) != 0) return;
   __shared__ int s_row[2 * kGetf2Max], s_src[2 * kGetf2Max];
   __shared__ int s_cnt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
-    int cont_lo = lane, xrow = -1, xcont = -1, ne = 0;
-    const int mypiv = lane < a.npiv ? a.ipiv[a.k0 + lane] - a.base : lane;  // all pivots in one load
-    for (int k = 0; k < a.npiv; ++k) {
-      const int p = __shfl_sync(0xffffffffu, mypiv, k);
-      if (p == k) continue;
-      const int ck = __shfl_sync(0xffffffffu, cont_lo, k);
-      if (p < a.npiv) {
-        const int cp = __shfl_sync(0xffffffffu, cont_lo, p);
-        if (lane == k) cont_lo = cp;
-        if (lane == p) cont_lo = ck;
-      } else {
-        const unsigned mk = __ballot_sync(0xffffffffu, xrow == p);
-        int slot;
-        if (mk) {
-          slot = __ffs(mk) - 1;
-        } else {
-          slot = ne++;
-          if (lane == slot) {
-            xrow = p;
-            xcont = p;
-          }
-        }
-        const int cp = __shfl_sync(0xffffffffu, xcont, slot);
-        if (lane == k) cont_lo = cp;
-        if (lane == slot) xcont = ck;
-      }
-    }
-    // the moved rows, compacted
-    const bool mv_lo = lane < a.npiv && cont_lo != lane, mv_x = xrow >= 0 && xcont != xrow;
-    const unsigned b_lo = __ballot_sync(0xffffffffu, mv_lo), b_x = __ballot_sync(0xffffffffu, mv_x);
-    const int n_lo = __popc(b_lo);
-    if (mv_lo) {
-      const int at = __popc(b_lo & ((1u << lane) - 1));
-      s_row[at] = lane;
-      s_src[at] = cont_lo;
-    }
-    if (mv_x) {
-      const int at = n_lo + __popc(b_x & ((1u << lane) - 1));
-      s_row[at] = xrow;
-      s_src[at] = xcont;
-    }
-    if (lane == 0) s_cnt = n_lo + __popc(b_x);
+    const int cnt = compose_pivots(a.ipiv + a.k0, a.npiv, a.base, s_row, s_src);
+    if (lane == 0) s_cnt = cnt;
   }
   __syncthreads();
   const int cnt = s_cnt;
@@ -980,19 +988,43 @@ __global__ void __launch_bounds__(256) k_permute(XPermArgs a) {
 }
 
 // Row interchanges: for k = k0 .. k1-1 (in order) swap rows k and ipiv[k] - base
-// of the columns [0, ncols) of A (layout 0).  One thread per column.
-__global__ void k_laswp(XLaswpArgs a) {
+// of the columns [0, ncols) of A (layout 0).  The pivots in chunks of 32, each
+// composed into one permutation (compose_pivots, warp 0 of every CTA; the next
+// chunk's composition overlaps the moves of the current one: two buffers);
+// one warp per column moves the chunk's rows (two loads in flight per lane).
+__global__ void __launch_bounds__(256) k_laswp(XLaswpArgs a) {
   if (ld_info(a.d_info) != 0) return;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.ncols) return;
-  double* col = a.A + (int64_t)c * a.ld;
-  for (int k = a.k0; k < a.k1; ++k) {
-    const int p = a.ipiv[k] - a.base;
-    if (p != k) {
-      const double t = col[k];
-      col[k] = col[p];
-      col[p] = t;
+  __shared__ int s_row[2][2 * kGetf2Max], s_src[2][2 * kGetf2Max];
+  __shared__ int s_cnt[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nchunks = (a.k1 - a.k0 + 31) / 32;
+  if (warp == 0 && nchunks > 0) {
+    const int cnt = compose_pivots(a.ipiv + a.k0, min(32, a.k1 - a.k0), a.base + a.k0, s_row[0], s_src[0]);
+    if (lane == 0) s_cnt[0] = cnt;
+  }
+  __syncthreads();
+  const int wpb = blockDim.x >> 5;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int cur = ch & 1, k = a.k0 + 32 * ch;
+    if (warp == 0 && ch + 1 < nchunks) {  // compose the next chunk into the other buffer
+      const int kn = k + 32;
+      const int cnt = compose_pivots(a.ipiv + kn, min(32, a.k1 - kn), a.base + kn, s_row[cur ^ 1], s_src[cur ^ 1]);
+      if (lane == 0) s_cnt[cur ^ 1] = cnt;
     }
+    const int cnt = s_cnt[cur];
+    if (cnt > 0) {
+      const int r0 = lane < cnt ? k + s_row[cur][lane] : 0, q0 = lane < cnt ? k + s_src[cur][lane] : 0;
+      const int r1 = lane + 32 < cnt ? k + s_row[cur][lane + 32] : 0;
+      const int q1 = lane + 32 < cnt ? k + s_src[cur][lane + 32] : 0;
+      for (int col = blockIdx.x * wpb + warp; col < a.ncols; col += gridDim.x * wpb) {
+        double* c = a.A + (int64_t)col * a.ld;
+        const double v0 = lane < cnt ? c[q0] : 0.0, v1 = lane + 32 < cnt ? c[q1] : 0.0;
+        __syncwarp();
+        if (lane < cnt) c[r0] = v0;
+        if (lane + 32 < cnt) c[r1] = v1;
+      }
+    }
+    __syncthreads();  // moves of this chunk done (column order), next composition visible
   }
 }
 
@@ -1110,7 +1142,9 @@ cudaError_t launch_getf2(const XGetf2Args& a, int grid, cudaStream_t st) {
 
 cudaError_t launch_laswp(const XLaswpArgs& a, cudaStream_t st) {
   if (a.ncols <= 0 || a.k1 <= a.k0) return cudaSuccess;
-  k_laswp<<<(a.ncols + 127) / 128, 128, 0, st>>>(a);
+  int grid = (a.ncols + 7) / 8;
+  if (grid > 148 * 8) grid = 148 * 8;
+  k_laswp<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -1123,21 +1157,18 @@ cudaError_t getf2_clr_dispatch(int rows_per_cta, F&& f) {
   return cudaErrorInvalidValue;
 }
 
-int getf2_cluster_caps() {
-  static int csz[kMaxDevices] = {}, done[kMaxDevices] = {};
+// Largest supported cluster size <= want (16 non-portable, 8), 0 if none.
+int getf2_cluster_size(int want) {
+  static int ok[kMaxDevices][2] = {}, done[kMaxDevices] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDevices) return 0;
   if (!done[dev]) {
     done[dev] = 1;
-    // opt-in (RELAPACK_GETF2_CLUSTER=16|8): measured slower end to end than the
-    // cooperative grid kernel at n = 16384 (225 vs 208 ms, tools/experiments r3q)
-    const char* v = getenv("RELAPACK_GETF2_CLUSTER");
-    const int want = v ? atoi(v) : 0;
     for (auto k : {k_getf2_clr<256, 2, 32>, k_getf2_clr<512, 2, 16>, k_getf2_clr<512, 4, 8>})
       cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int c : {16, 8}) {
-      if (c > want) continue;
+    for (int i = 0; i < 2; ++i) {
+      const int c = i == 0 ? 16 : 8;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c);
       cfg.blockDim = dim3(512);
@@ -1149,14 +1180,21 @@ int getf2_cluster_caps() {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, k_getf2_clr<512, 2, 16>, &cfg) == cudaSuccess && nc > 0) {
-        csz[dev] = c;
-        break;
-      }
+      ok[dev][i] = cudaOccupancyMaxActiveClusters(&nc, k_getf2_clr<512, 2, 16>, &cfg) == cudaSuccess && nc > 0;
       cudaGetLastError();
     }
   }
-  return csz[dev];
+  if (want >= 16 && ok[dev][0]) return 16;
+  if (want >= 8 && ok[dev][1]) return 8;
+  return 0;
+}
+
+int getf2_cluster_caps() {
+  // opt-in (RELAPACK_GETF2_CLUSTER=16|8) for the plain recursion: measured
+  // slower end to end than the cooperative grid kernel at n = 16384 (225 vs
+  // 208 ms, tools/experiments r3q); the lookahead plan uses it by default
+  const char* v = getenv("RELAPACK_GETF2_CLUSTER");
+  return getf2_cluster_size(v ? atoi(v) : 0);
 }
 
 cudaError_t launch_getf2_cl(const XGetf2ClArgs& a, int csize, cudaStream_t st) {

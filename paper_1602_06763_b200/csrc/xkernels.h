@@ -113,6 +113,7 @@ cudaError_t launch_laswp(const XLaswpArgs& a, cudaStream_t st);
 // cluster size C (16 or 8; 0: no cluster can be scheduled); configures the
 // cluster panel kernels once per device
 int getf2_cluster_caps();
+int getf2_cluster_size(int want);
 cudaError_t launch_getf2_cl(const XGetf2ClArgs& a, int csize, cudaStream_t st);
 cudaError_t launch_permute(const XPermArgs& a, cudaStream_t st);
 cudaError_t configure_xkernels();

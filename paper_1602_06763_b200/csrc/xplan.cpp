@@ -169,7 +169,11 @@ static int cluster_leaf_width(const XParams& p, int m) {
   return std::min(cap, p.getrf_base);
 }
 
-void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, int n, int level) {
+namespace {
+// The recursion with the interchanges of a panel-only (cluster) leaf applied
+// at once to the columns [zlo, zhi) of the matrix outside the leaf
+// (xplan_getrf: the whole matrix; the lookahead plan: its window).
+void getrf_rec(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, int n, int level, int zlo, int zhi) {
   if (m <= 0 || n <= 0) return;
   const int mn = std::min(m, n);
   const int wcl = cluster_leaf_width(p, m);
@@ -193,8 +197,8 @@ void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m,
         XOp q;
         q.kind = XK_PERM;
         q.level = level;
-        q.c = side == 0 ? XView{0, r0, c0 + n, 0} : XView{0, r0, 0, 0};
-        q.n = side == 0 ? p.getrf_cols - (c0 + n) : c0;
+        q.c = side == 0 ? XView{0, r0, c0 + n, 0} : XView{0, r0, zlo, 0};
+        q.n = side == 0 ? zhi - (c0 + n) : c0 - zlo;
         q.m = npiv;
         q.k = c0;
         if (q.n > 0) ops.push_back(q);
@@ -212,11 +216,74 @@ void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m,
   // lower rows after the right recursion): nothing reads those rows of the
   // other columns in between, so the order does not matter.
   const int n1 = mn <= base ? mn : xsplit(mn, base);
-  xplan_getrf(ops, p, r0, c0, m, n1, level + 1);
+  getrf_rec(ops, p, r0, c0, m, n1, level + 1, zlo, zhi);
   const XView L11{0, r0, c0, 0}, A12{0, r0, c0 + n1, 0}, A21{0, r0 + n1, c0, 0}, A22{0, r0 + n1, c0 + n1, 0};
   xplan_tri(ops, p, kTriSolveLT, L11, tr(A12), n - n1, n1, 1.0, 1, level + 1);
   gemm(ops, A22, A21, tr(A12), m - n1, n - n1, n1, -1.0, 0, level + 1);
-  xplan_getrf(ops, p, r0 + n1, c0 + n1, m - n1, n - n1, level + 1);
+  getrf_rec(ops, p, r0 + n1, c0 + n1, m - n1, n - n1, level + 1, zlo, zhi);
+}
+
+XOp laswp(int c0, int ncols, int k0, int k1, int level) {
+  XOp q;
+  q.kind = XK_LASWP;
+  q.level = level;
+  q.c = XView{0, 0, c0, 0};
+  q.n = ncols;
+  q.m = k0;
+  q.k = k1;
+  return q;
+}
+
+// Lookahead recursion (xplan_getrf_la): S:367-375 with the two laswp calls
+// of each level kept where the recursion puts them (P1 on the right part
+// before its solve, P2 on the left part after the right recursion), and the
+// right part's laswp / solve / update issued as column pieces along the left
+// spine of the right recursion — its first window only waits for the first
+// piece, the later pieces (deferred) overlap the windows before them.
+void getrf_la(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, int n, int level) {
+  if (m <= 0 || n <= 0) return;
+  const int W = p.getrf_window, mn = std::min(m, n);
+  if (n <= W || mn <= W) {
+    getrf_rec(ops, p, r0, c0, m, n, level, c0, c0 + n);  // a window: eager interchanges inside it
+    return;
+  }
+  const int wcl = cluster_leaf_width(p, m);
+  const int base = wcl > 0 ? wcl : p.getrf_base;
+  const int n1 = xsplit(mn, base);
+  getrf_la(ops, p, r0, c0, m, n1, level + 1);
+  const int M = m - n1, wR = n - n1;
+  // piece bounds (offsets into the right part): the left spine of getrf_la(M, wR)
+  std::vector<int> cuts{wR};
+  for (int w = wR; w > W && std::min(M, w) > W;) {
+    const int wb = cluster_leaf_width(p, M), bb = wb > 0 ? wb : p.getrf_base;
+    w = xsplit(std::min(M, w), bb);
+    cuts.push_back(w);
+  }
+  cuts.push_back(0);
+  std::reverse(cuts.begin(), cuts.end());
+  const XView L11{0, r0, c0, 0}, A21{0, r0 + n1, c0, 0};
+  for (size_t i = 0; i + 1 < cuts.size(); ++i) {
+    const int a = cuts[i], w = cuts[i + 1] - a;
+    const size_t first = ops.size();
+    ops.push_back(laswp(c0 + n1 + a, w, c0, c0 + n1, level + 1));  // P1 on the piece
+    const XView A12{0, r0, c0 + n1 + a, 0}, A22{0, r0 + n1, c0 + n1 + a, 0};
+    xplan_tri(ops, p, kTriSolveLT, L11, tr(A12), w, n1, 1.0, 1, level + 1);
+    gemm(ops, A22, A21, tr(A12), M, w, n1, -1.0, 0, level + 1);
+    if (i > 0)
+      for (size_t q = first; q < ops.size(); ++q) ops[q].defer = 1;
+  }
+  getrf_la(ops, p, r0 + n1, c0 + n1, M, wR, level + 1);
+  if (mn > n1) ops.push_back(laswp(c0, n1, c0 + n1, c0 + mn, level + 1));  // P2 on the left part
+}
+
+}  // namespace
+
+void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, int n, int level) {
+  getrf_rec(ops, p, r0, c0, m, n, level, 0, p.getrf_cols);
+}
+
+void xplan_getrf_la(std::vector<XOp>& ops, const XParams& p, int m, int n) {
+  getrf_la(ops, p, 0, 0, m, n, 0);
 }
 
 // ------------------------------------------------------------------ dependencies

@@ -46,6 +46,7 @@ struct XOp {
   int unit = 0;   // TRI / TRTI2: unit diagonal
   int info_base = 0;
   double flops = 0.0;  // leading-term algorithmic flops
+  int defer = 0;       // 1: off the critical path (getrf lookahead pieces): low priority, capped grid
 };
 
 struct XParams {
@@ -57,6 +58,7 @@ struct XParams {
   // the cooperative grid kernel k_getf2)
   int getf2_cluster = 0;
   int getrf_cols = 0;   // columns of the whole matrix (the interchanges' extent)
+  int getrf_window = 256;  // lookahead plan: column windows factored with eager interchanges
 };
 
 // Recursive TRSM / TRMM on rows: B(m x k) := op(B, T) with T (k x k) lower,
@@ -74,6 +76,12 @@ void xplan_lauum(std::vector<XOp>& ops, const XParams& p, int off, int n, int le
 void xplan_potrs(std::vector<XOp>& ops, const XParams& p, int n, int nrhs);
 // Recursive getrf of the m x n block at (r0, c0) (pivots in buffer 2)
 void xplan_getrf(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, int n, int level);
+// The same recursion with lookahead (needs panel-only leaves: p.getf2_cluster
+// > 0 and every leaf within the cluster kernel's rows): each level's P1 laswp,
+// solve and update on the right part issued as column pieces along the left
+// spine of the right recursion (pieces after the first: XOp::defer), windows
+// of <= p.getrf_window columns factored with eager interchanges inside them.
+void xplan_getrf_la(std::vector<XOp>& ops, const XParams& p, int m, int n);
 
 // Footprint rectangles of an op in logical buffer coordinates and the
 // transitively reduced dependency lists they imply (earlier ops only).

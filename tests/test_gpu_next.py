@@ -300,6 +300,30 @@ def test_getrf_panel_variants(cluster):
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
+@pytest.mark.parametrize("window", ["64", "256"])
+def test_getrf_lookahead_variant(window):
+    """The lookahead getrf plan (RELAPACK_GETRF_LA=1: panel-only cluster
+    leaves, each level's P1 laswp / solve / update issued as column pieces,
+    deferred pieces serialized at low priority, P2 laswp after the right
+    recursion) against the oracle — identical pivots, same factor tolerances;
+    window 64 puts the lookahead pieces and the multi-chunk laswp into every
+    size here.  In a subprocess (knobs read per plan key)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = ("from tests.test_gpu_next import test_getrf, test_getrf_singular_and_identity\n"
+            "for mn in [(33, 33), (300, 300), (1031, 1031), (2048, 2048), (1500, 700), (700, 1500), (4096, 64),"
+            " (16384, 48)]:\n"
+            "    test_getrf(*mn)\n"
+            "test_getrf_singular_and_identity()\nprint('variant ok')\n")
+    env = dict(os.environ, RELAPACK_GETRF_LA="1", RELAPACK_GETRF_WINDOW=window)
+    r = subprocess.run([sys.executable, "-c", code], cwd=Path(__file__).resolve().parents[1], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 def test_tri_leaf_row_kernel_variant():
     """The triangular leaves on the row-per-thread kernel (RELAPACK_TRI_MMA=0)
     instead of the DMMA one: the same parity checks of every operation that
