@@ -444,6 +444,8 @@ int x_run(const std::string& key, const std::vector<XOp>& ops_in, const XBuffers
       const int rs = env_int_x("RELAPACK_GETRF_RESERVE", 16);
       p->defer_ctas = rs < 0 ? 0 : std::max(1, p->sms - std::max(p->cl_size, rs));
     }
+    for (size_t i = 0; i < p->ops.size(); ++i)
+      if (p->ops[i].after >= 0 && p->ops[i].after < (int)i) deps[i].push_back(p->ops[i].after);
     serialize_deferred(p->ops, deps);
     if ((e = setup_exec(*p, anc)) != cudaSuccess) return cuda_fail(e, "x workspace");
     if (graphs) {
@@ -652,6 +654,7 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
   if (la && cl > 0 && (*m + cl - 1) / cl <= kGetf2ClRows8) {
     p.getf2_cluster = cl;
     p.getrf_window = std::max(8, env_int_x("RELAPACK_GETRF_WINDOW", 256));
+    p.getrf_first_piece = env_int_x("RELAPACK_GETRF_P0FIRST", 0);
     xplan_getrf_la(ops, p, *m, *n);
   } else {
     p.getf2_cluster = getf2_cluster_caps();
@@ -667,7 +670,7 @@ void relapack_dgetrf(const int* m, const int* n, double* A, const int* lda, int*
   b.cl_size = p.getf2_cluster;
   const std::string key = "getrf m" + std::to_string(*m) + " n" + std::to_string(*n) + " ld" + std::to_string(*lda) +
                           " A" + ptr_key(A) + " P" + ptr_key(ipiv) + params_key(p) + " la" + std::to_string(la) +
-                          " w" + std::to_string(p.getrf_window) + " rs" +
+                          " w" + std::to_string(p.getrf_window) + " pf" + std::to_string(p.getrf_first_piece) + " rs" +
                           std::to_string(env_int_x("RELAPACK_GETRF_RESERVE", 16)) + " se" +
                           std::to_string(env_int_x("RELAPACK_GETRF_SERIAL", 1));
   int r = x_run(key, ops, b, true, false, current_stream_or(nullptr), info);

@@ -262,6 +262,7 @@ void getrf_la(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, in
   cuts.push_back(0);
   std::reverse(cuts.begin(), cuts.end());
   const XView L11{0, r0, c0, 0}, A21{0, r0 + n1, c0, 0};
+  int first_update = -1;
   for (size_t i = 0; i + 1 < cuts.size(); ++i) {
     const int a = cuts[i], w = cuts[i + 1] - a;
     const size_t first = ops.size();
@@ -269,8 +270,12 @@ void getrf_la(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, in
     const XView A12{0, r0, c0 + n1 + a, 0}, A22{0, r0 + n1, c0 + n1 + a, 0};
     xplan_tri(ops, p, kTriSolveLT, L11, tr(A12), w, n1, 1.0, 1, level + 1);
     gemm(ops, A22, A21, tr(A12), M, w, n1, -1.0, 0, level + 1);
+    if (i == 0 && ops.size() > first && ops.back().kind == XK_GEMM) first_update = (int)ops.size() - 1;
     if (i > 0)
-      for (size_t q = first; q < ops.size(); ++q) ops[q].defer = 1;
+      for (size_t q = first; q < ops.size(); ++q) {
+        ops[q].defer = 1;
+        if (ops[q].kind == XK_GEMM && p.getrf_first_piece) ops[q].after = first_update;
+      }
   }
   getrf_la(ops, p, r0 + n1, c0 + n1, M, wR, level + 1);
   if (mn > n1) ops.push_back(laswp(c0, n1, c0 + n1, c0 + mn, level + 1));  // P2 on the left part

@@ -47,6 +47,7 @@ struct XOp {
   int info_base = 0;
   double flops = 0.0;  // leading-term algorithmic flops
   int defer = 0;       // 1: off the critical path (getrf lookahead pieces): low priority, capped grid
+  int after = -1;      // >= 0: an extra dependency on that (earlier) op (getrf lookahead: the first piece's update)
 };
 
 struct XParams {
@@ -59,6 +60,7 @@ struct XParams {
   int getf2_cluster = 0;
   int getrf_cols = 0;   // columns of the whole matrix (the interchanges' extent)
   int getrf_window = 256;  // lookahead plan: column windows factored with eager interchanges
+  int getrf_first_piece = 0;  // lookahead plan: deferred updates of a level after its first piece's update
 };
 
 // Recursive TRSM / TRMM on rows: B(m x k) := op(B, T) with T (k x k) lower,
