@@ -507,12 +507,15 @@ XParams x_params() {
   if (v) p.tri_base = std::max(8, std::min(kTriMax, atoi(v)));
   v = getenv("RELAPACK_GETRF_BASE");
   if (v) p.getrf_base = std::max(1, std::min(kGetf2Max, atoi(v)));
+  p.potrs_cols = std::max(0, env_int_x("RELAPACK_POTRS_COLS", 0));
+  p.tri_rows = std::max(0, env_int_x("RELAPACK_TRI_ROWS", 0));
   return p;
 }
 
 std::string params_key(const XParams& p) {
-  char b[96];
-  snprintf(b, sizeof(b), " tb%d st%d gb%d cl%d", p.tri_base, p.split_tile, p.getrf_base, p.getf2_cluster);
+  char b[128];
+  snprintf(b, sizeof(b), " tb%d st%d gb%d cl%d pc%d tr%d", p.tri_base, p.split_tile, p.getrf_base, p.getf2_cluster,
+           p.potrs_cols, p.tri_rows);
   return b;
 }
 

@@ -48,6 +48,22 @@ int xsplit(int n, int T) {
   return s > 0 ? s : n / 2;
 }
 
+// xplan_tri on row panels of B: the rows of B(m x k) := op(B, T) do not depend
+// on one another, so each panel is its own chain of leaves and updates
+// (footprint-disjoint: the DAG runs one panel's leaves under another's GEMMs).
+void tri_panels(std::vector<XOp>& ops, const XParams& p, int rows, int mode, XView T, XView B, int m, int k,
+                double alpha, int unit, int level) {
+  if (rows <= 0 || m <= rows + rows / 2) {
+    xplan_tri(ops, p, mode, T, B, m, k, alpha, unit, level);
+    return;
+  }
+  const int np = (m + rows - 1) / rows;
+  for (int q = 0; q < np; ++q) {
+    const int r0 = (int)((int64_t)m * q / np / 8 * 8), r1 = q + 1 == np ? m : (int)((int64_t)m * (q + 1) / np / 8 * 8);
+    xplan_tri(ops, p, mode, T, sub(B, r0, 0), r1 - r0, k, alpha, unit, level);
+  }
+}
+
 }  // namespace
 
 void xplan_tri(std::vector<XOp>& ops, const XParams& p, int mode, XView T, XView B, int m, int k, double alpha,
@@ -115,8 +131,8 @@ void xplan_trtri(std::vector<XOp>& ops, const XParams& p, int off, int n, int un
   const int s = xsplit(n, p.split_tile), q = n - s;
   const XView A11{0, off, off, 0}, A21{0, off + s, off, 0}, A22{0, off + s, off + s, 0};
   xplan_trtri(ops, p, off, s, unit, level + 1);
-  xplan_tri(ops, p, kTriMulL, A11, A21, q, s, -1.0, unit, level + 1);
-  xplan_tri(ops, p, kTriSolveLT, A22, tr(A21), s, q, 1.0, unit, level + 1);
+  tri_panels(ops, p, p.tri_rows, kTriMulL, A11, A21, q, s, -1.0, unit, level + 1);
+  tri_panels(ops, p, p.tri_rows, kTriSolveLT, A22, tr(A21), s, q, 1.0, unit, level + 1);
   xplan_trtri(ops, p, off + s, q, unit, level + 1);
 }
 
@@ -149,14 +165,21 @@ void xplan_lauum(std::vector<XOp>& ops, const XParams& p, int off, int n, int le
   const XView A11{0, off, off, 0}, A21{0, off + s, off, 0}, A22{0, off + s, off + s, 0};
   xplan_lauum(ops, p, off, s, level + 1);
   gemm(ops, A11, tr(A21), tr(A21), s, s, q, 1.0, 1, level + 1);
-  xplan_tri(ops, p, kTriMulL, A22, tr(A21), s, q, 1.0, 0, level + 1);
+  tri_panels(ops, p, p.tri_rows, kTriMulL, A22, tr(A21), s, q, 1.0, 0, level + 1);
   xplan_lauum(ops, p, off + s, q, level + 1);
 }
 
 void xplan_potrs(std::vector<XOp>& ops, const XParams& p, int n, int nrhs) {
   const XView L{0, 0, 0, 0}, Bt{1, 0, 0, 1};
-  xplan_tri(ops, p, kTriSolveLT, L, Bt, nrhs, n, 1.0, 0, 1);  // L Y = B    <=> Y^T L^T = B^T
-  xplan_tri(ops, p, kTriSolveL, L, Bt, nrhs, n, 1.0, 0, 1);   // L^T X = Y  <=> X^T L = Y^T
+  // every column panel of B runs both solves on its own (a panel's second solve
+  // follows its first; nothing orders two panels)
+  const int cols = p.potrs_cols, np = cols > 0 && nrhs > cols + cols / 2 ? (nrhs + cols - 1) / cols : 1;
+  for (int q = 0; q < np; ++q) {
+    const int c0 = (int)((int64_t)nrhs * q / np / 8 * 8), c1 = q + 1 == np ? nrhs : (int)((int64_t)nrhs * (q + 1) / np / 8 * 8);
+    const XView Bq = sub(Bt, c0, 0);
+    xplan_tri(ops, p, kTriSolveLT, L, Bq, c1 - c0, n, 1.0, 0, 1);  // L Y = B    <=> Y^T L^T = B^T
+    xplan_tri(ops, p, kTriSolveL, L, Bq, c1 - c0, n, 1.0, 0, 1);   // L^T X = Y  <=> X^T L = Y^T
+  }
 }
 
 // Panel width of a getrf leaf with m rows on a cluster: the configured width,

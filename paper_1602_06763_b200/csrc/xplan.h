@@ -61,6 +61,11 @@ struct XParams {
   int getrf_cols = 0;   // columns of the whole matrix (the interchanges' extent)
   int getrf_window = 256;  // lookahead plan: column windows factored with eager interchanges
   int getrf_first_piece = 0;  // lookahead plan: deferred updates of a level after its first piece's update
+  // potrs: the right-hand sides in panels of this many columns, each panel its
+  // own pair of recursive solves (independent chains the DAG overlaps); 0: one panel
+  int potrs_cols = 0;
+  // trtri / lauum: the rows of a level's TRMM / TRSM operand in panels of this many rows (0: whole)
+  int tri_rows = 0;
 };
 
 // Recursive TRSM / TRMM on rows: B(m x k) := op(B, T) with T (k x k) lower,
