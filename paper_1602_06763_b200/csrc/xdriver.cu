@@ -507,7 +507,7 @@ XParams x_params() {
   if (v) p.tri_base = std::max(8, std::min(kTriMax, atoi(v)));
   v = getenv("RELAPACK_GETRF_BASE");
   if (v) p.getrf_base = std::max(1, std::min(kGetf2Max, atoi(v)));
-  p.potrs_cols = std::max(0, env_int_x("RELAPACK_POTRS_COLS", 0));
+  p.potrs_cols = std::max(0, env_int_x("RELAPACK_POTRS_COLS", p.potrs_cols));
   p.tri_rows = std::max(0, env_int_x("RELAPACK_TRI_ROWS", 0));
   return p;
 }
@@ -737,6 +737,8 @@ int relapack_xplan_count(int op, int n, int nb, int* kinds_out, int max_kinds, d
   // 2 lauum, 3 potri, 4 potrs (nrhs = nb), 5 getrf (square), 6 getrf with lookahead (window nb)
   if (n < 0) return -1;
   XParams p;
+  p.potrs_cols = x_params().potrs_cols;  // the panel knobs as the executor reads them
+  p.tri_rows = x_params().tri_rows;
   std::vector<XOp> ops;
   switch (op) {
     case 0: xplan_trtri(ops, p, 0, n, 0, 0); break;

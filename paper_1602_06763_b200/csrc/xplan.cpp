@@ -241,7 +241,7 @@ void getrf_rec(std::vector<XOp>& ops, const XParams& p, int r0, int c0, int m, i
   const int n1 = mn <= base ? mn : xsplit(mn, base);
   getrf_rec(ops, p, r0, c0, m, n1, level + 1, zlo, zhi);
   const XView L11{0, r0, c0, 0}, A12{0, r0, c0 + n1, 0}, A21{0, r0 + n1, c0, 0}, A22{0, r0 + n1, c0 + n1, 0};
-  xplan_tri(ops, p, kTriSolveLT, L11, tr(A12), n - n1, n1, 1.0, 1, level + 1);
+  tri_panels(ops, p, p.tri_rows, kTriSolveLT, L11, tr(A12), n - n1, n1, 1.0, 1, level + 1);
   gemm(ops, A22, A21, tr(A12), m - n1, n - n1, n1, -1.0, 0, level + 1);
   getrf_rec(ops, p, r0 + n1, c0 + n1, m - n1, n - n1, level + 1, zlo, zhi);
 }

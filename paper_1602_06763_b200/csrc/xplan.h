@@ -63,8 +63,10 @@ struct XParams {
   int getrf_first_piece = 0;  // lookahead plan: deferred updates of a level after its first piece's update
   // potrs: the right-hand sides in panels of this many columns, each panel its
   // own pair of recursive solves (independent chains the DAG overlaps); 0: one panel
-  int potrs_cols = 0;
-  // trtri / lauum: the rows of a level's TRMM / TRSM operand in panels of this many rows (0: whole)
+  // (measured r7a, n = 16384, nrhs = 1024: 28.5 ms whole, 25.0 / 24.6 / 25.7 ms at 128 / 256 / 512)
+  int potrs_cols = 256;
+  // trtri / lauum / getrf: the rows of a level's TRMM / TRSM operand in panels of this many rows (0: whole;
+  // measured r7a: trtri 54.6 -> 59.6 / 56.1 / 54.4 ms at 512 / 1024 / 2048, lauum 49.0 -> 48.6 at 2048 — off)
   int tri_rows = 0;
 };
 

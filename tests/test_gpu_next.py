@@ -347,6 +347,34 @@ def test_tri_leaf_row_kernel_variant():
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
+@pytest.mark.parametrize("cols,rows", [("16", "64"), ("48", "200")])
+def test_panel_split_variant(cols, rows):
+    """potrs with the right-hand sides in column panels (RELAPACK_POTRS_COLS:
+    each panel its own pair of recursive solves) and trtri / lauum / potri with
+    the rows of each level's TRMM / TRSM operand in panels (RELAPACK_TRI_ROWS):
+    the same parity checks, incl. the untouched other triangle, with panel
+    sizes small enough that every size here splits (ragged last panels, panel
+    bounds rounded to 8).  In a subprocess (knobs are part of the plan key)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = ("import tests.test_gpu_next as t\n"
+            "for u in 'LU':\n"
+            "    for n, r in [(65, 7), (300, 100), (1031, 130), (2048, 301)]:\n"
+            "        t.test_potrs(n, r, u)\n"
+            "    for n in (65, 300, 1031, 2048):\n"
+            "        t.test_trtri(n, u); t.test_lauum(n, u)\n"
+            "    t.test_potri(1500, u); t.test_trtri_unit_and_integer(u)\n"
+            "t.test_trtri_blocked(1031, 128)\n"
+            "print('variant ok')\n")
+    env = dict(os.environ, RELAPACK_POTRS_COLS=cols, RELAPACK_TRI_ROWS=rows)
+    r = subprocess.run([sys.executable, "-c", code], cwd=Path(__file__).resolve().parents[1], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 # ------------------------------------------------------------------ N2 blocked dpotrf
 @pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("nb", [64, 128, 256])

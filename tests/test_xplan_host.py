@@ -30,3 +30,21 @@ def test_getrf_lookahead_plan_flops(n, window):
 def test_getrf_lookahead_plan_bounds():
     with pytest.raises(ValueError):
         rl.xplan_count("getrf_la", 16 * 2048 + 16)  # beyond the 16-CTA cluster panel's rows
+
+
+@pytest.mark.parametrize("op,n,nb", [("potrs", 4096, 1000), ("potrs", 1031, 130), ("trtri", 4096, 0),
+                                     ("lauum", 1031, 0), ("potri", 2048, 0)])
+def test_panel_split_plan_flops(op, n, nb, monkeypatch):
+    """Right-hand-side panels (potrs) / operand-row panels (trtri, lauum) are
+    the same recursion on independent rows: the plan's leading-term flops do not
+    change (potrs: 2 n^2 nrhs; trtri, lauum: n^3 / 3 each) and the launch count grows."""
+    monkeypatch.setenv("RELAPACK_POTRS_COLS", "0")
+    monkeypatch.setenv("RELAPACK_TRI_ROWS", "0")
+    c0, _, f0 = rl.xplan_count(op, n, nb)
+    monkeypatch.setenv("RELAPACK_POTRS_COLS", "64")
+    monkeypatch.setenv("RELAPACK_TRI_ROWS", "128")
+    c1, _, f1 = rl.xplan_count(op, n, nb)
+    assert f1 == pytest.approx(f0, rel=1e-12)
+    closed = {"potrs": 2.0 * n * n * nb, "trtri": n ** 3 / 3.0, "lauum": n ** 3 / 3.0, "potri": 2 * n ** 3 / 3.0}[op]
+    assert f0 == pytest.approx(closed, rel=1e-12)
+    assert c1 > c0
