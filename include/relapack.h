@@ -286,7 +286,9 @@ RELAPACK_API int relapack_trace_read(int max, double* out);
  *   relapack_dpotrf, same uplo) is in A: dtrtri then dlauum.  info = k > 0:
  *   the factor's k-th diagonal entry is zero.
  * relapack_dpotrs — B := A^{-1} B with the Cholesky factor in A: two
- *   recursive triangular solves (L Y = B, L^T X = Y).  B is a DEVICE n x nrhs
+ *   recursive triangular solves (L Y = B, L^T X = Y), run per panel of 256
+ *   right-hand sides (independent columns; RELAPACK_POTRS_COLS, 0 = one
+ *   panel).  B is a DEVICE n x nrhs
  *   column-major matrix (ldb >= max(1, n)).  Arguments: 1 uplo, 2 n, 3 nrhs,
  *   4 A, 5 lda, 6 B, 7 ldb.
  * relapack_dgetrf — P A = L U with partial pivoting (LAPACK dgetrf; recursive
