@@ -509,13 +509,14 @@ XParams x_params() {
   if (v) p.getrf_base = std::max(1, std::min(kGetf2Max, atoi(v)));
   p.potrs_cols = std::max(0, env_int_x("RELAPACK_POTRS_COLS", p.potrs_cols));
   p.tri_rows = std::max(0, env_int_x("RELAPACK_TRI_ROWS", 0));
+  p.trtri_order = env_int_x("RELAPACK_TRTRI_ORDER", p.trtri_order) == 1 ? 1 : 0;
   return p;
 }
 
 std::string params_key(const XParams& p) {
   char b[128];
-  snprintf(b, sizeof(b), " tb%d st%d gb%d cl%d pc%d tr%d", p.tri_base, p.split_tile, p.getrf_base, p.getf2_cluster,
-           p.potrs_cols, p.tri_rows);
+  snprintf(b, sizeof(b), " tb%d st%d gb%d cl%d pc%d tr%d to%d", p.tri_base, p.split_tile, p.getrf_base,
+           p.getf2_cluster, p.potrs_cols, p.tri_rows, p.trtri_order);
   return b;
 }
 
@@ -739,6 +740,7 @@ int relapack_xplan_count(int op, int n, int nb, int* kinds_out, int max_kinds, d
   XParams p;
   p.potrs_cols = x_params().potrs_cols;  // the panel knobs as the executor reads them
   p.tri_rows = x_params().tri_rows;
+  p.trtri_order = x_params().trtri_order;
   std::vector<XOp> ops;
   switch (op) {
     case 0: xplan_trtri(ops, p, 0, n, 0, 0); break;

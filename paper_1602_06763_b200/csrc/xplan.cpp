@@ -130,6 +130,16 @@ void xplan_trtri(std::vector<XOp>& ops, const XParams& p, int off, int n, int un
   // the trmm so the solve runs with alpha = 1
   const int s = xsplit(n, p.split_tile), q = n - s;
   const XView A11{0, off, off, 0}, A21{0, off + s, off, 0}, A22{0, off + s, off + s, 0};
+  if (p.trtri_order == 1) {
+    // -A_BR^{-1} A_BL A_TL^{-1} with the solve first: A_BL := A_BR^{-1} A_BL needs only the original
+    // A_BR, so trtri(A_TL) and [solve; trtri(A_BR)] share no footprint and run side by side; the trmm
+    // with the inverted A_TL closes the level (same two BLAS-3 kinds as the paper's form)
+    tri_panels(ops, p, p.tri_rows, kTriSolveLT, A22, tr(A21), s, q, 1.0, unit, level + 1);
+    xplan_trtri(ops, p, off, s, unit, level + 1);
+    xplan_trtri(ops, p, off + s, q, unit, level + 1);
+    tri_panels(ops, p, p.tri_rows, kTriMulL, A11, A21, q, s, -1.0, unit, level + 1);
+    return;
+  }
   xplan_trtri(ops, p, off, s, unit, level + 1);
   tri_panels(ops, p, p.tri_rows, kTriMulL, A11, A21, q, s, -1.0, unit, level + 1);
   tri_panels(ops, p, p.tri_rows, kTriSolveLT, A22, tr(A21), s, q, 1.0, unit, level + 1);

@@ -65,6 +65,9 @@ struct XParams {
   // own pair of recursive solves (independent chains the DAG overlaps); 0: one panel
   // (measured r7a, n = 16384, nrhs = 1024: 28.5 ms whole, 25.0 / 24.6 / 25.7 ms at 128 / 256 / 512)
   int potrs_cols = 256;
+  // trtri: 0 = the paper's order (trtri(A_TL); trmm; trsm; trtri(A_BR): one chain); 1 = the solve with the
+  // original A_BR first, then both recursive calls (independent in the DAG), then the trmm with A_TL^{-1}
+  int trtri_order = 0;
   // trtri / lauum / getrf: the rows of a level's TRMM / TRSM operand in panels of this many rows (0: whole;
   // measured r7a: trtri 54.6 -> 59.6 / 56.1 / 54.4 ms at 512 / 1024 / 2048, lauum 49.0 -> 48.6 at 2048 — off)
   int tri_rows = 0;

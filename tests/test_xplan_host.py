@@ -48,3 +48,14 @@ def test_panel_split_plan_flops(op, n, nb, monkeypatch):
     closed = {"potrs": 2.0 * n * n * nb, "trtri": n ** 3 / 3.0, "lauum": n ** 3 / 3.0, "potri": 2 * n ** 3 / 3.0}[op]
     assert f0 == pytest.approx(closed, rel=1e-12)
     assert c1 > c0
+
+
+@pytest.mark.parametrize("n", [65, 1031, 4096])
+def test_trtri_solve_first_plan(n, monkeypatch):
+    """RELAPACK_TRTRI_ORDER=1 reorders a level's four steps; the launches and their flops are the same multiset."""
+    monkeypatch.setenv("RELAPACK_TRTRI_ORDER", "0")
+    c0, k0, f0 = rl.xplan_count("trtri", n)
+    monkeypatch.setenv("RELAPACK_TRTRI_ORDER", "1")
+    c1, k1, f1 = rl.xplan_count("trtri", n)
+    assert c1 == c0 and sorted(k1) == sorted(k0) and f1 == pytest.approx(f0, rel=1e-12)
+    assert k1 != k0 or n <= 64
