@@ -29,6 +29,19 @@ import time
 # would put a non-JSON line before the one JSON line rank 0 prints: route NCCL's
 # debug output to a file unless the caller chose one
 os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/relapack_nccl_debug.%h.%p.log")
+# ... and, because a library may still write to file descriptor 1 (NCCL does when
+# it cannot open that file), keep the real stdout for the JSON line alone: fd 1
+# points at stderr for the rest of the process, emit() writes the line to the
+# saved descriptor.
+sys.stdout.flush()
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def emit(obj):
+    _JSON_OUT.write(json.dumps(obj) + "\n")
+    _JSON_OUT.flush()
+
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -311,7 +324,7 @@ def main():
         import numpy as np
 
         out["cpu_baseline"] = cpu_oracle_sample(np.asfortranarray(A_host), n, uplo)
-    print(json.dumps(out))
+    emit(out)
     return 0
 
 
@@ -619,7 +632,7 @@ def run_batch(args, rank, world, dev):
                 if e2e_ms else None),
         "info_parity": "per-matrix info == closed form (k+1 for the 1% negated diagonals)",
     }
-    print(json.dumps(out))
+    emit(out)
     return 0
 
 
@@ -747,7 +760,7 @@ def run_next(args, rank, world, local_rank):
     if not args.no_cpu_baseline and rank == 0:
         out["cpu_baseline"] = next_cpu_baseline(op, n, r, args.seed)
     if rank == 0:
-        print(json.dumps(out))
+        emit(out)
     return 0
 
 
@@ -824,7 +837,7 @@ def run_next_reference(args, rank, world, op, n, r, flops_fn, desc):
            "dtype": "f64", "data": "synthetic (seeded Philox)", "config": {"workload": f"{desc}, n={n}", "n": n},
            "cpu_baseline": dict(base, value=round(val, 3)),
            "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    emit(out)
     return 0
 
 
@@ -924,7 +937,7 @@ def run_dist(args, rank, world, dev, n, uplo, dist):
                  "api": "relapack_dpotrf_dist; every rank's replica copied from pinned host memory inside the "
                         "timed region, the info word read back"} if e2e_ms else None),
     }
-    print(json.dumps(out))
+    emit(out)
     return 0
 
 
@@ -1009,7 +1022,7 @@ def run_reference(args, rank, n, uplo, dist, cfg_idx, world):
                          "sample": sample},
         "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out))
+    emit(out)
     return 0
 
 
