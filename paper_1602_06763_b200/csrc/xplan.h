@@ -67,7 +67,8 @@ struct XParams {
   int potrs_cols = 256;
   // trtri: 0 = the paper's order (trtri(A_TL); trmm; trsm; trtri(A_BR): one chain); 1 = the solve with the
   // original A_BR first, then both recursive calls (independent in the DAG), then the trmm with A_TL^{-1}
-  int trtri_order = 0;
+  // (measured r7c, n = 16384: 54.6 -> 50.1 ms; DESIGN R16b)
+  int trtri_order = 1;
   // trtri / lauum / getrf: the rows of a level's TRMM / TRSM operand in panels of this many rows (0: whole;
   // measured r7a: trtri 54.6 -> 59.6 / 56.1 / 54.4 ms at 512 / 1024 / 2048, lauum 49.0 -> 48.6 at 2048 — off)
   int tri_rows = 0;

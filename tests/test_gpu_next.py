@@ -375,12 +375,15 @@ def test_panel_split_variant(cols, rows):
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
-def test_trtri_solve_first_variant():
-    """trtri with the level's solve first (RELAPACK_TRTRI_ORDER=1: A_BL :=
-    A_BR^{-1} A_BL with the original A_BR, both recursive calls side by side in
-    the DAG, then A_BL := -A_BL A_TL^{-1}): the same inverse up to rounding
-    order — the same parity checks against the oracle (which keeps the paper's
-    order), the exact integer / unit cases, singular info, potri."""
+@pytest.mark.parametrize("order", ["0", "1"])
+def test_trtri_order_variant(order):
+    """trtri in the paper's step order (RELAPACK_TRTRI_ORDER=0: trtri(A_TL),
+    trmm, trsm, trtri(A_BR) — one chain) and with the level's solve first (1,
+    the default: A_BL := A_BR^{-1} A_BL with the original A_BR, both recursive
+    calls side by side in the DAG, then A_BL := -A_BL A_TL^{-1}): the same
+    inverse up to rounding order — the same parity checks against the oracle
+    (which keeps the paper's order), the exact integer / unit cases, singular
+    info, potri.  In a subprocess with the knob set explicitly."""
     import os
     import subprocess
     import sys
@@ -393,7 +396,7 @@ def test_trtri_solve_first_variant():
             "    t.test_potri(1500, u); t.test_trtri_unit_and_integer(u)\n"
             "t.test_trtri_singular(); t.test_potri_after_potrf_on_gpu()\n"
             "print('variant ok')\n")
-    env = dict(os.environ, RELAPACK_TRTRI_ORDER="1")
+    env = dict(os.environ, RELAPACK_TRTRI_ORDER=order)
     r = subprocess.run([sys.executable, "-c", code], cwd=Path(__file__).resolve().parents[1], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
