@@ -271,7 +271,10 @@ RELAPACK_API int relapack_trace_read(int max, double* out);
  *   running example; recursive algorithm: invert A_TL,
  *   A_BL := -A_BL A_TL^{-1} (trmm) and A_BL := A_BR^{-1} A_BL (trsm, the
  *   stable form), invert A_BR; crossover to an unblocked in-SM
- *   kernel at n <= 64).  diag 'N'/'U' (unit: the diagonal is neither read nor
+ *   kernel at n <= 64).  The default plan issues a level's steps as solve
+ *   (with the original A_BR), both inversions, trmm — the same product
+ *   -A_BR^{-1} A_BL A_TL^{-1}, the two inversions independent of one another
+ *   (R16b; RELAPACK_TRTRI_ORDER=0 keeps the paper's order).  diag 'N'/'U' (unit: the diagonal is neither read nor
  *   written).  Arguments: 1 uplo, 2 diag, 3 n, 4 A, 5 lda.  info = k > 0:
  *   A(k,k) == 0, A is not modified (checked first, as LAPACK).
  * relapack_dtrtri_blocked — the blocked algorithm of P:384-409 / S:287-296
